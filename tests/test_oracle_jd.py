@@ -1,0 +1,138 @@
+"""Pins for oracle.jd_full: constraints, stationarity, Pythagoras, Proposition 1, Theorem 1 (with
+the corrected lower bound), the Corollary, Eckart-Young, monotonicity, and printed values."""
+import numpy as np
+import pytest
+
+from oracle import jd_full, jd_objective, mean_relative_error, svd_truncate
+from workloads import gen_loras
+
+
+def _L(Bs, As):
+    return np.stack([(B @ A).ravel() for B, A in zip(Bs, As)], axis=1)
+
+
+@pytest.mark.parametrize("kind", ["random", "trained_like", "exact_span"])
+def test_orthonormal_stationary_pythagoras(kind):
+    Bs, As, _ = gen_loras(kind, 30, 24, 6, 3, 11, r_span=10, n_families=2)
+    res = jd_full(Bs, As, 5)
+    U, V, S = res["U"], res["V"], res["sigma"]
+    np.testing.assert_allclose(U.T @ U, np.eye(5), atol=1e-12)          # Eq. 2 constraint
+    np.testing.assert_allclose(V.T @ V, np.eye(5), atol=1e-12)
+    for B, A, Si in zip(Bs, As, S):                                       # dObj/dSigma_i = 0
+        np.testing.assert_allclose(U.T @ (U @ Si @ V.T - B @ A) @ V, 0, atol=1e-12)
+    direct = jd_objective(Bs, As, U, V, S)                                # Pythagoras
+    assert res["objective"] == pytest.approx(direct, rel=1e-9, abs=1e-12)
+
+
+def test_proposition1_lossless_iff_r_ge_rtilde():
+    """Prop. 1: exact at r = r~, nonzero error below."""
+    Bs, As, _ = gen_loras("exact_span", 40, 32, 5, 2, 3, r_span=6)
+    tot = sum(np.sum((B @ A) ** 2) for B, A in zip(Bs, As))
+    lossless = jd_full(Bs, As, 6)
+    assert jd_objective(Bs, As, lossless["U"], lossless["V"], lossless["sigma"]) < 1e-24 * tot
+    lossy = jd_full(Bs, As, 5)
+    assert jd_objective(Bs, As, lossy["U"], lossy["V"], lossy["sigma"]) > 1e-3 * tot
+    # generic (random) LoRAs: r~ = sum r_i = 8 (config-1 shape: 4 LoRAs of rank 2)
+    Bs, As, _ = gen_loras("random", 64, 64, 4, 2, 5)
+    assert jd_full(Bs, As, 8)["objective"] < 1e-20
+    assert jd_full(Bs, As, 4)["objective"] > 1e-2
+
+
+def test_app_h_zero_error_at_r256_with_10_loras():
+    """App H table: 10 LoRAs of rank 16 at r = 256 reconstruct with error 0.00, as
+    Prop. 1 predicts since sum r_i = 160 <= 256."""
+    Bs, As, _ = gen_loras("random", 320, 300, 10, 16, 9)
+    res = jd_full(Bs, As, 256, method="span")
+    assert mean_relative_error(Bs, As, res["U"], res["V"], res["sigma"]) < 1e-10
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_monotone_per_half_step(seed):
+    """Each U and V step cannot decrease sum ||Sigma_i||^2 (App A.1 "decreases the objective in
+    each step")."""
+    Bs, As, _ = gen_loras("random", 25, 20, 7, 3, seed)
+    tr = np.array(jd_full(Bs, As, 4)["captured_trace"])
+    assert np.all(np.diff(tr) >= -1e-12 * tr[-1])
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_monotone_in_r(seed):
+    Bs, As, _ = gen_loras("trained_like", 30, 28, 8, 4, seed, n_families=3)
+    objs = [jd_full(Bs, As, r)["objective"] for r in range(1, 13)]
+    assert np.all(np.diff(objs) <= 1e-10)
+
+
+@pytest.mark.parametrize("r", [1, 3, 5])
+def test_single_lora_is_truncated_svd(r):
+    """k = n (one LoRA per cluster) reduces JD to an SVD by Eckart-Young (Eq. 4)."""
+    Bs, As, _ = gen_loras("random", 20, 18, 1, 8, 4)
+    res = jd_full(Bs, As, r, normalize=False)
+    U, S, V = svd_truncate(Bs[0], As[0], r)
+    np.testing.assert_allclose(res["U"] @ res["sigma"][0] @ res["V"].T, U @ S @ V.T, atol=1e-10)
+    sv = np.linalg.svd(Bs[0] @ As[0], compute_uv=False)
+    assert res["objective"] == pytest.approx(np.sum(sv[r:] ** 2), rel=1e-9, abs=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_theorem1_sandwich_corrected(seed):
+    """Theorem 1.  Upper bound: sum ||Sigma_i||^2 <= sum_{j<=min(r^2,n)} sigma_j(L)^2.
+    Lower bound as CORRECTED (reading R7): (1/n) sum_{j<=r} sigmabar_j^2 <= sum||Sigma_i||^2;
+    the printed bound drops the 1/n of Cauchy-Schwarz in the proof's "Jensen" step."""
+    g = np.random.default_rng(seed)
+    n, r = int(g.integers(2, 9)), int(g.integers(1, 5))
+    Bs, As, _ = gen_loras("random", 16, 14, n, 2, 50 + seed)
+    res = jd_full(Bs, As, r, normalize=False, iters=30)
+    cap = np.sum(res["sigma"] ** 2)
+    sL = np.linalg.svd(_L(Bs, As), compute_uv=False)
+    sbar = np.linalg.svd(sum(B @ A for B, A in zip(Bs, As)), compute_uv=False)
+    assert cap <= np.sum(sL[:min(r * r, n)] ** 2) * (1 + 1e-12)
+    assert np.sum(sbar[:r] ** 2) / n <= cap * (1 + 1e-12)
+
+
+def test_theorem1_printed_lower_bound_counterexample():
+    """n identical adapters: the printed lower bound sum_{j<=r} sigmabar_j^2 equals n times the
+    achievable optimum, so it cannot hold (why the corrected 1/n form is used)."""
+    Bs, As, _ = gen_loras("random", 12, 10, 1, 3, 2)
+    Bs, As = Bs * 3, As * 3
+    res = jd_full(Bs, As, 1, normalize=False)
+    cap = np.sum(res["sigma"] ** 2)
+    sbar = np.linalg.svd(3 * (Bs[0] @ As[0]), compute_uv=False)
+    assert np.sum(sbar[:1] ** 2) == pytest.approx(3 * cap, rel=1e-9)
+
+
+@pytest.mark.parametrize("n,r", [(32, 3), (20, 2), (9, 4), (6, 3)])
+def test_corollary_orthogonal_unit_loras(n, r):
+    """Corollary, inequality read as 1 - min(r^2/n, 1) <= err <= 1 - 1/n (reading R3);
+    r >= min_i rank = 1 makes the upper side hold (reading R8)."""
+    Bs, As, _ = gen_loras("orthogonal", 40, 40, n, 1, n + r)
+    res = jd_full(Bs, As, r)
+    err = jd_objective(Bs, As, res["U"], res["V"], res["sigma"]) / n
+    assert 1 - min(r * r / n, 1) - 1e-12 <= err <= 1 - 1 / n + 1e-12
+    # this instance hits exactly r of the n unit LoRAs: error 1 - r/n
+    assert err == pytest.approx(1 - r / n, abs=1e-9)
+
+
+def test_span_and_direct_agree():
+    Bs, As, _ = gen_loras("trained_like", 60, 50, 7, 3, 21, n_families=2)
+    a = jd_full(Bs, As, 6, method="direct")
+    b = jd_full(Bs, As, 6, method="span")
+    assert a["objective"] == pytest.approx(b["objective"], rel=1e-9)
+    np.testing.assert_allclose(a["U"] @ a["U"].T, b["U"] @ b["U"].T, atol=1e-8)
+    np.testing.assert_allclose(a["V"] @ a["V"].T, b["V"] @ b["V"].T, atol=1e-8)
+
+
+def test_structured_reconstructs_better_than_random():
+    """App H property only: shared structure is retained, random is not.
+    The printed random-LoRA values are parity-unpinned (distribution unknown, reading R10)."""
+    St, At, _ = gen_loras("trained_like", 64, 64, 20, 4, 1, n_families=2, noise=0.3)
+    Sr, Ar, _ = gen_loras("random", 64, 64, 20, 4, 1)
+    et = jd_full(St, At, 8)
+    er = jd_full(Sr, Ar, 8)
+    assert (mean_relative_error(St, At, et["U"], et["V"], et["sigma"])
+            < mean_relative_error(Sr, Ar, er["U"], er["V"], er["sigma"]))
+
+
+def test_convergence_criterion_stops_early():
+    Bs, As, _ = gen_loras("trained_like", 30, 30, 6, 2, 3, n_families=1, noise=0.05)
+    res = jd_full(Bs, As, 4, iters=50, tol=1e-3)
+    assert 1 <= res["iters"] < 50
