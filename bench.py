@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""bench.py -- batched compressed-LoRA apply ("Compress then Serve", arXiv 2407.00066) on B200.
+
+One step = one pass of the whole hot path over one synthetic batch: cts_segment (all 224 cluster
+maps in one launch) + cts_apply for the 224 Mistral-7B projections (32 layers x q,k,v,o,gate,up,
+down), each apply = shrink+Sigma kernel + expand+residual kernel, replayed as one CUDA graph.
+
+  python bench.py [--config decode|prefill|q_proj|multi] [--gpus N --steps K --warmup W]
+  python bench.py --impl reference ...     # the fp64 CPU oracle as the reference arm
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N: data-parallel request sharding, each rank
+holds a replicated bank and its own token stream (seed 1+rank); weak scaling; no collective on the
+data path, only the timing barrier and a max-over-ranks reduction.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads.gen import MISTRAL_LAYERS, MISTRAL_MODULES  # noqa: E402
+
+CONFIGS = {
+    # BASELINE.json configs[2]: the metric's "1000 adapters" decode configuration (default)
+    "decode": dict(workload="cfg3_decode", N=1000, C=25, r=16, T=1024, prefill=False, layers=MISTRAL_LAYERS,
+                   modules=MISTRAL_MODULES, steps=300, warmup=10),
+    # configs[3]: prefill, same bank, 16k tokens per batch
+    "prefill": dict(workload="cfg4_prefill", N=1000, C=25, r=16, T=16384, prefill=True, layers=MISTRAL_LAYERS,
+                    modules=MISTRAL_MODULES, steps=30, warmup=3),
+    # configs[1]: single q_proj, 64 LoRAs, JD without clustering r=64, decode 256
+    "q_proj": dict(workload="cfg2_q_proj", N=64, C=1, r=64, T=256, prefill=False, layers=1,
+                   modules=(("q", 4096, 4096),), steps=2000, warmup=20),
+    # configs[4], per GPU: 8192 adapters in 128 clusters, replicated bank
+    "multi": dict(workload="cfg5_multi_decode", N=8192, C=128, r=16, T=1024, prefill=False,
+                  layers=MISTRAL_LAYERS, modules=MISTRAL_MODULES, steps=200, warmup=10),
+}
+SCALE = 2.0          # LoRA alpha / r = 32 / 16 (App C; reading R11)
+
+
+# ----------------------------------------------------------------------------- helpers (host only)
+def module_list(cfg):
+    return [(layer, name, di, do) for layer in range(cfg["layers"]) for (name, di, do) in cfg["modules"]]
+
+
+def x_slot(name):
+    """q/k/v share the attention input, gate/up the MLP input (one x buffer per role per layer)."""
+    return {"q": "attn", "k": "attn", "v": "attn", "o": "o", "gate": "mlp", "up": "mlp", "down": "down"}[name]
+
+
+def algorithmic_bytes(tokens, cluster_maps, mods, r):
+    """Per-module algorithmic bytes: shrink = x rows + touched in_basis + touched
+    Sigma + ids; expand = y read + write + touched out_basis + perm.  Counted from the batch."""
+    tokens = np.asarray(tokens)
+    bound = tokens >= 0
+    Tb = int(bound.sum())
+    T = len(tokens)
+    adapters = np.unique(tokens[bound])
+    shrink, expand = [], []
+    for (_, _, di, do), cmap in zip(mods, cluster_maps):
+        ct = len(np.unique(cmap[adapters])) if adapters.size else 0
+        shrink.append(Tb * di * 2 + ct * di * r * 2 + adapters.size * r * r * 2 + 4 * T)
+        expand.append(2 * Tb * do * 2 + ct * do * r * 2 + 4 * T)
+    return np.array(shrink, dtype=np.float64), np.array(expand, dtype=np.float64)
+
+
+def aggregate(values_ms, units_per_rank, world):
+    """Whole-job throughput: units all ranks processed / the slowest rank's time (weak scaling)."""
+    t = max(values_ms)
+    return units_per_rank * world / (t / 1e3), t
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload, kernel):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        e = d[workload][kernel]
+        return float(e["dram_bytes_per_launch"]), float(e["algorithmic_bytes_per_launch"])
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """Polls NVML SM clock + clock-event reasons every 20 ms while the timed region runs."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+               0x2: "applications_clocks_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def result(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle leg
+class OracleLayer:
+    """One full layer (7 modules) of the workload as fp64 images of bf16 inputs, for the oracle."""
+
+    def __init__(self, cfg, seed_rank=0):
+        import torch
+        from workloads.bf16 import bf16_to_f64
+        from workloads.gen_torch import direct_bank_torch, tokens_torch
+
+        self.cfg = cfg
+        T, N, C, r = cfg["T"], cfg["N"], cfg["C"], cfg["r"]
+        self.mods = [(0, n, di, do) for (n, di, do) in cfg["modules"]]
+        self.toks = tokens_torch(T, N, 1 + seed_rank, cfg["prefill"], "cpu").numpy()
+        g = torch.Generator().manual_seed(2)
+
+        def f64(t):
+            return bf16_to_f64(t.contiguous().view(torch.int16).numpy().view(np.uint16))
+
+        self.banks, self.xs = [], {}
+        for m, (_, name, di, do) in enumerate(self.mods):
+            b = direct_bank_torch(di, do, N, C, r, seed=m, device="cpu", cluster_seed=50 + m)
+            self.banks.append({k: (f64(v) if k != "cluster_of" else v.numpy()) for k, v in b.items()})
+            if x_slot(name) not in self.xs:
+                self.xs[x_slot(name)] = f64(torch.randn(T, di, generator=g).to(torch.bfloat16))
+
+    def run_module(self, m):
+        """segment_ref + apply_ref of module m; returns wall seconds."""
+        from oracle import apply_ref, segment_ref
+        (_, name, _, _), b = self.mods[m], self.banks[m]
+        t0 = time.perf_counter()
+        segment_ref(self.toks, b["cluster_of"], self.cfg["C"])
+        apply_ref(self.xs[x_slot(name)], self.toks, b["cluster_of"], b["in_basis"], b["out_basis"], b["sigma"],
+                  SCALE)
+        return time.perf_counter() - t0
+
+
+def oracle_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        return int(max((i.get("num_threads", 1) for i in threadpool_info()), default=1))
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def oracle_sample(cfg, budget_s=20.0):
+    """Time the oracle on full layers (all 7 modules) repeatedly within ~budget_s; tokens/s
+    extrapolated to the whole step (x layers)."""
+    ol = OracleLayer(cfg)
+    reps, t_start = [], time.perf_counter()
+    while not reps or time.perf_counter() - t_start + reps[-1] < budget_s:
+        reps.append(sum(ol.run_module(m) for m in range(len(ol.mods))))
+    per_layer = statistics.median(reps)
+    info = {"cores": oracle_cores(), "kind": "oracle",
+            "sample": f"1 of {cfg['layers']} layers ({len(ol.mods)} modules, T={cfg['T']}), {len(reps)} rep(s), "
+                      f"median {per_layer:.3f} s/layer, extrapolated x{cfg['layers']}"}
+    return cfg["T"] / (per_layer * cfg["layers"]), info
+
+
+def run_reference(args, cfg):
+    """Reference arm: the fp64 oracle as it stands on the host cores.  Step i = module (i mod 7) of
+    one layer, so K+W steps stay within minutes; a layer's time = sum of its modules' medians."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    ol = OracleLayer(cfg)
+    nm = len(ol.mods)
+    per_mod = {m: [] for m in range(nm)}
+    for i in range(args.warmup):
+        ol.run_module(i % nm)
+    for i in range(max(args.steps, nm)):
+        per_mod[i % nm].append(ol.run_module(i % nm))
+    per_layer = sum(statistics.median(v) for v in per_mod.values())
+    value = cfg["T"] / (per_layer * cfg["layers"])
+    sample = (f"each step = one module of layer 0 (segment_ref + apply_ref, T={cfg['T']}); layer time = sum of "
+              f"the {nm} modules' medians = {per_layer:.3f} s, extrapolated x{cfg['layers']} layers")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_layer * cfg["layers"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(cfg, args.gpus),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": oracle_cores(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+METRIC = "compressed-LoRA apply tokens/s at 1000 adapters"
+
+
+def config_dict(cfg, world):
+    mods = "+".join(n for (n, _, _) in cfg["modules"])
+    return {"workload": cfg["workload"],
+            "description": f"Mistral-7B {mods} x {cfg['layers']} layers = {cfg['layers'] * len(cfg['modules'])} "
+                           f"modules, {cfg['N']} adapters / {cfg['C']} clusters, shared rank r={cfg['r']}, "
+                           f"T={cfg['T']} {'prefill' if cfg['prefill'] else 'decode'} tokens per GPU",
+            "n_adapters": cfg["N"], "n_clusters": cfg["C"], "rank": cfg["r"], "tokens_per_gpu": cfg["T"],
+            "cluster_maps": "per module", "parallelism": f"dp{world} (replicated bank, request sharding)",
+            "l2": "inputs larger than L2: every module reads its own x/y/bases (>= 10 GB per step vs 126 MB L2)",
+            "timing": "one CUDA graph per step (segment + all applies), CUDA events, max over ranks"}
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_gpu(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_00066_b200 as cts
+    from workloads.gen_torch import direct_bank_torch, tokens_torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    T, N, C, r = cfg["T"], cfg["N"], cfg["C"], cfg["r"]
+    mods = module_list(cfg)
+    M = len(mods)
+    # --- resident bank (replicated on every rank: same seeds)
+    srcs = [direct_bank_torch(di, do, N, C, r, seed=m % len(cfg["modules"]) + 1000 * (m // len(cfg["modules"])),
+                              device=dev, cluster_seed=50 + m) for m, (_, _, di, do) in enumerate(mods)]
+    bank = cts.Bank([s["in_basis"] for s in srcs], [s["out_basis"] for s in srcs], [s["sigma"] for s in srcs],
+                    [s["cluster_of"] for s in srcs])
+    cmaps = [s["cluster_of"].cpu().numpy() for s in srcs]
+    del srcs
+    torch.cuda.empty_cache()
+    # --- this rank's batch (request sharding: its own token stream) and activations
+    tokens = tokens_torch(T, N, 1 + rank, cfg["prefill"], dev)
+    g = torch.Generator(device=dev).manual_seed(2 + rank)
+    xs, ys = [], []
+    xbuf = {}
+    for (layer, name, di, do) in mods:
+        key = (layer, x_slot(name))
+        if key not in xbuf:
+            xbuf[key] = torch.randn(T, di, generator=g, device=dev).to(torch.bfloat16)
+        xs.append(xbuf[key])
+        ys.append(torch.randn(T, do, generator=g, device=dev).to(torch.bfloat16))
+    plan = cts.Plan(bank, T)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        plan.segment(tokens)
+        for m in range(M):
+            plan.apply(m, xs[m], ys[m], SCALE)
+
+    with torch.cuda.stream(stream):
+        step()                                   # eager warm-up (kernel attributes, lazy init)
+        torch.cuda.synchronize()
+        assert plan.error() == (0, -1)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        g_shrink = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_shrink, stream=stream):
+            for m in range(M):
+                plan.shrink(m, xs[m], SCALE)
+        g_expand = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_expand, stream=stream):
+            for m in range(M):
+                plan.expand(m, ys[m])
+        for _ in range(args.warmup):
+            graph.replay()
+        stream.synchronize()
+
+        # --- timed region: exactly K steps
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clocks:
+            e0.record(stream)
+            for _ in range(args.steps):
+                graph.replay()
+            e1.record(stream)
+            e1.synchronize()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms_total = e0.elapsed_time(e1)
+
+        # --- per-kernel timing: all 224 shrinks / all 224 expands as their own graphs
+        def time_graph(gr, reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            gr.replay()
+            a.record(stream)
+            for _ in range(reps):
+                gr.replay()
+            b.record(stream)
+            b.synchronize()
+            return a.elapsed_time(b) / reps
+        kreps = max(3, min(args.steps, 50))
+        ms_shrink = time_graph(g_shrink, kreps)
+        ms_expand = time_graph(g_expand, kreps)
+
+        # --- e2e through the public API with host buffers (pinned), copies inside the timed region
+        e2e_steps = max(1, min(args.steps, 3 if cfg["prefill"] else 10))
+        pin_x = {di: torch.empty(T, di, dtype=torch.bfloat16).pin_memory() for (_, _, di, _) in mods}
+        pin_y = {do: torch.empty(T, do, dtype=torch.bfloat16).pin_memory() for (_, _, _, do) in mods}
+        for k, v in pin_x.items():
+            v.copy_(xs[[m[2] for m in mods].index(k)].cpu())
+        for k, v in pin_y.items():
+            v.copy_(ys[[m[3] for m in mods].index(k)].cpu())
+        pin_tok = tokens.cpu().pin_memory()
+        dev_tok = torch.empty_like(tokens)
+        h2d = d2h = 0
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(e2e_steps):
+            h2d = d2h = 0
+            dev_tok.copy_(pin_tok, non_blocking=True)
+            h2d += pin_tok.numel() * 4
+            plan.segment(dev_tok)
+            seen = set()
+            for m, (layer, name, di, do) in enumerate(mods):
+                key = (layer, x_slot(name))
+                if key not in seen:
+                    xs[m].copy_(pin_x[di], non_blocking=True)
+                    h2d += T * di * 2
+                    seen.add(key)
+                ys[m].copy_(pin_y[do], non_blocking=True)
+                h2d += T * do * 2
+                plan.apply(m, xs[m], ys[m], SCALE)
+                pin_y[do].copy_(ys[m], non_blocking=True)
+                d2h += T * do * 2
+        b.record(stream)
+        b.synchronize()
+        ms_e2e = a.elapsed_time(b) / e2e_steps
+
+    # --- aggregate over ranks
+    per_step = ms_total / args.steps
+    if world > 1:
+        t = torch.tensor([per_step, ms_e2e, ms_shrink, ms_expand], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        per_step, ms_e2e, ms_shrink, ms_expand = t.tolist()
+    value = T * world / (per_step / 1e3)
+    e2e_value = T * world / (ms_e2e / 1e3)
+
+    tok_np = tokens.cpu().numpy()
+    b_shrink, b_expand = algorithmic_bytes(tok_np, cmaps, mods, r)
+    hbm, bf16_peak, peak_src = measured_peaks()
+    kern = {"shrink_sigma_kernel": (b_shrink.sum(), ms_shrink), "expand_kernel": (b_expand.sum(), ms_expand)}
+    dom = max(kern, key=lambda k: kern[k][1])
+    dom_bytes, dom_ms = kern[dom]
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    traffic, traffic_alg = ncu_traffic(cfg["workload"], dom)
+    path_gbs = (b_shrink.sum() + b_expand.sum()) / (per_step / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded direct banks + Gaussian activations)",
+        "config": config_dict(cfg, world),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "peak_source": peak_src,
+                     "traffic": (traffic / traffic_alg * dom_bytes / M) if traffic else None,
+                     "algorithmic_bytes_per_launch": dom_bytes / M, "avg_launch_us": dom_ms / M * 1e3,
+                     "path": {"algorithmic_bytes_per_step": b_shrink.sum() + b_expand.sum(),
+                              "achieved_gbs": path_gbs, "frac": path_gbs / hbm},
+                     "kernels": {k: {"algorithmic_bytes_per_launch": v[0] / M, "avg_launch_us": v[1] / M * 1e3,
+                                     "achieved_gbs": v[0] / (v[1] / 1e3) / 1e9,
+                                     "frac": v[0] / (v[1] / 1e3) / 1e9 / hbm} for k, v in kern.items()}},
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "public API with pinned host buffers; H2D of ids, x and y_base, D2H of y, per step"},
+        "gpu_launches": args.steps * (1 + 2 * M),
+        "clocks": clocks.result(),
+    }
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            tok_s, info = oracle_sample(cfg, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = {"value": tok_s, "unit": "tokens/s", "cores": info["cores"], "kind": "oracle",
+                                    "sample": info["sample"]}
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    plan.close()
+    bank.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
+    ap.add_argument("--impl", choices=["cts", "reference"], default="cts")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="decode")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = cfg["steps"] if args.impl == "cts" else 5
+    if args.warmup is None:
+        args.warmup = cfg["warmup"] if args.impl == "cts" else 1
+    args.warmup = max(args.warmup, 3) if args.impl == "cts" else args.warmup
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

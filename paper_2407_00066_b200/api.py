@@ -1,0 +1,216 @@
+"""Python binding of libcts.so: the C entry points under the same names, plus thin `Bank`/`Plan`
+owners.  Argument marshalling only -- every step of the apply runs in the CUDA kernels of
+csrc/.  PyTorch supplies device memory and streams; nothing here computes on the data.
+"""
+import ctypes
+
+import torch
+
+from ._lib import BankDesc, check, lib
+
+
+def _stream_handle(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _bf16(t, name):
+    if t.dtype != torch.bfloat16 or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous torch.bfloat16 tensor")
+    return t
+
+
+def cts_bank_load(in_basis, out_basis, sigma, cluster_of, stream=None):
+    """in_basis[m]: [C][d_in][r] bf16 (paper V_c), out_basis[m]: [C][d_out][r] bf16 (paper U_c),
+    sigma[m]: [N][r][r] bf16 (row = out index), cluster_of[m]: [N] int32.  All on the GPU or all
+    on the host.  Returns an opaque bank handle (ctypes.c_void_p)."""
+    M = len(in_basis)
+    if not (len(out_basis) == len(sigma) == len(cluster_of) == M) or M == 0:
+        raise ValueError("per-module lists must have the same non-zero length")
+    C, _, r = in_basis[0].shape
+    N = sigma[0].shape[0]
+    on_dev = in_basis[0].is_cuda
+    keep = []
+    for m in range(M):
+        for t, nm in ((in_basis[m], "in_basis"), (out_basis[m], "out_basis"), (sigma[m], "sigma")):
+            _bf16(t, nm)
+            if t.is_cuda != on_dev:
+                raise ValueError("bank sources must be all on the GPU or all on the host")
+        cm = cluster_of[m]
+        if cm.dtype != torch.int32 or not cm.is_contiguous() or cm.is_cuda != on_dev:
+            raise TypeError("cluster_of must be contiguous int32 on the same device as the bases")
+        if in_basis[m].shape[0] != C or in_basis[m].shape[2] != r or out_basis[m].shape[0] != C \
+                or out_basis[m].shape[2] != r or tuple(sigma[m].shape) != (N, r, r) or cm.shape[0] != N:
+            raise ValueError(f"module {m}: inconsistent bank shapes")
+        keep += [in_basis[m], out_basis[m], sigma[m], cm]
+    d_in = (ctypes.c_int32 * M)(*[int(t.shape[1]) for t in in_basis])
+    d_out = (ctypes.c_int32 * M)(*[int(t.shape[1]) for t in out_basis])
+    ptrs = lambda ts: (ctypes.c_void_p * M)(*[t.data_ptr() for t in ts])  # noqa: E731
+    desc = BankDesc(M, N, C, r, d_in, d_out, ptrs(in_basis), ptrs(out_basis), ptrs(sigma), ptrs(cluster_of),
+                    1 if on_dev else 0)
+    h = ctypes.c_void_p()
+    check("cts_bank_load", lib().cts_bank_load(ctypes.byref(desc), _stream_handle(stream), ctypes.byref(h)))
+    del keep
+    return h
+
+
+def cts_bank_bytes(bank):
+    n = ctypes.c_size_t()
+    check("cts_bank_bytes", lib().cts_bank_bytes(bank, ctypes.byref(n)))
+    return n.value
+
+
+def cts_bank_params(bank, module):
+    n = ctypes.c_int64()
+    check("cts_bank_params", lib().cts_bank_params(bank, module, ctypes.byref(n)))
+    return n.value
+
+
+def cts_bank_free(bank):
+    check("cts_bank_free", lib().cts_bank_free(bank))
+
+
+def cts_plan_create(bank, T_max):
+    h = ctypes.c_void_p()
+    check("cts_plan_create", lib().cts_plan_create(bank, int(T_max), ctypes.byref(h)))
+    return h
+
+
+def cts_plan_free(plan):
+    check("cts_plan_free", lib().cts_plan_free(plan))
+
+
+def cts_plan_max_tiles(plan, T):
+    return int(lib().cts_plan_max_tiles(plan, int(T)))
+
+
+def cts_segment(plan, token_adapter, stream=None):
+    """token_adapter: int32 CUDA tensor [T]; -1 = no adapter."""
+    if token_adapter.dtype != torch.int32 or not token_adapter.is_cuda or not token_adapter.is_contiguous():
+        raise TypeError("token_adapter must be a contiguous int32 CUDA tensor")
+    T = token_adapter.shape[0]
+    check("cts_segment", lib().cts_segment(plan, ctypes.c_void_p(token_adapter.data_ptr()), T,
+                                           _stream_handle(stream)))
+
+
+def cts_segment_readback(plan, module, T, C, stream=None):
+    """Host copies (perm[:bound], offsets[C+1], tiles[n_tiles,3]) of module's segmentation."""
+    import numpy as np
+    perm = np.zeros(max(T, 1), dtype=np.int32)
+    offsets = np.zeros(C + 1, dtype=np.int32)
+    mt = max(cts_plan_max_tiles(plan, T), 1)
+    tiles = np.zeros((mt, 3), dtype=np.int32)
+    nt = ctypes.c_int32()
+    vp = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    check("cts_segment_readback", lib().cts_segment_readback(plan, module, vp(perm), vp(offsets), vp(tiles),
+                                                             ctypes.c_void_p(ctypes.addressof(nt)),
+                                                             _stream_handle(stream)))
+    return perm[:offsets[-1]], offsets, tiles[:nt.value]
+
+
+def cts_apply(plan, module, x, y, scale=1.0, stream=None):
+    """y[t] += scale * U_c Sigma_i V_c^T x[t] in place for bound tokens (bf16 CUDA tensors, 2-D,
+    unit stride along the feature dimension)."""
+    for t, nm in ((x, "x"), (y, "y")):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or t.dim() != 2 or t.stride(1) != 1:
+            raise TypeError(f"{nm} must be a 2-D bf16 CUDA tensor with unit inner stride")
+    check("cts_apply", lib().cts_apply(plan, int(module), ctypes.c_void_p(x.data_ptr()), x.stride(0),
+                                       ctypes.c_void_p(y.data_ptr()), y.stride(0), ctypes.c_float(scale),
+                                       _stream_handle(stream)))
+
+
+def cts_shrink(plan, module, x, scale=1.0, stream=None):
+    """Kernel 1 only: t = scale * Sigma_i V_c^T x_t into the plan's scratch for `module`."""
+    if x.dtype != torch.bfloat16 or not x.is_cuda or x.dim() != 2 or x.stride(1) != 1:
+        raise TypeError("x must be a 2-D bf16 CUDA tensor with unit inner stride")
+    check("cts_shrink", lib().cts_shrink(plan, int(module), ctypes.c_void_p(x.data_ptr()), x.stride(0),
+                                         ctypes.c_float(scale), _stream_handle(stream)))
+
+
+def cts_expand(plan, module, y, stream=None):
+    """Kernel 2 only: y_t = bf16(y_t + U_c t_t) from the scratch of the last cts_shrink(module)."""
+    if y.dtype != torch.bfloat16 or not y.is_cuda or y.dim() != 2 or y.stride(1) != 1:
+        raise TypeError("y must be a 2-D bf16 CUDA tensor with unit inner stride")
+    check("cts_expand", lib().cts_expand(plan, int(module), ctypes.c_void_p(y.data_ptr()), y.stride(0),
+                                         _stream_handle(stream)))
+
+
+def cts_plan_error(plan):
+    code, bad = ctypes.c_int32(), ctypes.c_int32()
+    check("cts_plan_error", lib().cts_plan_error(plan, ctypes.byref(code), ctypes.byref(bad)))
+    return code.value, bad.value
+
+
+class Bank:
+    """Owner of a resident compressed bank (frees it on close / garbage collection)."""
+
+    def __init__(self, in_basis, out_basis, sigma, cluster_of, stream=None):
+        self.handle = cts_bank_load(in_basis, out_basis, sigma, cluster_of, stream)
+        self.n_modules = len(in_basis)
+        self.C = int(in_basis[0].shape[0])
+        self.N = int(sigma[0].shape[0])
+        self.r = int(in_basis[0].shape[2])
+        self.d_in = [int(t.shape[1]) for t in in_basis]
+        self.d_out = [int(t.shape[1]) for t in out_basis]
+
+    @property
+    def bytes(self):
+        return cts_bank_bytes(self.handle)
+
+    def params(self, module):
+        return cts_bank_params(self.handle, module)
+
+    def close(self):
+        if self.handle is not None:
+            cts_bank_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Plan:
+    """Per-batch segmentation + scratch for batches of up to T_max tokens."""
+
+    def __init__(self, bank: Bank, T_max: int):
+        self.bank = bank
+        self.T_max = T_max
+        self.T = 0
+        self.handle = cts_plan_create(bank.handle, T_max)
+
+    def segment(self, token_adapter, stream=None):
+        cts_segment(self.handle, token_adapter, stream)
+        self.T = int(token_adapter.shape[0])
+
+    def readback(self, module, stream=None):
+        return cts_segment_readback(self.handle, module, self.T, self.bank.C, stream)
+
+    def apply(self, module, x, y, scale=1.0, stream=None):
+        cts_apply(self.handle, module, x, y, scale, stream)
+
+    def shrink(self, module, x, scale=1.0, stream=None):
+        cts_shrink(self.handle, module, x, scale, stream)
+
+    def expand(self, module, y, stream=None):
+        cts_expand(self.handle, module, y, stream)
+
+    def error(self):
+        return cts_plan_error(self.handle)
+
+    def max_tiles(self, T=None):
+        return cts_plan_max_tiles(self.handle, self.T if T is None else T)
+
+    def close(self):
+        if self.handle is not None:
+            cts_plan_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,540 @@
+// cts.cu -- host side of libcts.so: bank relayout, plans, segmentation and apply launches.
+// See include/cts.h for the contract of every entry point.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/cts.h"
+#include "expand.cuh"
+#include "segment.cuh"
+#include "shrink_sigma.cuh"
+
+using namespace cts;
+
+namespace {
+
+// ------------------------------------------------------------------ driver entry point (TMA maps)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+CUtensorMapSwizzle swizzle_for(int row_bytes) {
+  switch (row_bytes) {
+    case 32: return CU_TENSOR_MAP_SWIZZLE_32B;
+    case 64: return CU_TENSOR_MAP_SWIZZLE_64B;
+    default: return CU_TENSOR_MAP_SWIZZLE_128B;
+  }
+}
+
+// 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows, `row_stride` bytes.
+bool make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride,
+               uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int pad_rank(int r) { return r <= 16 ? 16 : (r <= 32 ? 32 : 64); }
+
+int choose_bn(int d_out) {
+  for (int bn : {256, 192, 128, 64})
+    if (d_out % bn == 0) return bn;
+  return 64;
+}
+
+// ------------------------------------------------------------------ relayout kernels
+// in_basis [C][d_in][r] (paper V_c, row-major) -> [C][rp][d_in], zero rows for k >= r.
+__global__ void relayout_in_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, int C, int d_in, int r, int rp) {
+  const size_t n = static_cast<size_t>(C) * rp * d_in;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i % d_in);
+    const int k = static_cast<int>((i / d_in) % rp);
+    const int c = static_cast<int>(i / (size_t(d_in) * rp));
+    dst[i] = k < r ? src[(size_t(c) * d_in + j) * r + k] : __float2bfloat16_rn(0.f);
+  }
+}
+// [rows][r] -> [rows][rp] (out_basis rows, or Sigma rows after the row padding below).
+__global__ void relayout_pad_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, size_t rows, int r, int rp) {
+  const size_t n = rows * rp;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % rp);
+    dst[i] = k < r ? src[(i / rp) * r + k] : __float2bfloat16_rn(0.f);
+  }
+}
+// Sigma [N][r][r] -> [N][rp][rp]
+__global__ void relayout_sigma_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, int N, int r, int rp) {
+  const size_t n = static_cast<size_t>(N) * rp * rp;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % rp);
+    const int o = static_cast<int>((i / rp) % rp);
+    const int a = static_cast<int>(i / (size_t(rp) * rp));
+    dst[i] = (k < r && o < r) ? src[(size_t(a) * r + o) * r + k] : __float2bfloat16_rn(0.f);
+  }
+}
+
+struct Module {
+  int d_in, d_out, bn, map_id;
+  __nv_bfloat16* in_t;    // [C][rp][d_in]
+  __nv_bfloat16* out;     // [C][d_out][rp]
+  __nv_bfloat16* sigma;   // [N][rp][rp]
+  CUtensorMap tm_in, tm_out;
+};
+
+}  // namespace
+
+struct cts_bank_s {
+  int n_modules, N, C, r, rp;
+  std::vector<Module> mods;
+  int n_maps;
+  int32_t* maps;          // [n_maps][N]
+  void* arena;
+  size_t bytes;
+};
+
+struct cts_plan_s {
+  cts_bank_t bank;
+  int T_max, max_tiles;
+  int T;                  // tokens of the last segmented batch (host view)
+  void* arena;
+  int32_t* tok_adapter;   // [T_max]
+  int32_t* perm;          // [n_maps][T_max]
+  int32_t* offsets;       // [n_maps][C+1]
+  int4* tiles;            // [n_maps][max_tiles]
+  int32_t* n_tiles;       // [n_maps]
+  int32_t* err;           // [2]
+  __nv_bfloat16* tbuf;    // [n_modules][max_tiles*128][2*rp]  rank-r intermediate (t hi | t lo)
+  std::vector<CUtensorMap> tm_t;  // per module, over its tbuf slice
+};
+
+namespace {
+
+#define CTS_CUDA(call)                                  \
+  do {                                                  \
+    if ((call) != cudaSuccess) {                        \
+      (void)cudaGetLastError();                         \
+      return CTS_ERR_CUDA;                              \
+    }                                                   \
+  } while (0)
+
+template <typename T>
+bool aligned16(const T* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+template <int RP>
+cudaError_t set_kernel_attrs() {
+  static cudaError_t once = [] {
+    cudaError_t e = cudaFuncSetAttribute(shrink_sigma_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         ShrinkSmem<RP>::kBytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(expand_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, ExpandSmem<RP>::kBytes);
+    return e;
+  }();
+  return once;
+}
+
+__nv_bfloat16* module_tbuf(cts_plan_t p, int module) {
+  return p->tbuf + size_t(module) * p->max_tiles * kTileM * 2 * p->bank->rp;
+}
+
+template <int RP>
+cts_status_t launch_shrink(cts_plan_t p, int module, const void* x, int64_t ld_x, float scale, cudaStream_t stream) {
+  const Module& m = p->bank->mods[module];
+  const int T = p->T;
+  const int tiles_bound = cts_plan_max_tiles(p, T);
+  CUtensorMap tm_x;
+  if (!make_tmap(&tm_x, x, m.d_in, T, ld_x * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
+  CTS_CUDA(set_kernel_attrs<RP>());
+  const size_t mid = m.map_id;
+  ShrinkArgs sa;
+  sa.tiles = p->tiles + mid * p->max_tiles;
+  sa.n_tiles = p->n_tiles + mid;
+  sa.perm = p->perm + mid * p->T_max;
+  sa.tok_adapter = p->tok_adapter;
+  sa.sigma = m.sigma;
+  sa.tbuf = module_tbuf(p, module);
+  sa.kblocks = m.d_in / kBK;
+  sa.scale = scale;
+  // split-K: smallest cluster size giving >= 2 CTAs per SM worth of work, at most 8 (portable)
+  int ks = 1;
+  for (int cand : {1, 2, 4, 8}) {
+    if (cand > sa.kblocks) break;
+    ks = cand;
+    if (tiles_bound * cand >= 2 * 148) break;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ks, tiles_bound, 1);
+  cfg.blockDim = dim3(kShrinkThreads, 1, 1);
+  cfg.dynamicSmemBytes = ShrinkSmem<RP>::kBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ks;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CTS_CUDA(cudaLaunchKernelEx(&cfg, shrink_sigma_kernel<RP>, tm_x, m.tm_in, sa));
+  return CTS_OK;
+}
+
+template <int RP>
+cts_status_t launch_expand(cts_plan_t p, int module, void* y, int64_t ld_y, cudaStream_t stream) {
+  const Module& m = p->bank->mods[module];
+  const int T = p->T;
+  const int tiles_bound = cts_plan_max_tiles(p, T);
+  CUtensorMap tm_y;
+  if (!make_tmap(&tm_y, y, m.d_out, T, ld_y * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
+  CTS_CUDA(set_kernel_attrs<RP>());
+  const size_t mid = m.map_id;
+  ExpandArgs ea;
+  ea.tiles = p->tiles + mid * p->max_tiles;
+  ea.n_tiles = p->n_tiles + mid;
+  ea.perm = p->perm + mid * p->T_max;
+  ea.bn = m.bn;
+  expand_kernel<RP><<<dim3(m.d_out / m.bn, tiles_bound, 1), kExpandThreads, ExpandSmem<RP>::kBytes, stream>>>(
+      p->tm_t[module], m.tm_out, tm_y, ea);
+  CTS_CUDA(cudaGetLastError());
+  return CTS_OK;
+}
+
+cts_status_t check_x(cts_plan_t p, int32_t module, const void* x, int64_t ld_x) {
+  if (!p || !x) return CTS_ERR_INVALID_ARGUMENT;
+  if (module < 0 || module >= p->bank->n_modules) return CTS_ERR_SHAPE;
+  const Module& m = p->bank->mods[module];
+  if (ld_x < m.d_in || (ld_x * 2) % 16 || !aligned16(x)) return CTS_ERR_SHAPE;
+  return CTS_OK;
+}
+
+cts_status_t check_y(cts_plan_t p, int32_t module, const void* y, int64_t ld_y) {
+  if (!p || !y) return CTS_ERR_INVALID_ARGUMENT;
+  if (module < 0 || module >= p->bank->n_modules) return CTS_ERR_SHAPE;
+  const Module& m = p->bank->mods[module];
+  if (ld_y < m.d_out || (ld_y * 2) % 16 || !aligned16(y)) return CTS_ERR_SHAPE;
+  return CTS_OK;
+}
+
+cts_status_t do_shrink(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, float scale, cudaStream_t s) {
+  switch (p->bank->rp) {
+    case 16: return launch_shrink<16>(p, module, x, ld_x, scale, s);
+    case 32: return launch_shrink<32>(p, module, x, ld_x, scale, s);
+    default: return launch_shrink<64>(p, module, x, ld_x, scale, s);
+  }
+}
+
+cts_status_t do_expand(cts_plan_t p, int32_t module, void* y, int64_t ld_y, cudaStream_t s) {
+  switch (p->bank->rp) {
+    case 16: return launch_expand<16>(p, module, y, ld_y, s);
+    case 32: return launch_expand<32>(p, module, y, ld_y, s);
+    default: return launch_expand<64>(p, module, y, ld_y, s);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cts_status_string(cts_status_t s) {
+  switch (s) {
+    case CTS_OK: return "ok";
+    case CTS_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case CTS_ERR_SHAPE: return "shape or alignment violation";
+    case CTS_ERR_INDEX_OUT_OF_RANGE: return "index out of range";
+    case CTS_ERR_UNSUPPORTED: return "unsupported device or configuration";
+    case CTS_ERR_OUT_OF_MEMORY: return "out of device memory";
+    case CTS_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_bank_t* out) {
+  if (!out) return CTS_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (!d || !d->d_in || !d->d_out || !d->in_basis || !d->out_basis || !d->sigma || !d->cluster_of)
+    return CTS_ERR_INVALID_ARGUMENT;
+  if (d->n_modules < 1 || d->n_adapters < 1 || d->n_clusters < 1 || d->rank < 1) return CTS_ERR_SHAPE;
+  if (d->rank > 64 || d->n_clusters > 1024) return CTS_ERR_UNSUPPORTED;
+  int dev = 0, major = 0;
+  CTS_CUDA(cudaGetDevice(&dev));
+  CTS_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) return CTS_ERR_UNSUPPORTED;
+  if (!encode_fn()) return CTS_ERR_CUDA;
+  const int M = d->n_modules, N = d->n_adapters, C = d->n_clusters, r = d->rank, rp = pad_rank(r);
+  for (int m = 0; m < M; ++m) {
+    if (d->d_in[m] <= 0 || d->d_out[m] <= 0 || d->d_in[m] % 64 || d->d_out[m] % 64) return CTS_ERR_SHAPE;
+    if (!d->in_basis[m] || !d->out_basis[m] || !d->sigma[m] || !d->cluster_of[m]) return CTS_ERR_INVALID_ARGUMENT;
+  }
+  // cluster maps: bring to host, validate, dedupe
+  std::vector<std::vector<int32_t>> uniq;
+  std::vector<int> map_id(M);
+  std::vector<int32_t> tmp(N);
+  for (int m = 0; m < M; ++m) {
+    if (d->sources_on_device)
+      CTS_CUDA(cudaMemcpy(tmp.data(), d->cluster_of[m], N * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    else
+      std::memcpy(tmp.data(), d->cluster_of[m], N * sizeof(int32_t));
+    for (int i = 0; i < N; ++i)
+      if (tmp[i] < 0 || tmp[i] >= C) return CTS_ERR_INDEX_OUT_OF_RANGE;
+    int found = -1;
+    for (size_t u = 0; u < uniq.size(); ++u)
+      if (std::memcmp(uniq[u].data(), tmp.data(), N * sizeof(int32_t)) == 0) { found = int(u); break; }
+    if (found < 0) { found = int(uniq.size()); uniq.push_back(tmp); }
+    map_id[m] = found;
+  }
+  // arena layout
+  std::vector<size_t> off_in(M), off_out(M), off_sig(M);
+  size_t total = 0, stage = 0;
+  for (int m = 0; m < M; ++m) {
+    const size_t n_in = size_t(C) * rp * d->d_in[m], n_out = size_t(C) * d->d_out[m] * rp, n_sig = size_t(N) * rp * rp;
+    off_in[m] = total;  total = align_up(total + n_in * 2, 1024);
+    off_out[m] = total; total = align_up(total + n_out * 2, 1024);
+    off_sig[m] = total; total = align_up(total + n_sig * 2, 1024);
+    stage = std::max(stage, std::max(size_t(C) * d->d_in[m] * r, std::max(size_t(C) * d->d_out[m] * r, size_t(N) * r * r)) * 2);
+  }
+  const size_t off_maps = total;
+  total = align_up(total + uniq.size() * N * sizeof(int32_t), 1024);
+
+  auto* b = new (std::nothrow) cts_bank_s();
+  if (!b) return CTS_ERR_OUT_OF_MEMORY;
+  b->n_modules = M; b->N = N; b->C = C; b->r = r; b->rp = rp;
+  b->n_maps = int(uniq.size());
+  b->bytes = total;
+  if (cudaMalloc(&b->arena, total) != cudaSuccess) { (void)cudaGetLastError(); delete b; return CTS_ERR_OUT_OF_MEMORY; }
+  void* staging = nullptr;
+  if (!d->sources_on_device && cudaMalloc(&staging, stage) != cudaSuccess) {
+    (void)cudaGetLastError(); cudaFree(b->arena); delete b; return CTS_ERR_OUT_OF_MEMORY;
+  }
+  auto fail = [&](cts_status_t s) { (void)cudaGetLastError(); if (staging) cudaFree(staging); cudaFree(b->arena); delete b; return s; };
+  uint8_t* base = static_cast<uint8_t*>(b->arena);
+  b->maps = reinterpret_cast<int32_t*>(base + off_maps);
+  for (size_t u = 0; u < uniq.size(); ++u)
+    if (cudaMemcpyAsync(b->maps + u * N, uniq[u].data(), N * 4, cudaMemcpyHostToDevice, stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
+  b->mods.resize(M);
+  for (int m = 0; m < M; ++m) {
+    Module& mod = b->mods[m];
+    mod.d_in = d->d_in[m]; mod.d_out = d->d_out[m]; mod.bn = choose_bn(mod.d_out); mod.map_id = map_id[m];
+    mod.in_t = reinterpret_cast<__nv_bfloat16*>(base + off_in[m]);
+    mod.out = reinterpret_cast<__nv_bfloat16*>(base + off_out[m]);
+    mod.sigma = reinterpret_cast<__nv_bfloat16*>(base + off_sig[m]);
+    const void* srcs[3] = {d->in_basis[m], d->out_basis[m], d->sigma[m]};
+    const size_t nbytes[3] = {size_t(C) * mod.d_in * r * 2, size_t(C) * mod.d_out * r * 2, size_t(N) * r * r * 2};
+    for (int k = 0; k < 3; ++k) {
+      const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(srcs[k]);
+      if (!d->sources_on_device) {
+        if (cudaMemcpyAsync(staging, srcs[k], nbytes[k], cudaMemcpyHostToDevice, stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
+        src = static_cast<const __nv_bfloat16*>(staging);
+      }
+      if (k == 0) relayout_in_kernel<<<1184, 256, 0, stream>>>(src, mod.in_t, C, mod.d_in, r, rp);
+      if (k == 1) relayout_pad_kernel<<<1184, 256, 0, stream>>>(src, mod.out, size_t(C) * mod.d_out, r, rp);
+      if (k == 2) relayout_sigma_kernel<<<1184, 256, 0, stream>>>(src, mod.sigma, N, r, rp);
+      if (cudaGetLastError() != cudaSuccess) return fail(CTS_ERR_CUDA);
+      if (!d->sources_on_device && cudaStreamSynchronize(stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
+    }
+    if (!make_tmap(&mod.tm_in, mod.in_t, mod.d_in, uint64_t(C) * rp, uint64_t(mod.d_in) * 2, 64, rp,
+                   CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap(&mod.tm_out, mod.out, rp, uint64_t(C) * mod.d_out, uint64_t(rp) * 2, rp, mod.bn, swizzle_for(rp * 2)))
+      return fail(CTS_ERR_CUDA);
+  }
+  if (cudaStreamSynchronize(stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
+  if (staging) cudaFree(staging);
+  *out = b;
+  return CTS_OK;
+}
+
+cts_status_t cts_bank_bytes(cts_bank_t b, size_t* bytes) {
+  if (!b || !bytes) return CTS_ERR_INVALID_ARGUMENT;
+  *bytes = b->bytes;
+  return CTS_OK;
+}
+
+cts_status_t cts_bank_params(cts_bank_t b, int32_t module, int64_t* params) {
+  if (!b || !params) return CTS_ERR_INVALID_ARGUMENT;
+  if (module < 0 || module >= b->n_modules) return CTS_ERR_SHAPE;
+  const Module& m = b->mods[module];
+  *params = int64_t(b->C) * (m.d_in + m.d_out) * b->r + int64_t(b->N) * (int64_t(b->r) * b->r + (b->C > 1 ? 1 : 0));
+  return CTS_OK;
+}
+
+cts_status_t cts_bank_free(cts_bank_t b) {
+  if (!b) return CTS_ERR_INVALID_ARGUMENT;
+  cudaFree(b->arena);
+  delete b;
+  return CTS_OK;
+}
+
+int32_t cts_plan_max_tiles(cts_plan_t p, int32_t T) {
+  if (!p || T <= 0) return 0;
+  return (T + kTileM - 1) / kTileM + std::min(p->bank->C, T);
+}
+
+cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
+  if (!out) return CTS_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (!b || T_max < 1) return CTS_ERR_INVALID_ARGUMENT;
+  auto* p = new (std::nothrow) cts_plan_s();
+  if (!p) return CTS_ERR_OUT_OF_MEMORY;
+  p->bank = b;
+  p->T_max = T_max;
+  p->T = 0;
+  p->max_tiles = cts_plan_max_tiles(p, T_max);
+  const size_t nm = b->n_maps;
+  size_t off = 0;
+  const size_t o_tok = off; off = align_up(off + size_t(T_max) * 4, 256);
+  const size_t o_perm = off; off = align_up(off + nm * T_max * 4, 256);
+  const size_t o_offs = off; off = align_up(off + nm * (b->C + 1) * 4, 256);
+  const size_t o_tiles = off; off = align_up(off + nm * p->max_tiles * 16, 256);
+  const size_t o_nt = off; off = align_up(off + nm * 4, 256);
+  const size_t o_err = off; off = align_up(off + 16, 1024);
+  const size_t o_t = off; off = align_up(off + size_t(b->n_modules) * p->max_tiles * kTileM * 2 * b->rp * 2, 1024);
+  if (cudaMalloc(&p->arena, off) != cudaSuccess) { (void)cudaGetLastError(); delete p; return CTS_ERR_OUT_OF_MEMORY; }
+  uint8_t* base = static_cast<uint8_t*>(p->arena);
+  p->tok_adapter = reinterpret_cast<int32_t*>(base + o_tok);
+  p->perm = reinterpret_cast<int32_t*>(base + o_perm);
+  p->offsets = reinterpret_cast<int32_t*>(base + o_offs);
+  p->tiles = reinterpret_cast<int4*>(base + o_tiles);
+  p->n_tiles = reinterpret_cast<int32_t*>(base + o_nt);
+  p->err = reinterpret_cast<int32_t*>(base + o_err);
+  p->tbuf = reinterpret_cast<__nv_bfloat16*>(base + o_t);
+  const int32_t init_err[2] = {0, -1};
+  bool ok = cudaMemset(p->n_tiles, 0, nm * 4) == cudaSuccess &&
+            cudaMemcpy(p->err, init_err, 8, cudaMemcpyHostToDevice) == cudaSuccess;
+  p->tm_t.resize(b->n_modules);
+  for (int m = 0; ok && m < b->n_modules; ++m)
+    ok = make_tmap(&p->tm_t[m], module_tbuf(p, m), 2 * b->rp, uint64_t(p->max_tiles) * kTileM, uint64_t(4 * b->rp),
+                   b->rp, kTileM, swizzle_for(2 * b->rp));
+  if (!ok) {
+    (void)cudaGetLastError();
+    cudaFree(p->arena);
+    delete p;
+    return CTS_ERR_CUDA;
+  }
+  *out = p;
+  return CTS_OK;
+}
+
+cts_status_t cts_plan_free(cts_plan_t p) {
+  if (!p) return CTS_ERR_INVALID_ARGUMENT;
+  cudaFree(p->arena);
+  delete p;
+  return CTS_OK;
+}
+
+cts_status_t cts_segment(cts_plan_t p, const int32_t* token_adapter, int32_t T, cudaStream_t stream) {
+  if (!p || T < 0 || (T > 0 && !token_adapter)) return CTS_ERR_INVALID_ARGUMENT;
+  if (T > p->T_max) return CTS_ERR_SHAPE;
+  const cts_bank_t b = p->bank;
+  SegArgs a;
+  a.token_adapter = token_adapter;
+  a.tok_adapter_copy = p->tok_adapter;
+  a.maps = b->maps;
+  a.perm = p->perm;
+  a.offsets = p->offsets;
+  a.tiles = p->tiles;
+  a.n_tiles = p->n_tiles;
+  a.err = p->err;
+  a.T = T;
+  a.T_max = p->T_max;
+  a.N = b->N;
+  a.C = b->C;
+  a.max_tiles = p->max_tiles;
+  static const cudaError_t seg_attr = cudaFuncSetAttribute(
+      segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (kSegWarps + 2) * 1024 * 4);
+  CTS_CUDA(seg_attr);
+  segment_kernel<<<b->n_maps, kSegThreads, (kSegWarps + 2) * b->C * 4, stream>>>(a);
+  CTS_CUDA(cudaGetLastError());
+  p->T = T;
+  return CTS_OK;
+}
+
+cts_status_t cts_segment_readback(cts_plan_t p, int32_t module, int32_t* perm, int32_t* offsets, int32_t* tiles,
+                                  int32_t* n_tiles, cudaStream_t stream) {
+  if (!p) return CTS_ERR_INVALID_ARGUMENT;
+  const cts_bank_t b = p->bank;
+  if (module < 0 || module >= b->n_modules) return CTS_ERR_SHAPE;
+  const size_t mid = b->mods[module].map_id;
+  CTS_CUDA(cudaStreamSynchronize(stream));
+  if (perm && p->T > 0)
+    CTS_CUDA(cudaMemcpy(perm, p->perm + mid * p->T_max, size_t(p->T) * 4, cudaMemcpyDeviceToHost));
+  if (offsets)
+    CTS_CUDA(cudaMemcpy(offsets, p->offsets + mid * (b->C + 1), size_t(b->C + 1) * 4, cudaMemcpyDeviceToHost));
+  int32_t nt = 0;
+  CTS_CUDA(cudaMemcpy(&nt, p->n_tiles + mid, 4, cudaMemcpyDeviceToHost));
+  if (n_tiles) *n_tiles = nt;
+  if (tiles && nt > 0) {
+    std::vector<int4> tmp(nt);
+    CTS_CUDA(cudaMemcpy(tmp.data(), p->tiles + mid * p->max_tiles, size_t(nt) * 16, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < nt; ++i) {
+      tiles[3 * i] = tmp[i].x;
+      tiles[3 * i + 1] = tmp[i].y;
+      tiles[3 * i + 2] = tmp[i].z;
+    }
+  }
+  return CTS_OK;
+}
+
+cts_status_t cts_shrink(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, float scale,
+                        cudaStream_t stream) {
+  cts_status_t st = check_x(p, module, x, ld_x);
+  if (st != CTS_OK) return st;
+  if (p->T == 0) return CTS_OK;
+  return do_shrink(p, module, x, ld_x, scale, stream);
+}
+
+cts_status_t cts_expand(cts_plan_t p, int32_t module, void* y, int64_t ld_y, cudaStream_t stream) {
+  cts_status_t st = check_y(p, module, y, ld_y);
+  if (st != CTS_OK) return st;
+  if (p->T == 0) return CTS_OK;
+  return do_expand(p, module, y, ld_y, stream);
+}
+
+cts_status_t cts_apply(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, void* y, int64_t ld_y, float scale,
+                       cudaStream_t stream) {
+  cts_status_t st = check_x(p, module, x, ld_x);
+  if (st != CTS_OK) return st;
+  if ((st = check_y(p, module, y, ld_y)) != CTS_OK) return st;
+  const Module& m = p->bank->mods[module];
+  const int T = p->T;
+  if (T == 0) return CTS_OK;
+  const uint8_t* xb = static_cast<const uint8_t*>(x);
+  const uint8_t* yb = static_cast<const uint8_t*>(y);
+  const size_t xbytes = size_t(T - 1) * ld_x * 2 + m.d_in * 2, ybytes = size_t(T - 1) * ld_y * 2 + m.d_out * 2;
+  if (xb < yb + ybytes && yb < xb + xbytes) return CTS_ERR_INVALID_ARGUMENT;
+  if ((st = do_shrink(p, module, x, ld_x, scale, stream)) != CTS_OK) return st;
+  return do_expand(p, module, y, ld_y, stream);
+}
+
+cts_status_t cts_plan_error(cts_plan_t p, int32_t* code, int32_t* first_bad_token) {
+  if (!p || !code || !first_bad_token) return CTS_ERR_INVALID_ARGUMENT;
+  int32_t e[2];
+  CTS_CUDA(cudaMemcpy(e, p->err, 8, cudaMemcpyDeviceToHost));
+  *code = e[0];
+  *first_bad_token = e[1];
+  return CTS_OK;
+}
+
+}  // extern "C"

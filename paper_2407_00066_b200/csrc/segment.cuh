@@ -1,0 +1,188 @@
+// segment.cuh -- token segmentation by cluster, one CTA per distinct map.
+//
+// For a module whose adapter->cluster map is cmap:  tc[t] = cmap[token_adapter[t]] (or -1),
+// perm = bound tokens stably sorted by (cluster, token index), offsets = exclusive prefix sum of
+// per-cluster counts, tiles = (cluster, start, len <= 128).  Grouping tokens that share weights
+// is SGMV's idea; grouping by cluster makes App D's broadcast products real GEMMs.
+//
+// Algorithm (deterministic, no atomics on the data path):
+//   A. warp w owns the contiguous token range [w*seg, (w+1)*seg); per 32-token chunk,
+//      __match_any_sync groups lanes with equal keys; the group's highest lane adds the group
+//      size (popc) to the warp-private histogram hist[w][c].
+//   B. per cluster c, exclusive scan over warps (cluster-major, warp-minor) plus a block scan over
+//      clusters of the totals gives every (warp, cluster) its first output slot.
+//   C. each warp re-walks its range: a token's slot = base[w][key] + popc(peers & lanes_below).
+// Stable by construction: warps own increasing token ranges, chunks are walked in order, and the
+// within-chunk rank counts lower lanes (= lower token indices) only.
+#pragma once
+#include <cstdint>
+
+namespace cts {
+
+constexpr int kTileM = 128;          // token rows per GEMM tile (tcgen05 M)
+constexpr int kSegThreads = 1024;
+constexpr int kSegWarps = kSegThreads / 32;
+
+struct SegArgs {
+  const int32_t* token_adapter;  // [T] caller buffer
+  int32_t* tok_adapter_copy;     // [T_max] plan copy (for the Sigma lookup)
+  const int32_t* maps;           // [n_maps][N]
+  int32_t* perm;                 // [n_maps][T_max]
+  int32_t* offsets;              // [n_maps][C+1]
+  int4* tiles;                   // [n_maps][max_tiles]  (c, start, len, 0)
+  int32_t* n_tiles;              // [n_maps]
+  int32_t* err;                  // [2] code, first bad token
+  int T, T_max, N, C, max_tiles;
+};
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += n;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int s = warp_sums[lane];
+    int si = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int n = __shfl_up_sync(0xffffffffu, si, o);
+      if (lane >= o) si += n;
+    }
+    warp_sums[lane] = si - s;       // exclusive per-warp base
+    if (lane == 31) warp_sums[32] = si;
+  }
+  __syncthreads();
+  const int res = warp_sums[warp] + incl - v;
+  total = warp_sums[32];
+  __syncthreads();
+  return res;
+}
+
+__global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
+  extern __shared__ int seg_smem[];
+  int* hist = seg_smem;                            // [kSegWarps][C]
+  int* cnt = hist + kSegWarps * a.C;               // [C]
+  int* tile_base = cnt + a.C;                      // [C]
+  __shared__ int warp_sums[33];
+  __shared__ int s_bad;
+
+  const int map_id = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int* cmap = a.maps + static_cast<size_t>(map_id) * a.N;
+  int32_t* perm = a.perm + static_cast<size_t>(map_id) * a.T_max;
+  int32_t* offsets = a.offsets + static_cast<size_t>(map_id) * (a.C + 1);
+  int4* tiles = a.tiles + static_cast<size_t>(map_id) * a.max_tiles;
+
+  if (threadIdx.x == 0) s_bad = 0x7fffffff;
+  for (int i = threadIdx.x; i < kSegWarps * a.C; i += kSegThreads) hist[i] = 0;
+  __syncthreads();
+
+  // Validation (+ plan copy of the ids, done once by CTA 0).
+  for (int t = threadIdx.x; t < a.T; t += kSegThreads) {
+    const int id = a.token_adapter[t];
+    if (id < -1 || id >= a.N) atomicMin(&s_bad, t);
+    if (map_id == 0) a.tok_adapter_copy[t] = id;
+  }
+  __syncthreads();
+  if (s_bad != 0x7fffffff) {                       // poison: no tiles for any module
+    if (threadIdx.x == 0) {
+      a.n_tiles[map_id] = 0;
+      if (map_id == 0) {
+        a.err[0] = 3;  // CTS_ERR_INDEX_OUT_OF_RANGE
+        a.err[1] = s_bad;
+      }
+    }
+    return;
+  }
+  if (map_id == 0 && threadIdx.x == 0) {
+    a.err[0] = 0;
+    a.err[1] = -1;
+  }
+
+  // A. per-warp histograms over contiguous token ranges.
+  const int seg = ((a.T + kSegWarps - 1) / kSegWarps + 31) & ~31;
+  const int t_lo = warp * seg, t_hi = min(a.T, t_lo + seg);
+  int* my_hist = hist + warp * a.C;
+  for (int t0 = t_lo; t0 < t_hi; t0 += 32) {
+    const int t = t0 + lane;
+    int key = -1;
+    if (t < t_hi) {
+      const int id = a.token_adapter[t];
+      key = id >= 0 ? cmap[id] : -1;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (key >= 0 && lane == 31 - __clz(peers)) my_hist[key] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // B. (cluster-major, warp-minor) exclusive scan.
+  for (int c0 = 0; c0 < a.C; c0 += kSegThreads) {
+    const int c = c0 + threadIdx.x;
+    int run = 0;
+    if (c < a.C) {
+      for (int w = 0; w < kSegWarps; ++w) {
+        const int h = hist[w * a.C + c];
+        hist[w * a.C + c] = run;
+        run += h;
+      }
+      cnt[c] = run;
+    }
+  }
+  __syncthreads();
+  int carry = 0, tcarry = 0;
+  for (int c0 = 0; c0 < a.C; c0 += kSegThreads) {
+    const int c = c0 + threadIdx.x;
+    const int v = c < a.C ? cnt[c] : 0;
+    const int nt = (v + kTileM - 1) / kTileM;
+    int tot, ttot;
+    const int ex = block_exclusive_scan(v, warp_sums, tot);
+    const int tex = block_exclusive_scan(nt, warp_sums, ttot);
+    if (c < a.C) {
+      offsets[c] = carry + ex;
+      tile_base[c] = tcarry + tex;
+      cnt[c] = v;
+    }
+    carry += tot;
+    tcarry += ttot;
+  }
+  if (threadIdx.x == 0) {
+    offsets[a.C] = carry;
+    a.n_tiles[map_id] = tcarry;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSegWarps * a.C; i += kSegThreads) hist[i] += offsets[i % a.C];
+  __syncthreads();
+
+  // C. stable scatter.
+  for (int t0 = t_lo; t0 < t_hi; t0 += 32) {
+    const int t = t0 + lane;
+    int key = -1;
+    if (t < t_hi) {
+      const int id = a.token_adapter[t];
+      key = id >= 0 ? cmap[id] : -1;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (key >= 0) {
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      perm[my_hist[key] + rank] = t;
+    }
+    __syncwarp();
+    if (key >= 0 && lane == 31 - __clz(peers)) my_hist[key] += __popc(peers);
+    __syncwarp();
+  }
+
+  // D. tile list.
+  for (int c = threadIdx.x; c < a.C; c += kSegThreads) {
+    const int n = cnt[c], base = tile_base[c], off = offsets[c];
+    for (int j = 0; j * kTileM < n; ++j)
+      tiles[base + j] = make_int4(c, off + j * kTileM, min(kTileM, n - j * kTileM), 0);
+  }
+}
+
+}  // namespace cts

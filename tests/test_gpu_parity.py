@@ -1,0 +1,288 @@
+"""CUDA path (libcts.so through the C ABI) vs the fp64 oracle.  -m gpu."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import apply_ref, jd_full, segment_ref
+from workloads import (MISTRAL_MODULES, activations, bf16_round, bf16_to_f64, cluster_map,
+                       decode_tokens, gen_loras, prefill_tokens)
+
+from gpu_helpers import PARITY_TOL, bf16_ulp, dev_bf16, host_bits, quantized_bank, row_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cts():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2407_00066_b200 as m
+    return m
+
+
+def make_bank(cts, banks_bits):
+    return cts.Bank([dev_bf16(b["in_basis"]) for b in banks_bits],
+                    [dev_bf16(b["out_basis"]) for b in banks_bits],
+                    [dev_bf16(b["sigma"]) for b in banks_bits],
+                    [torch.from_numpy(b["cluster_of"]).cuda() for b in banks_bits])
+
+
+def run_apply(cts, plan, module, x_bits, y_bits, scale):
+    x = dev_bf16(x_bits)
+    y = dev_bf16(y_bits)
+    plan.apply(module, x, y, scale)
+    torch.cuda.synchronize()
+    return host_bits(y)
+
+
+def check_delta(ta, got_bits, f64, x_bits, scale, rows=None):
+    dy, _ = apply_ref(bf16_to_f64(x_bits), ta, f64["cluster_of"], f64["in_basis"], f64["out_basis"],
+                      f64["sigma"], scale)
+    got = bf16_to_f64(got_bits)
+    sel = np.arange(len(ta)) if rows is None else rows
+    bound = sel[ta[sel] >= 0]
+    err = row_rel_err(got[bound], dy[bound])
+    assert err.size == 0 or err.max() <= PARITY_TOL, f"max per-row rel err {err.max():.3e}"
+    unbound = sel[ta[sel] < 0]
+    assert np.all(got_bits[unbound] == 0)
+    return err
+
+
+# ---------------------------------------------------------------- segmentation: bit-exact
+@pytest.mark.parametrize("T,N,C,frac_none", [(1, 4, 1, 0.0), (32, 4, 1, 0.1), (257, 64, 1, 0.0),
+                                             (1024, 1000, 25, 0.05), (999, 8192, 128, 0.0),
+                                             (1000, 50, 1024, 0.2), (5, 3, 7, 0.0)])
+def test_segment_bit_exact(cts, T, N, C, frac_none):
+    bits, _ = quantized_bank(64, 64, N, C, 4, seed=T)
+    maps = [cluster_map(N, C, s) for s in (1, 2)]
+    banks = [dict(bits, cluster_of=m) for m in maps] + [dict(bits, cluster_of=maps[0])]
+    bank = make_bank(cts, banks)
+    plan = cts.Plan(bank, T + 5)
+    ta = decode_tokens(T, N, seed=T + 1, frac_none=frac_none)
+    plan.segment(torch.from_numpy(ta).cuda())
+    for m in range(3):
+        perm, offs, tiles = plan.readback(m)
+        rp, ro, rt = segment_ref(ta, banks[m]["cluster_of"], C)
+        assert np.array_equal(perm, rp) and np.array_equal(offs, ro) and np.array_equal(tiles, rt)
+    assert plan.error() == (0, -1)
+
+
+def test_segment_prefill_and_all_unbound(cts):
+    bits, _ = quantized_bank(64, 64, 1000, 25, 16, seed=0)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, 16384)
+    ta = prefill_tokens(16384, 1000, 5)
+    plan.segment(torch.from_numpy(ta).cuda())
+    perm, offs, tiles = plan.readback(0)
+    rp, ro, rt = segment_ref(ta, bits["cluster_of"], 25)
+    assert np.array_equal(perm, rp) and np.array_equal(offs, ro) and np.array_equal(tiles, rt)
+    plan.segment(torch.full((100,), -1, dtype=torch.int32, device="cuda"))
+    perm, offs, tiles = plan.readback(0)
+    assert perm.size == 0 and offs.tolist() == [0] * 26 and tiles.shape[0] == 0
+
+
+def test_invalid_adapter_poisons_plan(cts):
+    bits, f64 = quantized_bank(64, 128, 10, 2, 4, seed=1)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, 64)
+    ta = decode_tokens(64, 10, 2)
+    ta[[9, 40]] = [10, -3]
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(64, 64, 3))
+    y0 = bf16_round(activations(64, 128, 4))
+    got = run_apply(cts, plan, 0, x, y0, 1.0)
+    assert plan.error() == (3, 9)
+    assert np.array_equal(got, y0)                 # untouched
+    ta[[9, 40]] = 0                                # recovers on the next good batch
+    plan.segment(torch.from_numpy(ta).cuda())
+    torch.cuda.synchronize()
+    assert plan.error() == (0, -1)
+
+
+# ---------------------------------------------------------------- apply parity
+def test_config1_tiny_jd_bank(cts):
+    """Config 1: d=64, 4 LoRAs rank 2, JD-Full r=4, 1 cluster, 32 tokens."""
+    Bs, As, _ = gen_loras("random", 64, 64, 4, 2, seed=11)
+    res = jd_full(Bs, As, 4)
+    bits = {"in_basis": bf16_round(res["V"][None]), "out_basis": bf16_round(res["U"][None]),
+            "sigma": bf16_round(res["sigma"]), "cluster_of": np.zeros(4, np.int32)}
+    f64 = {k: (bf16_to_f64(v) if k != "cluster_of" else v) for k, v in bits.items()}
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, 32)
+    ta = decode_tokens(32, 4, 12, frac_none=0.1)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(32, 64, 13))
+    got = run_apply(cts, plan, 0, x, np.zeros((32, 64), np.uint16), 1.0)
+    check_delta(ta, got, f64, x, 1.0)
+
+
+@pytest.mark.parametrize("r", [4, 16, 24, 32, 64])
+@pytest.mark.parametrize("T", [1, 7, 130, 300])
+def test_ranks_and_ragged_tiles(cts, r, T):
+    """r padded to 16/32/64; tiles with len not a multiple of 4, several tiles per cluster."""
+    bits, f64 = quantized_bank(192, 320, 20, 3, r, seed=r * 7 + T)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, 20, T + r, frac_none=0.1)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(T, 192, 1))
+    got = run_apply(cts, plan, 0, x, np.zeros((T, 320), np.uint16), 0.75)
+    check_delta(ta, got, f64, x, 0.75)
+
+
+def test_config2_q_proj_r64(cts):
+    """Config 2: q_proj 4096->4096, 64 LoRAs, JD r=64, 1 cluster, T=256 decode."""
+    bits, f64 = quantized_bank(4096, 4096, 64, 1, 64, seed=2)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, 256)
+    ta = decode_tokens(256, 64, 21)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(256, 4096, 22))
+    got = run_apply(cts, plan, 0, x, np.zeros((256, 4096), np.uint16), 2.0)
+    check_delta(ta, got, f64, x, 2.0)
+
+
+@pytest.mark.slow
+def test_config2_jd_built_bank(cts):
+    """Config 2 with the bank from the oracle's JD-Full of 64 trained-like rank-16 LoRAs."""
+    Bs, As, _ = gen_loras("trained_like", 4096, 4096, 64, 16, seed=5, n_families=4)
+    res = jd_full(Bs, As, 64, iters=3)
+    bits = {"in_basis": bf16_round(res["V"][None]), "out_basis": bf16_round(res["U"][None]),
+            "sigma": bf16_round(res["sigma"]), "cluster_of": np.zeros(64, np.int32)}
+    f64 = {k: (bf16_to_f64(v) if k != "cluster_of" else v) for k, v in bits.items()}
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, 256)
+    ta = decode_tokens(256, 64, 6)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(256, 4096, 7))
+    got = run_apply(cts, plan, 0, x, np.zeros((256, 4096), np.uint16), 2.0)
+    check_delta(ta, got, f64, x, 2.0)
+
+
+def test_mistral_layer_decode_sampled(cts):
+    """One Mistral-7B layer (q,k,v,o,gate,up,down) of config 3: N=1000, C=25, r=16, T=1024,
+    per-module cluster maps; every row of every module."""
+    N, C, r, T = 1000, 25, 16, 1024
+    banks, f64s = [], []
+    for m, (_, di, do) in enumerate(MISTRAL_MODULES):
+        b, f = quantized_bank(di, do, N, C, r, seed=1000 + m, cluster_of=cluster_map(N, C, 50 + m))
+        banks.append(b)
+        f64s.append(f)
+    bank = make_bank(cts, banks)
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, N, 1)
+    plan.segment(torch.from_numpy(ta).cuda())
+    for m, (_, di, do) in enumerate(MISTRAL_MODULES):
+        x = bf16_round(activations(T, di, 2 + m))
+        got = run_apply(cts, plan, m, x, np.zeros((T, do), np.uint16), 2.0)
+        check_delta(ta, got, f64s[m], x, 2.0)
+
+
+def test_prefill_sampled(cts):
+    """Config 4 shape for one q module: T=16384 prefill (request runs, empty clusters)."""
+    N, C, r, T = 1000, 25, 16, 16384
+    bits, f64 = quantized_bank(4096, 4096, N, C, r, seed=44)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    ta = prefill_tokens(T, N, 45)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(T, 4096, 46))
+    got = run_apply(cts, plan, 0, x, np.zeros((T, 4096), np.uint16), 2.0)
+    rows = np.random.default_rng(1).choice(T, 512, replace=False)
+    # oracle on the sampled rows only (row-local computation)
+    dy, _ = apply_ref(bf16_to_f64(x[rows]), ta[rows], f64["cluster_of"], f64["in_basis"],
+                      f64["out_basis"], f64["sigma"], 2.0)
+    err = row_rel_err(bf16_to_f64(got[rows]), dy)
+    assert err.max() <= PARITY_TOL
+
+
+# ---------------------------------------------------------------- semantics
+def test_residual_add_and_untouched_rows(cts):
+    N, C, r, T = 30, 4, 16, 200
+    bits, f64 = quantized_bank(256, 512, N, C, r, seed=9)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, N, 10, frac_none=0.25)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(T, 256, 11))
+    yb = bf16_round(activations(T, 512, 12))
+    got = run_apply(cts, plan, 0, x, yb, 1.0)
+    assert np.array_equal(got[ta < 0], yb[ta < 0])                       # bit-identical
+    dy, yref = apply_ref(bf16_to_f64(x), ta, f64["cluster_of"], f64["in_basis"], f64["out_basis"],
+                         f64["sigma"], 1.0, y_base=bf16_to_f64(yb))
+    g = bf16_to_f64(got)[ta >= 0]
+    e = yref[ta >= 0]
+    # y = bf16_rne(y_base + delta_y_fp32): one rounding of the exact sum (<= 1 ulp of the result)
+    # plus the fp32 error of delta_y itself (t carried as bf16 hi+lo: ~2^-16 of the row's scale).
+    # A mis-wired residual (wrong column chunk / row) would be off by ~|delta_y|, far above this.
+    dscale = np.max(np.abs(dy[ta >= 0]), axis=1, keepdims=True)
+    assert np.all(np.abs(g - e) <= bf16_ulp(e) + 1e-3 * dscale)
+
+
+def test_sigma_zero_leaves_y(cts):
+    N, C, r, T = 8, 2, 16, 64
+    bits, _ = quantized_bank(128, 128, N, C, r, seed=3)
+    bits["sigma"] = np.zeros_like(bits["sigma"])
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, N, 4)
+    plan.segment(torch.from_numpy(ta).cuda())
+    yb = bf16_round(activations(T, 128, 5))
+    got = run_apply(cts, plan, 0, bf16_round(activations(T, 128, 6)), yb, 1.0)
+    assert np.array_equal(bf16_to_f64(got), bf16_to_f64(yb))            # value-identical (+-0)
+
+
+def test_deterministic_and_strided(cts):
+    N, C, r, T = 100, 5, 16, 500
+    bits, f64 = quantized_bank(512, 256, N, C, r, seed=8)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, N, 9)
+    plan.segment(torch.from_numpy(ta).cuda())
+    xfull = dev_bf16(bf16_round(activations(T, 640, 10)))
+    x = xfull[:, 64:576]                                                  # ld_x = 640
+    outs = []
+    for _ in range(2):
+        yfull = torch.zeros(T, 320, dtype=torch.bfloat16, device="cuda")
+        plan.apply(0, x, yfull[:, :256], 1.0)                             # ld_y = 320
+        torch.cuda.synchronize()
+        outs.append(host_bits(yfull))
+    assert np.array_equal(outs[0], outs[1])
+    assert np.all(outs[0][:, 256:] == 0)
+    check_delta(ta, outs[0][:, :256], f64, host_bits(x.contiguous()), 1.0)
+
+
+def test_permutation_equivariance(cts):
+    N, C, r, T = 40, 3, 16, 256
+    bits, _ = quantized_bank(256, 256, N, C, r, seed=12)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, N, 13, frac_none=0.1)
+    x = bf16_round(activations(T, 256, 14))
+    plan.segment(torch.from_numpy(ta).cuda())
+    a = run_apply(cts, plan, 0, x, np.zeros((T, 256), np.uint16), 1.0)
+    p = np.random.default_rng(2).permutation(T)
+    plan.segment(torch.from_numpy(np.ascontiguousarray(ta[p])).cuda())
+    b = run_apply(cts, plan, 0, np.ascontiguousarray(x[p]), np.zeros((T, 256), np.uint16), 1.0)
+    # same tokens in a different order: per-row results agree to rounding of the split-K order
+    err = row_rel_err(bf16_to_f64(b), bf16_to_f64(a[p]))
+    assert err.size == 0 or err.max() <= 2 * PARITY_TOL
+
+
+def test_host_validation(cts):
+    bits, _ = quantized_bank(64, 64, 4, 1, 4, seed=0)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, 8)
+    plan.segment(torch.zeros(8, dtype=torch.int32, device="cuda"))
+    x = torch.zeros(8, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(cts.CtsError):
+        plan.apply(1, x, torch.zeros_like(x))                              # bad module
+    with pytest.raises(cts.CtsError):
+        plan.apply(0, x, x)                                                # aliasing
+    with pytest.raises(cts.CtsError):                                     # ld_x * 2 % 16 != 0
+        plan.apply(0, torch.zeros(8, 68, dtype=torch.bfloat16, device="cuda")[:, :64], torch.zeros_like(x))
+    with pytest.raises(cts.CtsError):
+        plan.segment(torch.zeros(9, dtype=torch.int32, device="cuda"))     # T > T_max
+    assert bank.bytes > 0 and bank.params(0) == 1 * (64 + 64) * 4 + 4 * 16

@@ -1,0 +1,45 @@
+"""Device-side (torch) generators for the full-size bench banks (configs 3-5: 224 modules,
+2.2 GB at 1000 adapters) -- same recipe as gen.direct_bank, drawn on the GPU because the host
+would need ~8 GB of fp64 to draw them.  Seeded torch generators; no method arithmetic."""
+import torch
+
+
+def direct_bank_torch(d_in: int, d_out: int, N: int, C: int, r: int, seed: int, device,
+                      cluster_seed: int | None = None):
+    """bf16 tensors in the C-ABI layout: in_basis [C][d_in][r] (paper V_c, orthonormal columns),
+    out_basis [C][d_out][r] (paper U_c), sigma [N][r][r] = G a / ||G||_F with
+    a = exp(U[ln 1/2, ln 2]), cluster_of [N] int32 = pi(i) mod C."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+
+    def ortho(rows):
+        q, rr = torch.linalg.qr(torch.randn(C, rows, r, generator=g, device=device, dtype=torch.float32))
+        s = torch.sign(torch.diagonal(rr, dim1=-2, dim2=-1))
+        s[s == 0] = 1
+        return (q * s[:, None, :]).to(torch.bfloat16).contiguous()
+
+    in_basis = ortho(d_in)
+    out_basis = ortho(d_out)
+    G = torch.randn(N, r, r, generator=g, device=device, dtype=torch.float32)
+    a = torch.exp(torch.empty(N, device=device).uniform_(-0.6931471805599453, 0.6931471805599453, generator=g))
+    sigma = (G * (a / G.flatten(1).norm(dim=1))[:, None, None]).to(torch.bfloat16).contiguous()
+    gc = torch.Generator()
+    gc.manual_seed(seed + 7919 if cluster_seed is None else cluster_seed)
+    cluster_of = (torch.randperm(N, generator=gc) % C).to(torch.int32).to(device)
+    return {"in_basis": in_basis, "out_basis": out_basis, "sigma": sigma, "cluster_of": cluster_of}
+
+
+def tokens_torch(T: int, N: int, seed: int, prefill: bool, device):
+    """Decode: adapter uniform per token.  Prefill: requests of U{128..256} tokens, adapter uniform
+    per request (same recipe as gen.decode_tokens / gen.prefill_tokens, torch RNG)."""
+    g = torch.Generator()
+    g.manual_seed(seed)
+    if not prefill:
+        return torch.randint(0, N, (T,), generator=g, dtype=torch.int32).to(device)
+    out = torch.empty(T, dtype=torch.int32)
+    pos = 0
+    while pos < T:
+        L = int(torch.randint(128, 257, (1,), generator=g))
+        out[pos:pos + L] = int(torch.randint(0, N, (1,), generator=g))
+        pos += L
+    return out.to(device)
