@@ -120,9 +120,10 @@ cts_status_t cts_segment_readback(cts_plan_t plan, int32_t module, int32_t* perm
  * x: bf16 [T][ld_x] (first d_in columns used), y: bf16 [T][ld_y] read and written IN PLACE (the
  * base projection output, Punica's in-place slice update P:L1118).  scale (fp32) multiplies the
  * rank-r intermediate before the expand.  Rows of unbound tokens are not touched.
- * Two kernels: shrink + Sigma (tcgen05 grouped GEMM over cluster tiles, split-K across a thread-
- * block cluster reduced through DSMEM, per-token Sigma_i matvec in the epilogue) and expand +
- * residual (tcgen05, y rows gathered/scattered by TMA).  Deterministic (no float atomics).
+ * Two persistent kernels (one CTA per SM): shrink + Sigma (tcgen05 GEMM over 128-token cluster
+ * tiles, split-K chunks reduced in a fixed order by the last-arriving CTA, per-token Sigma_i matvec
+ * in the epilogue) and expand + residual (tcgen05, y rows gathered/scattered by TMA).
+ * Deterministic (no float atomics; the reduction order does not depend on scheduling).
  * Host validation: CTS_ERR_INVALID_ARGUMENT (null, x/y overlap), CTS_ERR_SHAPE (module index,
  * ld_x < d_in, ld_y < d_out, ld or pointer not 16-byte aligned). */
 cts_status_t cts_apply(cts_plan_t plan, int32_t module, const void* x, int64_t ld_x, void* y,
@@ -138,6 +139,20 @@ cts_status_t cts_apply(cts_plan_t plan, int32_t module, const void* x, int64_t l
 cts_status_t cts_shrink(cts_plan_t plan, int32_t module, const void* x, int64_t ld_x, float scale,
                         cudaStream_t stream);
 cts_status_t cts_expand(cts_plan_t plan, int32_t module, void* y, int64_t ld_y, cudaStream_t stream);
+
+/* Grouped forms: ONE launch per kernel covers n (1..16) distinct modules, e.g. the q, k, v
+ * projections of a layer (which may share one x) or gate and up.  modules: host int32 [n];
+ * xs / ys: host arrays [n] of device pointers; ld_x / ld_y: host int64 [n] (elements).  Each module
+ * behaves exactly as its own cts_apply; the work items of all modules are spread over the SMs of
+ * one persistent grid.  Errors as cts_apply, plus CTS_ERR_SHAPE for n > 16 and
+ * CTS_ERR_INVALID_ARGUMENT for a repeated module or a y overlapping any x or another y. */
+cts_status_t cts_apply_group(cts_plan_t plan, int32_t n, const int32_t* modules, const void* const* xs,
+                             const int64_t* ld_x, void* const* ys, const int64_t* ld_y, float scale,
+                             cudaStream_t stream);
+cts_status_t cts_shrink_group(cts_plan_t plan, int32_t n, const int32_t* modules, const void* const* xs,
+                              const int64_t* ld_x, float scale, cudaStream_t stream);
+cts_status_t cts_expand_group(cts_plan_t plan, int32_t n, const int32_t* modules, void* const* ys,
+                              const int64_t* ld_y, cudaStream_t stream);
 
 /* Read the plan's device error word (call after synchronizing the stream that ran cts_segment).
  * *code = CTS_OK or CTS_ERR_INDEX_OUT_OF_RANGE; *first_bad_token = smallest offending t or -1. */

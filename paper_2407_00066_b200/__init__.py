@@ -5,6 +5,9 @@ from .api import (  # noqa: F401
     Bank,
     Plan,
     cts_apply,
+    cts_apply_group,
+    cts_expand_group,
+    cts_shrink_group,
     cts_expand,
     cts_shrink,
     cts_bank_bytes,

@@ -23,7 +23,8 @@ STATUS = {
 EXPORTS = (
     "cts_bank_load", "cts_bank_bytes", "cts_bank_params", "cts_bank_free",
     "cts_plan_create", "cts_plan_free", "cts_plan_max_tiles",
-    "cts_segment", "cts_segment_readback", "cts_apply", "cts_shrink", "cts_expand", "cts_plan_error", "cts_status_string",
+    "cts_segment", "cts_segment_readback", "cts_apply", "cts_shrink", "cts_expand",
+    "cts_apply_group", "cts_shrink_group", "cts_expand_group", "cts_plan_error", "cts_status_string",
 )
 
 
@@ -81,6 +82,9 @@ def lib():
         "cts_apply": ([P, I32, VP, I64, VP, I64, F, P], I32),
         "cts_shrink": ([P, I32, VP, I64, F, P], I32),
         "cts_expand": ([P, I32, VP, I64, P], I32),
+        "cts_apply_group": ([P, I32, VP, VP, VP, VP, VP, F, P], I32),
+        "cts_shrink_group": ([P, I32, VP, VP, VP, F, P], I32),
+        "cts_expand_group": ([P, I32, VP, VP, VP, P], I32),
         "cts_plan_error": ([P, ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
         "cts_status_string": ([I32], ctypes.c_char_p),
     }

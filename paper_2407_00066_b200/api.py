@@ -136,6 +136,38 @@ def cts_expand(plan, module, y, stream=None):
                                          _stream_handle(stream)))
 
 
+def _group_args(modules, tensors, name):
+    n = len(modules)
+    if n == 0 or len(tensors) != n:
+        raise ValueError(f"need one {name} tensor per module")
+    for t in tensors:
+        if t.dtype != torch.bfloat16 or not t.is_cuda or t.dim() != 2 or t.stride(1) != 1:
+            raise TypeError(f"{name} must be 2-D bf16 CUDA tensors with unit inner stride")
+    mods = (ctypes.c_int32 * n)(*[int(m) for m in modules])
+    ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for t in tensors])
+    lds = (ctypes.c_int64 * n)(*[t.stride(0) for t in tensors])
+    return n, mods, ptrs, lds
+
+
+def cts_apply_group(plan, modules, xs, ys, scale=1.0, stream=None):
+    """One shrink launch + one expand launch for several modules (e.g. q, k, v sharing one x)."""
+    n, mods, xp, xl = _group_args(modules, xs, "x")
+    _, _, yp, yl = _group_args(modules, ys, "y")
+    check("cts_apply_group", lib().cts_apply_group(plan, n, mods, xp, xl, yp, yl, ctypes.c_float(scale),
+                                                   _stream_handle(stream)))
+
+
+def cts_shrink_group(plan, modules, xs, scale=1.0, stream=None):
+    n, mods, xp, xl = _group_args(modules, xs, "x")
+    check("cts_shrink_group", lib().cts_shrink_group(plan, n, mods, xp, xl, ctypes.c_float(scale),
+                                                     _stream_handle(stream)))
+
+
+def cts_expand_group(plan, modules, ys, stream=None):
+    n, mods, yp, yl = _group_args(modules, ys, "y")
+    check("cts_expand_group", lib().cts_expand_group(plan, n, mods, yp, yl, _stream_handle(stream)))
+
+
 def cts_plan_error(plan):
     code, bad = ctypes.c_int32(), ctypes.c_int32()
     check("cts_plan_error", lib().cts_plan_error(plan, ctypes.byref(code), ctypes.byref(bad)))
@@ -197,6 +229,15 @@ class Plan:
 
     def expand(self, module, y, stream=None):
         cts_expand(self.handle, module, y, stream)
+
+    def apply_group(self, modules, xs, ys, scale=1.0, stream=None):
+        cts_apply_group(self.handle, modules, xs, ys, scale, stream)
+
+    def shrink_group(self, modules, xs, scale=1.0, stream=None):
+        cts_shrink_group(self.handle, modules, xs, scale, stream)
+
+    def expand_group(self, modules, ys, stream=None):
+        cts_expand_group(self.handle, modules, ys, stream)
 
     def error(self):
         return cts_plan_error(self.handle)

@@ -1,10 +1,11 @@
-// cts.cu -- host side of libcts.so: bank relayout, plans, segmentation and apply launches.
+// cts.cu -- host side of libcts.so: bank relayout, plans, segmentation and grouped apply launches.
 // See include/cts.h for the contract of every entry point.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -61,10 +62,16 @@ bool make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, 
 
 int pad_rank(int r) { return r <= 16 ? 16 : (r <= 32 ? 32 : 64); }
 
-int choose_bn(int d_out) {
-  for (int bn : {256, 192, 128, 64})
-    if (d_out % bn == 0) return bn;
-  return 64;
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      (void)cudaGetLastError();
+      v = 148;
+    }
+    return v;
+  }();
+  return n;
 }
 
 // ------------------------------------------------------------------ relayout kernels
@@ -78,7 +85,7 @@ __global__ void relayout_in_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst,
     dst[i] = k < r ? src[(size_t(c) * d_in + j) * r + k] : __float2bfloat16_rn(0.f);
   }
 }
-// [rows][r] -> [rows][rp] (out_basis rows, or Sigma rows after the row padding below).
+// out_basis rows [rows][r] -> [rows][rp]
 __global__ void relayout_pad_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, size_t rows, int r, int rp) {
   const size_t n = rows * rp;
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
@@ -98,11 +105,10 @@ __global__ void relayout_sigma_kernel(const __nv_bfloat16* src, __nv_bfloat16* d
 }
 
 struct Module {
-  int d_in, d_out, bn, map_id;
+  int d_in, d_out, map_id;
   __nv_bfloat16* in_t;    // [C][rp][d_in]
   __nv_bfloat16* out;     // [C][d_out][rp]
   __nv_bfloat16* sigma;   // [N][rp][rp]
-  CUtensorMap tm_in, tm_out;
 };
 
 }  // namespace
@@ -112,6 +118,8 @@ struct cts_bank_s {
   std::vector<Module> mods;
   int n_maps;
   int32_t* maps;          // [n_maps][N]
+  CUtensorMap* d_tm_in;   // [n_modules] device copies (TMA descriptors in global memory)
+  CUtensorMap* d_tm_out;  // [n_modules]
   void* arena;
   size_t bytes;
 };
@@ -128,7 +136,10 @@ struct cts_plan_s {
   int32_t* n_tiles;       // [n_maps]
   int32_t* err;           // [2]
   __nv_bfloat16* tbuf;    // [n_modules][max_tiles*128][2*rp]  rank-r intermediate (t hi | t lo)
-  std::vector<CUtensorMap> tm_t;  // per module, over its tbuf slice
+  CUtensorMap* d_tm_t;    // [n_modules] device copies
+  float* ws;              // [kMaxGroup][ws_cap rows][rp]  split-K partials
+  size_t ws_cap_rows;
+  int32_t* counters;      // [kMaxGroup][max_tiles]
 };
 
 namespace {
@@ -146,113 +157,162 @@ bool aligned16(const T* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+constexpr int kTargetItemsPerSM = 3;
+
 template <int RP>
 cudaError_t set_kernel_attrs() {
   static cudaError_t once = [] {
     cudaError_t e = cudaFuncSetAttribute(shrink_sigma_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         ShrinkSmem<RP>::kBytes);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(expand_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, ExpandSmem<RP>::kBytes);
+                                         ShrinkCfg<RP>::kBytes);
     return e;
   }();
   return once;
+}
+
+template <int RP, int BN, bool EAGER>
+cudaError_t set_expand_attrs() {
+  static cudaError_t once = cudaFuncSetAttribute(expand_kernel<RP, BN, EAGER>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, ExpandCfg<RP, BN>::kBytes);
+  return once;
+}
+
+// expand variant knob (tuning aid): CTS_EXPAND_VARIANT = 0 (BN 128, lazy release), 1 (BN 128,
+// eager), 2 (BN 64, lazy), 3 (BN 64, eager).
+int expand_variant() {
+  static int v = [] {
+    const char* e = std::getenv("CTS_EXPAND_VARIANT");
+    return e ? (std::atoi(e) & 3) : 1;   // measured best: BN 128, eager release
+  }();
+  return v;
 }
 
 __nv_bfloat16* module_tbuf(cts_plan_t p, int module) {
   return p->tbuf + size_t(module) * p->max_tiles * kTileM * 2 * p->bank->rp;
 }
 
-template <int RP>
-cts_status_t launch_shrink(cts_plan_t p, int module, const void* x, int64_t ld_x, float scale, cudaStream_t stream) {
-  const Module& m = p->bank->mods[module];
-  const int T = p->T;
-  const int tiles_bound = cts_plan_max_tiles(p, T);
-  CUtensorMap tm_x;
-  if (!make_tmap(&tm_x, x, m.d_in, T, ld_x * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
-  CTS_CUDA(set_kernel_attrs<RP>());
-  const size_t mid = m.map_id;
-  ShrinkArgs sa;
-  sa.tiles = p->tiles + mid * p->max_tiles;
-  sa.n_tiles = p->n_tiles + mid;
-  sa.perm = p->perm + mid * p->T_max;
-  sa.tok_adapter = p->tok_adapter;
-  sa.sigma = m.sigma;
-  sa.tbuf = module_tbuf(p, module);
-  sa.kblocks = m.d_in / kBK;
-  sa.scale = scale;
-  // split-K: smallest cluster size giving >= 2 CTAs per SM worth of work, at most 8 (portable)
-  int ks = 1;
-  for (int cand : {1, 2, 4, 8}) {
-    if (cand > sa.kblocks) break;
-    ks = cand;
-    if (tiles_bound * cand >= 2 * 148) break;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ks, tiles_bound, 1);
-  cfg.blockDim = dim3(kShrinkThreads, 1, 1);
-  cfg.dynamicSmemBytes = ShrinkSmem<RP>::kBytes;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = ks;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CTS_CUDA(cudaLaunchKernelEx(&cfg, shrink_sigma_kernel<RP>, tm_x, m.tm_in, sa));
-  return CTS_OK;
+// K chunks per tile for a group: aim for >= kTargetItemsPerSM items per SM, each >= 4 K blocks.
+int choose_ks(int tiles_total, int min_kblocks) {
+  const int want = (kTargetItemsPerSM * sm_count() + tiles_total - 1) / std::max(tiles_total, 1);
+  return std::max(1, std::min({want, 16, std::max(1, min_kblocks / 4)}));
 }
 
 template <int RP>
-cts_status_t launch_expand(cts_plan_t p, int module, void* y, int64_t ld_y, cudaStream_t stream) {
-  const Module& m = p->bank->mods[module];
+cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
+                           float scale, cudaStream_t stream) {
+  const cts_bank_t b = p->bank;
   const int T = p->T;
   const int tiles_bound = cts_plan_max_tiles(p, T);
-  CUtensorMap tm_y;
-  if (!make_tmap(&tm_y, y, m.d_out, T, ld_y * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
   CTS_CUDA(set_kernel_attrs<RP>());
-  const size_t mid = m.map_id;
-  ExpandArgs ea;
-  ea.tiles = p->tiles + mid * p->max_tiles;
-  ea.n_tiles = p->n_tiles + mid;
-  ea.perm = p->perm + mid * p->T_max;
-  ea.bn = m.bn;
-  expand_kernel<RP><<<dim3(m.d_out / m.bn, tiles_bound, 1), kExpandThreads, ExpandSmem<RP>::kBytes, stream>>>(
-      p->tm_t[module], m.tm_out, tm_y, ea);
+  int min_kb = 1 << 30;
+  for (int i = 0; i < n; ++i) min_kb = std::min(min_kb, b->mods[modules[i]].d_in / kBK);
+  const int ks = choose_ks(tiles_bound * n, min_kb);
+  if (size_t(ks) * tiles_bound * kTileM > p->ws_cap_rows) return CTS_ERR_SHAPE;
+  ShrinkParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  prm.n_mod = n;
+  prm.tok_adapter = p->tok_adapter;
+  for (int i = 0; i < n; ++i) {
+    const Module& m = b->mods[modules[i]];
+    ShrinkMod& sm = prm.mod[i];
+    if (!make_tmap(&sm.tm_x, xs[i], m.d_in, T, ld_x[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
+    sm.tm_in = b->d_tm_in + modules[i];
+    const size_t mid = m.map_id;
+    sm.tiles = p->tiles + mid * p->max_tiles;
+    sm.n_tiles = p->n_tiles + mid;
+    sm.perm = p->perm + mid * p->T_max;
+    sm.sigma = m.sigma;
+    sm.tbuf = module_tbuf(p, modules[i]);
+    sm.ws = p->ws + size_t(i) * p->ws_cap_rows * b->rp;
+    sm.counters = p->counters + size_t(i) * p->max_tiles;
+    sm.kblocks = m.d_in / kBK;
+    sm.ks = ks;
+    sm.ws_rows = tiles_bound * kTileM;
+    sm.scale = scale;
+  }
+  const int grid = std::min(sm_count(), tiles_bound * n * ks);
+  shrink_sigma_kernel<RP><<<grid, kShrinkThreads, ShrinkCfg<RP>::kBytes, stream>>>(prm);
   CTS_CUDA(cudaGetLastError());
   return CTS_OK;
 }
 
-cts_status_t check_x(cts_plan_t p, int32_t module, const void* x, int64_t ld_x) {
-  if (!p || !x) return CTS_ERR_INVALID_ARGUMENT;
-  if (module < 0 || module >= p->bank->n_modules) return CTS_ERR_SHAPE;
-  const Module& m = p->bank->mods[module];
-  if (ld_x < m.d_in || (ld_x * 2) % 16 || !aligned16(x)) return CTS_ERR_SHAPE;
+template <int RP, int BN, bool EAGER>
+cts_status_t launch_expand(cts_plan_t p, int n, const int32_t* modules, void* const* ys, const int64_t* ld_y,
+                           cudaStream_t stream) {
+  const cts_bank_t b = p->bank;
+  const int T = p->T;
+  const int tiles_bound = cts_plan_max_tiles(p, T);
+  CTS_CUDA((set_expand_attrs<RP, BN, EAGER>()));
+  ExpandParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  prm.n_mod = n;
+  int items = 0;
+  for (int i = 0; i < n; ++i) {
+    const Module& m = b->mods[modules[i]];
+    ExpandMod& em = prm.mod[i];
+    if (!make_tmap(&em.tm_y, ys[i], m.d_out, T, ld_y[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
+    em.tm_t = p->d_tm_t + modules[i];
+    em.tm_out = b->d_tm_out + modules[i];
+    const size_t mid = m.map_id;
+    em.tiles = p->tiles + mid * p->max_tiles;
+    em.n_tiles = p->n_tiles + mid;
+    em.perm = p->perm + mid * p->T_max;
+    em.nblk = (m.d_out + BN - 1) / BN;
+    em.d_out = m.d_out;
+    items += tiles_bound * em.nblk;
+  }
+  const int grid = std::min(sm_count(), items);
+  expand_kernel<RP, BN, EAGER><<<grid, kExpandThreads, ExpandCfg<RP, BN>::kBytes, stream>>>(prm);
+  CTS_CUDA(cudaGetLastError());
   return CTS_OK;
 }
 
-cts_status_t check_y(cts_plan_t p, int32_t module, const void* y, int64_t ld_y) {
-  if (!p || !y) return CTS_ERR_INVALID_ARGUMENT;
-  if (module < 0 || module >= p->bank->n_modules) return CTS_ERR_SHAPE;
-  const Module& m = p->bank->mods[module];
-  if (ld_y < m.d_out || (ld_y * 2) % 16 || !aligned16(y)) return CTS_ERR_SHAPE;
+cts_status_t check_group(cts_plan_t p, int32_t n, const int32_t* modules, const void* const* ptrs, const int64_t* lds,
+                         bool is_x) {
+  if (!p || n < 1 || !modules || !ptrs || !lds) return CTS_ERR_INVALID_ARGUMENT;
+  if (n > kMaxGroup) return CTS_ERR_SHAPE;
+  for (int i = 0; i < n; ++i) {
+    if (modules[i] < 0 || modules[i] >= p->bank->n_modules) return CTS_ERR_SHAPE;
+    for (int j = 0; j < i; ++j)
+      if (modules[j] == modules[i]) return CTS_ERR_INVALID_ARGUMENT;
+    if (!ptrs[i]) return CTS_ERR_INVALID_ARGUMENT;
+    const Module& m = p->bank->mods[modules[i]];
+    const int64_t need = is_x ? m.d_in : m.d_out;
+    if (lds[i] < need || (lds[i] * 2) % 16 || !aligned16(ptrs[i])) return CTS_ERR_SHAPE;
+  }
   return CTS_OK;
 }
 
-cts_status_t do_shrink(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, float scale, cudaStream_t s) {
+cts_status_t do_shrink(cts_plan_t p, int n, const int32_t* mods, const void* const* xs, const int64_t* ld, float scale,
+                       cudaStream_t s) {
   switch (p->bank->rp) {
-    case 16: return launch_shrink<16>(p, module, x, ld_x, scale, s);
-    case 32: return launch_shrink<32>(p, module, x, ld_x, scale, s);
-    default: return launch_shrink<64>(p, module, x, ld_x, scale, s);
+    case 16: return launch_shrink<16>(p, n, mods, xs, ld, scale, s);
+    case 32: return launch_shrink<32>(p, n, mods, xs, ld, scale, s);
+    default: return launch_shrink<64>(p, n, mods, xs, ld, scale, s);
   }
 }
 
-cts_status_t do_expand(cts_plan_t p, int32_t module, void* y, int64_t ld_y, cudaStream_t s) {
-  switch (p->bank->rp) {
-    case 16: return launch_expand<16>(p, module, y, ld_y, s);
-    case 32: return launch_expand<32>(p, module, y, ld_y, s);
-    default: return launch_expand<64>(p, module, y, ld_y, s);
+template <int RP>
+cts_status_t expand_rp(cts_plan_t p, int n, const int32_t* mods, void* const* ys, const int64_t* ld, cudaStream_t s) {
+  switch (expand_variant()) {
+    case 1: return launch_expand<RP, 128, true>(p, n, mods, ys, ld, s);
+    case 2: return launch_expand<RP, 64, false>(p, n, mods, ys, ld, s);
+    case 3: return launch_expand<RP, 64, true>(p, n, mods, ys, ld, s);
+    default: return launch_expand<RP, 128, false>(p, n, mods, ys, ld, s);
   }
+}
+
+cts_status_t do_expand(cts_plan_t p, int n, const int32_t* mods, void* const* ys, const int64_t* ld, cudaStream_t s) {
+  switch (p->bank->rp) {
+    case 16: return expand_rp<16>(p, n, mods, ys, ld, s);
+    case 32: return expand_rp<32>(p, n, mods, ys, ld, s);
+    default: return expand_rp<64>(p, n, mods, ys, ld, s);
+  }
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  const uint8_t* x = static_cast<const uint8_t*>(a);
+  const uint8_t* y = static_cast<const uint8_t*>(b);
+  return x < y + nb && y < x + na;
 }
 
 }  // namespace
@@ -318,6 +378,8 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
   }
   const size_t off_maps = total;
   total = align_up(total + uniq.size() * N * sizeof(int32_t), 1024);
+  const size_t off_tm = total;
+  total = align_up(total + 2 * size_t(M) * sizeof(CUtensorMap), 1024);
 
   auto* b = new (std::nothrow) cts_bank_s();
   if (!b) return CTS_ERR_OUT_OF_MEMORY;
@@ -332,12 +394,15 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
   auto fail = [&](cts_status_t s) { (void)cudaGetLastError(); if (staging) cudaFree(staging); cudaFree(b->arena); delete b; return s; };
   uint8_t* base = static_cast<uint8_t*>(b->arena);
   b->maps = reinterpret_cast<int32_t*>(base + off_maps);
+  b->d_tm_in = reinterpret_cast<CUtensorMap*>(base + off_tm);
+  b->d_tm_out = b->d_tm_in + M;
   for (size_t u = 0; u < uniq.size(); ++u)
     if (cudaMemcpyAsync(b->maps + u * N, uniq[u].data(), N * 4, cudaMemcpyHostToDevice, stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
+  std::vector<CUtensorMap> h_tm(2 * size_t(M));
   b->mods.resize(M);
   for (int m = 0; m < M; ++m) {
     Module& mod = b->mods[m];
-    mod.d_in = d->d_in[m]; mod.d_out = d->d_out[m]; mod.bn = choose_bn(mod.d_out); mod.map_id = map_id[m];
+    mod.d_in = d->d_in[m]; mod.d_out = d->d_out[m]; mod.map_id = map_id[m];
     mod.in_t = reinterpret_cast<__nv_bfloat16*>(base + off_in[m]);
     mod.out = reinterpret_cast<__nv_bfloat16*>(base + off_out[m]);
     mod.sigma = reinterpret_cast<__nv_bfloat16*>(base + off_sig[m]);
@@ -355,11 +420,13 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
       if (cudaGetLastError() != cudaSuccess) return fail(CTS_ERR_CUDA);
       if (!d->sources_on_device && cudaStreamSynchronize(stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
     }
-    if (!make_tmap(&mod.tm_in, mod.in_t, mod.d_in, uint64_t(C) * rp, uint64_t(mod.d_in) * 2, 64, rp,
+    if (!make_tmap(&h_tm[m], mod.in_t, mod.d_in, uint64_t(C) * rp, uint64_t(mod.d_in) * 2, 64, rp,
                    CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap(&mod.tm_out, mod.out, rp, uint64_t(C) * mod.d_out, uint64_t(rp) * 2, rp, mod.bn, swizzle_for(rp * 2)))
+        !make_tmap(&h_tm[M + m], mod.out, rp, uint64_t(C) * mod.d_out, uint64_t(rp) * 2, rp, 64, swizzle_for(rp * 2)))
       return fail(CTS_ERR_CUDA);
   }
+  if (cudaMemcpyAsync(b->d_tm_in, h_tm.data(), h_tm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return fail(CTS_ERR_CUDA);
   if (cudaStreamSynchronize(stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
   if (staging) cudaFree(staging);
   *out = b;
@@ -402,6 +469,8 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->T_max = T_max;
   p->T = 0;
   p->max_tiles = cts_plan_max_tiles(p, T_max);
+  // split-K workspace rows per group slot: ks * tiles_bound * 128 <= (target items + tiles) * 128
+  p->ws_cap_rows = size_t(kTargetItemsPerSM * sm_count() + p->max_tiles) * kTileM;
   const size_t nm = b->n_maps;
   size_t off = 0;
   const size_t o_tok = off; off = align_up(off + size_t(T_max) * 4, 256);
@@ -409,7 +478,10 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   const size_t o_offs = off; off = align_up(off + nm * (b->C + 1) * 4, 256);
   const size_t o_tiles = off; off = align_up(off + nm * p->max_tiles * 16, 256);
   const size_t o_nt = off; off = align_up(off + nm * 4, 256);
-  const size_t o_err = off; off = align_up(off + 16, 1024);
+  const size_t o_err = off; off = align_up(off + 16, 256);
+  const size_t o_cnt = off; off = align_up(off + size_t(kMaxGroup) * p->max_tiles * 4, 1024);
+  const size_t o_tm = off; off = align_up(off + size_t(b->n_modules) * sizeof(CUtensorMap), 1024);
+  const size_t o_ws = off; off = align_up(off + size_t(kMaxGroup) * p->ws_cap_rows * b->rp * 4, 1024);
   const size_t o_t = off; off = align_up(off + size_t(b->n_modules) * p->max_tiles * kTileM * 2 * b->rp * 2, 1024);
   if (cudaMalloc(&p->arena, off) != cudaSuccess) { (void)cudaGetLastError(); delete p; return CTS_ERR_OUT_OF_MEMORY; }
   uint8_t* base = static_cast<uint8_t*>(p->arena);
@@ -419,14 +491,19 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->tiles = reinterpret_cast<int4*>(base + o_tiles);
   p->n_tiles = reinterpret_cast<int32_t*>(base + o_nt);
   p->err = reinterpret_cast<int32_t*>(base + o_err);
+  p->counters = reinterpret_cast<int32_t*>(base + o_cnt);
+  p->d_tm_t = reinterpret_cast<CUtensorMap*>(base + o_tm);
+  p->ws = reinterpret_cast<float*>(base + o_ws);
   p->tbuf = reinterpret_cast<__nv_bfloat16*>(base + o_t);
   const int32_t init_err[2] = {0, -1};
   bool ok = cudaMemset(p->n_tiles, 0, nm * 4) == cudaSuccess &&
+            cudaMemset(p->counters, 0, size_t(kMaxGroup) * p->max_tiles * 4) == cudaSuccess &&
             cudaMemcpy(p->err, init_err, 8, cudaMemcpyHostToDevice) == cudaSuccess;
-  p->tm_t.resize(b->n_modules);
+  std::vector<CUtensorMap> h_tm(b->n_modules);
   for (int m = 0; ok && m < b->n_modules; ++m)
-    ok = make_tmap(&p->tm_t[m], module_tbuf(p, m), 2 * b->rp, uint64_t(p->max_tiles) * kTileM, uint64_t(4 * b->rp),
+    ok = make_tmap(&h_tm[m], module_tbuf(p, m), 2 * b->rp, uint64_t(p->max_tiles) * kTileM, uint64_t(4 * b->rp),
                    b->rp, kTileM, swizzle_for(2 * b->rp));
+  ok = ok && cudaMemcpy(p->d_tm_t, h_tm.data(), h_tm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) == cudaSuccess;
   if (!ok) {
     (void)cudaGetLastError();
     cudaFree(p->arena);
@@ -497,35 +574,57 @@ cts_status_t cts_segment_readback(cts_plan_t p, int32_t module, int32_t* perm, i
   return CTS_OK;
 }
 
-cts_status_t cts_shrink(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, float scale,
-                        cudaStream_t stream) {
-  cts_status_t st = check_x(p, module, x, ld_x);
+cts_status_t cts_shrink_group(cts_plan_t p, int32_t n, const int32_t* modules, const void* const* xs,
+                              const int64_t* ld_x, float scale, cudaStream_t stream) {
+  cts_status_t st = check_group(p, n, modules, xs, ld_x, true);
   if (st != CTS_OK) return st;
   if (p->T == 0) return CTS_OK;
-  return do_shrink(p, module, x, ld_x, scale, stream);
+  return do_shrink(p, n, modules, xs, ld_x, scale, stream);
+}
+
+cts_status_t cts_expand_group(cts_plan_t p, int32_t n, const int32_t* modules, void* const* ys, const int64_t* ld_y,
+                              cudaStream_t stream) {
+  cts_status_t st = check_group(p, n, modules, ys, ld_y, false);
+  if (st != CTS_OK) return st;
+  if (p->T == 0) return CTS_OK;
+  return do_expand(p, n, modules, ys, ld_y, stream);
+}
+
+cts_status_t cts_apply_group(cts_plan_t p, int32_t n, const int32_t* modules, const void* const* xs,
+                             const int64_t* ld_x, void* const* ys, const int64_t* ld_y, float scale,
+                             cudaStream_t stream) {
+  cts_status_t st = check_group(p, n, modules, xs, ld_x, true);
+  if (st != CTS_OK) return st;
+  if ((st = check_group(p, n, modules, ys, ld_y, false)) != CTS_OK) return st;
+  const int T = p->T;
+  if (T == 0) return CTS_OK;
+  // no y may overlap any x or another y of the group (x's may be shared: q, k, v read one x)
+  for (int i = 0; i < n; ++i) {
+    const Module& mi = p->bank->mods[modules[i]];
+    const size_t yb = size_t(T - 1) * ld_y[i] * 2 + mi.d_out * 2;
+    for (int j = 0; j < n; ++j) {
+      const Module& mj = p->bank->mods[modules[j]];
+      const size_t xb = size_t(T - 1) * ld_x[j] * 2 + mj.d_in * 2;
+      if (overlaps(ys[i], yb, xs[j], xb)) return CTS_ERR_INVALID_ARGUMENT;
+      if (j != i && overlaps(ys[i], yb, ys[j], size_t(T - 1) * ld_y[j] * 2 + mj.d_out * 2))
+        return CTS_ERR_INVALID_ARGUMENT;
+    }
+  }
+  if ((st = do_shrink(p, n, modules, xs, ld_x, scale, stream)) != CTS_OK) return st;
+  return do_expand(p, n, modules, ys, ld_y, stream);
+}
+
+cts_status_t cts_shrink(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, float scale, cudaStream_t stream) {
+  return cts_shrink_group(p, 1, &module, &x, &ld_x, scale, stream);
 }
 
 cts_status_t cts_expand(cts_plan_t p, int32_t module, void* y, int64_t ld_y, cudaStream_t stream) {
-  cts_status_t st = check_y(p, module, y, ld_y);
-  if (st != CTS_OK) return st;
-  if (p->T == 0) return CTS_OK;
-  return do_expand(p, module, y, ld_y, stream);
+  return cts_expand_group(p, 1, &module, &y, &ld_y, stream);
 }
 
 cts_status_t cts_apply(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, void* y, int64_t ld_y, float scale,
                        cudaStream_t stream) {
-  cts_status_t st = check_x(p, module, x, ld_x);
-  if (st != CTS_OK) return st;
-  if ((st = check_y(p, module, y, ld_y)) != CTS_OK) return st;
-  const Module& m = p->bank->mods[module];
-  const int T = p->T;
-  if (T == 0) return CTS_OK;
-  const uint8_t* xb = static_cast<const uint8_t*>(x);
-  const uint8_t* yb = static_cast<const uint8_t*>(y);
-  const size_t xbytes = size_t(T - 1) * ld_x * 2 + m.d_in * 2, ybytes = size_t(T - 1) * ld_y * 2 + m.d_out * 2;
-  if (xb < yb + ybytes && yb < xb + xbytes) return CTS_ERR_INVALID_ARGUMENT;
-  if ((st = do_shrink(p, module, x, ld_x, scale, stream)) != CTS_OK) return st;
-  return do_expand(p, module, y, ld_y, stream);
+  return cts_apply_group(p, 1, &module, &x, &ld_x, &y, &ld_y, scale, stream);
 }
 
 cts_status_t cts_plan_error(cts_plan_t p, int32_t* code, int32_t* first_bad_token) {

@@ -4,157 +4,243 @@
 // Paper: App D "U (Sigma V^T x) ... broadcasted"; Punica BGMV #3 "apply matrix B and
 // update y" with `scale` -- here scale was already folded into t by kernel 1.
 //
-// One CTA per (128-token tile, BN-column block of d_out):
-//   warp 0      TMA: t_hi / t_lo tile (A operand, K-major), out_basis block (B operand, K-major),
-//               and the tile's y rows gathered by token index (tile::gather4, 64-column segments,
-//               128B swizzle) -- the y read overlaps the MMA.
-//   warp 1      one lane issues D = t_hi U^T + t_lo U^T (M=128 tokens, N=BN, K=16 per MMA).
-//   warps 0-3   epilogue, thread = token row: tcgen05.ld 32 fp32 columns, add y_base from smem,
-//               round to bf16 (RNE), write back in place; then 4-row TMA scatter to y.
+// Persistent, grouped (same scheme as the shrink): one CTA per SM walks a static round-robin list
+// of work items item = (module g, 128-token tile, BN-column block of d_out):
+//   warps 0-3   TMA producers (items dealt round-robin, one warp's gather4 issue rate is not
+//               enough): t_hi / t_lo tile (A operand, K-major), the out_basis block (B operand,
+//               K-major) and the tile's y rows gathered by token index (tile::gather4, 64-column
+//               segments, 128B swizzle) into a kStages-deep ring -- y streams in while earlier
+//               items are multiplied and stored.  The producer also leaves the item's token rows
+//               and tile descriptor in the stage, so the epilogue never waits on L2.
+//   warp 4      one lane issues D = t_hi U^T + t_lo U^T (M=128 tokens, N=BN, K=16 per MMA) into
+//               one of kAccSlots TMEM accumulators.
+//   warps 5-12  epilogue: two sets of 4 warps take alternate items; in a set each warp owns one
+//               32-row quarter (its TMEM lanes), thread = token row: tcgen05.ld 64 fp32 columns at
+//               a time, add y_base from smem, round to bf16 (RNE) in place, then the warp itself
+//               TMA-scatters its 8 four-row groups to y.  A stage is released when the set's 4
+//               warps have seen their scatters read it (bulk-group wait, one item behind).
 #pragma once
 #include "sm100.cuh"
 #include "segment.cuh"
+#include "shrink_sigma.cuh"
 
 namespace cts {
 
-constexpr int kExpandThreads = 128;
-constexpr int kExpandMaxBN = 256;
+constexpr int kEpiSets = 2;
+constexpr int kExpandThreads = 32 * (kProducerWarps + 1 + 4 * kEpiSets);
+constexpr int kBNMax = 128;              // largest d_out block per work item
+constexpr int kExpandAccSlots = 4;       // 4 x 128 fp32 columns = all of TMEM
 
-struct ExpandArgs {
+struct alignas(64) ExpandMod {
+  CUtensorMap tm_y;                      // y [T][d_out], box {64, 1}, 128B swizzle (per call)
+  const CUtensorMap* tm_t;               // tbuf [max_tiles*128][2*rp], box {rp, 128} (plan, global mem)
+  const CUtensorMap* tm_out;             // out_basis [C*d_out][rp], box {rp, 64} (bank, global mem)
   const int4* tiles;
   const int32_t* n_tiles;
   const int32_t* perm;
-  int bn;                            // columns per CTA: 64..256, multiple of 64
+  int nblk;                              // ceil(d_out / BN)
+  int d_out;
 };
 
-template <int RP>
-struct ExpandSmem {
-  static constexpr int kY = kTileM * 128;               // one 64-column segment of y rows
-  static constexpr int kOffY = 0;
-  static constexpr int kOffAhi = kOffY + (kExpandMaxBN / 64) * kY;
-  static constexpr int kOffAlo = kOffAhi + kTileM * RP * 2;
-  static constexpr int kOffB = kOffAlo + kTileM * RP * 2;
-  static constexpr int kOffRows = kOffB + kExpandMaxBN * RP * 2;
-  static constexpr int kOffBar = kOffRows + kTileM * 4;
-  static constexpr int kOffTmem = kOffBar + 3 * 8;
-  static constexpr int kBytes = kOffTmem + 16 + 1024;
-  static constexpr uint32_t kTmemCols = 256;
+struct ExpandParams {
+  ExpandMod mod[kMaxGroup];
+  int n_mod;
 };
 
-template <int RP>
-__global__ void __launch_bounds__(kExpandThreads, 1)
-    expand_kernel(const __grid_constant__ CUtensorMap tm_t, const __grid_constant__ CUtensorMap tm_out,
-                  const __grid_constant__ CUtensorMap tm_y, ExpandArgs a) {
-  using L = ExpandSmem<RP>;
+template <int RP, int BN>
+struct ExpandCfg {
+  static constexpr int kY = kTileM * 128;                    // one 64-column segment of y rows (16 KB)
+  static constexpr int kSeg = BN / 64;
+  static constexpr int kA = kTileM * RP * 2;                 // t_hi (or t_lo) tile
+  static constexpr int kB = BN * RP * 2;                     // out_basis block
+  static constexpr int kMeta = kTileM * 4 + 16;              // token rows + (g, tile, nb, len4)
+  static constexpr int kStage = kSeg * kY + 2 * kA + kB;
+  static constexpr int kStages = (200 * 1024) / (kStage + kMeta);   // rp=16: 4 (BN 128) / 7 (BN 64)
+  static constexpr int kOffMeta = kStages * kStage;
+  static constexpr int kOffBar = kOffMeta + kStages * kMeta;
+  static constexpr int kNumBars = 2 * kStages + 2 * kExpandAccSlots;
+  static constexpr int kOffMisc = kOffBar + kNumBars * 8;
+  static constexpr int kBytes = kOffMisc + 64 + 1024;
+  static constexpr uint32_t kTmemCols = kBNMax * kExpandAccSlots;
+};
+
+// EAGER: release a stage as soon as this warp's scatter has read it (blocking wait) instead of
+// one item later.
+template <int RP, int BN, bool EAGER>
+__global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_constant__ ExpandParams p) {
+  using L = ExpandCfg<RP, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sY = smem + L::kOffY;
-  uint8_t* sAhi = smem + L::kOffAhi;
-  uint8_t* sAlo = smem + L::kOffAlo;
-  uint8_t* sB = smem + L::kOffB;
-  int* rows = reinterpret_cast<int*>(smem + L::kOffRows);
-  uint64_t* bar_ab = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-  uint64_t* bar_y = bar_ab + 1;
-  uint64_t* bar_acc = bar_ab + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kOffTmem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  uint64_t* empty = full + L::kStages;
+  uint64_t* acc_full = empty + L::kStages;
+  uint64_t* acc_empty = acc_full + kExpandAccSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);
+  __shared__ int prefix[kMaxGroup + 1];
 
-  const int tile_idx = blockIdx.y;
-  if (tile_idx >= *a.n_tiles) return;
-  const int4 tile = a.tiles[tile_idx];
-  const int c = tile.x, start = tile.y, len = tile.z;
-  const int len4 = min(kTileM, (len + 3) & ~3);
-  const int ngroups = len4 >> 2;
-  const int bn = a.bn;
-  const int nseg = bn / 64;
-  const int n0 = blockIdx.x * bn;
-  const int d_out = gridDim.x * bn;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  for (int j = threadIdx.x; j < kTileM; j += kExpandThreads) rows[j] = a.perm[start + min(j, len - 1)];
   if (threadIdx.x == 0) {
-    mbar_init(bar_ab, 1);
-    mbar_init(bar_y, 1);
-    mbar_init(bar_acc, 1);
+    prefix[0] = 0;
+    for (int g = 0; g < p.n_mod; ++g) prefix[g + 1] = prefix[g] + *p.mod[g].n_tiles * p.mod[g].nblk;
+    for (int s = 0; s < L::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);            // one arrival per epilogue warp of the owning set
+    }
+    for (int s = 0; s < kExpandAccSlots; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 4);
+    }
     fence_barrier_init();
-    tma_prefetch_desc(&tm_t);
-    tma_prefetch_desc(&tm_out);
-    tma_prefetch_desc(&tm_y);
   }
-  if (warp == 2) tmem_alloc<L::kTmemCols>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<L::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int total = prefix[p.n_mod];
 
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(bar_ab, static_cast<uint32_t>(2 * kTileM * RP * 2 + bn * RP * 2));
-      tma_load_2d(sAhi, &tm_t, bar_ab, 0, tile_idx * kTileM);
-      tma_load_2d(sAlo, &tm_t, bar_ab, RP, tile_idx * kTileM);
-      tma_load_2d(sB, &tm_out, bar_ab, 0, c * d_out + n0);
-      mbar_arrive_expect_tx(bar_y, static_cast<uint32_t>(nseg * ngroups * 512));
-    }
-    __syncwarp();
-    for (int g = lane; g < ngroups; g += 32)
-      for (int s = 0; s < nseg; ++s)
-        tma_gather4(sY + s * L::kY + g * 512, &tm_y, bar_y, n0 + s * 64, rows[4 * g], rows[4 * g + 1],
-                    rows[4 * g + 2], rows[4 * g + 3]);
-    __syncwarp();
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = umma_idesc_bf16(kTileM, static_cast<uint32_t>(bn));
-      mbar_wait(bar_ab, 0);
-      tc_fence_after();
-      const uint32_t hi = smem_u32(sAhi), lo = smem_u32(sAlo), b = smem_u32(sB);
-#pragma unroll
-      for (int k = 0; k < RP / 16; ++k)
-        umma_bf16(tmem, umma_desc_kmajor(hi + k * 32, RP * 2), umma_desc_kmajor(b + k * 32, RP * 2), idesc,
-                  k != 0);
-#pragma unroll
-      for (int k = 0; k < RP / 16; ++k)
-        umma_bf16(tmem, umma_desc_kmajor(lo + k * 32, RP * 2), umma_desc_kmajor(b + k * 32, RP * 2), idesc, 1);
-      umma_commit(bar_acc);
-    }
-    __syncwarp();
-  }
+  auto stage_y = [&](int s) { return smem + s * L::kStage; };
+  auto stage_a = [&](int s) { return smem + s * L::kStage + L::kSeg * L::kY; };
+  auto stage_b = [&](int s) { return smem + s * L::kStage + L::kSeg * L::kY + 2 * L::kA; };
+  auto stage_rows = [&](int s) { return reinterpret_cast<int*>(smem + L::kOffMeta + s * L::kMeta); };
+  auto stage_info = [&](int s) { return reinterpret_cast<int4*>(smem + L::kOffMeta + s * L::kMeta + kTileM * 4); };
 
-  // ---------------- epilogue: y = bf16(y_base + acc), in smem
-  mbar_wait(bar_acc, 0);
-  mbar_wait(bar_y, 0);
-  tc_fence_after();
-  const int row = warp * 32 + lane;
-  for (int j = 0; j < bn / 32; ++j) {
-    float v[32];
-    tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + j * 32, v);
-    tmem_ld_wait();
-    if (row < len4) {
-      uint8_t* base = sY + (j >> 1) * L::kY + row * 128;
+  if (warp < kProducerWarps) {
+    // ------------------------------------------------------------ TMA producers (items round-robin)
+    int li = 0;
+    for (int item = blockIdx.x; item < total; item += gridDim.x, ++li) {
+      if (li % kProducerWarps != warp) continue;
+      const int stage = li % L::kStages;
+      const uint32_t phase = (li / L::kStages) & 1;
+      const int g = find_module(prefix, p.n_mod, item);
+      const ExpandMod& m = p.mod[g];
+      const int tile = (item - prefix[g]) / m.nblk, nb = (item - prefix[g]) % m.nblk;
+      const int4 t4 = m.tiles[tile];
+      const int len4 = min(kTileM, (t4.z + 3) & ~3);
+      const int ngroups = len4 >> 2;
+      int r4[4];
 #pragma unroll
-      for (int qd = 0; qd < 4; ++qd) {
-        const int phys = (((j & 1) * 4 + qd) ^ (row & 7)) * 16;
-        uint4 w = *reinterpret_cast<uint4*>(base + phys);
-        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+      for (int q = 0; q < 4; ++q) r4[q] = m.perm[t4.y + min(4 * lane + q, t4.z - 1)];
+      mbar_wait(&empty[stage], phase ^ 1);
+      *reinterpret_cast<int4*>(stage_rows(stage) + 4 * lane) = make_int4(r4[0], r4[1], r4[2], r4[3]);
+      if (lane == 0) *stage_info(stage) = make_int4(g, t4.x, nb, len4);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(2 * L::kA + L::kB + L::kSeg * ngroups * 512));
+        tma_load_2d(stage_a(stage), m.tm_t, &full[stage], 0, tile * kTileM);
+        tma_load_2d(stage_a(stage) + L::kA, m.tm_t, &full[stage], RP, tile * kTileM);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(h[e]);
-          h[e] = __floats2bfloat162_rn(f.x + v[qd * 8 + 2 * e], f.y + v[qd * 8 + 2 * e + 1]);
-        }
-        *reinterpret_cast<uint4*>(base + phys) = w;
+        for (int s = 0; s < L::kSeg; ++s)
+          tma_load_2d(stage_b(stage) + s * 64 * RP * 2, m.tm_out, &full[stage], 0, t4.x * m.d_out + nb * BN + s * 64);
+      }
+      __syncwarp();
+      if (lane < ngroups) {
+#pragma unroll
+        for (int s = 0; s < L::kSeg; ++s)
+          tma_gather4(stage_y(stage) + s * L::kY + lane * 512, &m.tm_y, &full[stage], nb * BN + s * 64, r4[0], r4[1],
+                      r4[2], r4[3]);
       }
     }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(kTileM, BN);
+    int stage = 0, slot = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+      mbar_wait(&acc_empty[slot], aphase ^ 1);
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t acc = tmem + slot * kBNMax;
+        const uint32_t hi = smem_u32(stage_a(stage)), lo = hi + L::kA, b = smem_u32(stage_b(stage));
+#pragma unroll
+        for (int k = 0; k < RP / 16; ++k)
+          umma_bf16(acc, umma_desc_kmajor(hi + k * 32, RP * 2), umma_desc_kmajor(b + k * 32, RP * 2), idesc, k != 0);
+#pragma unroll
+        for (int k = 0; k < RP / 16; ++k)
+          umma_bf16(acc, umma_desc_kmajor(lo + k * 32, RP * 2), umma_desc_kmajor(b + k * 32, RP * 2), idesc, 1);
+        umma_commit(&acc_full[slot]);
+      }
+      __syncwarp();
+      if (++stage == L::kStages) { stage = 0; phase ^= 1; }
+      if (++slot == kExpandAccSlots) { slot = 0; aphase ^= 1; }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (2 sets x 4 warps)
+    const int ew = warp - kEpiWarp0;           // 0..7
+    const int set = ew >> 2;
+    const int quarter = warp & 3;              // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    int prev_stage = -1;
+    int li = set;
+    for (int item = blockIdx.x + set * gridDim.x; item < total; item += kEpiSets * gridDim.x, li += kEpiSets) {
+      const int stage = li % L::kStages, slot = li % kExpandAccSlots;
+      const uint32_t phase = (li / L::kStages) & 1, aphase = (li / kExpandAccSlots) & 1;
+      mbar_wait(&acc_full[slot], aphase);
+      mbar_wait(&full[stage], phase);        // y rows + metadata landed (acquire for this thread)
+      tc_fence_after();
+      const int4 info = *stage_info(stage);   // (g, cluster, nb, len4)
+      const int len4 = info.w;
+      uint8_t* ys = stage_y(stage);
+      const bool active = quarter * 32 < len4;   // warp-uniform: this quarter holds valid rows
+      if (active) {
+#pragma unroll 1
+        for (int j2 = 0; j2 < BN / 64; ++j2) {
+          float v[64];
+          const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * kBNMax + j2 * 64;
+          tmem_ld32(taddr, v);
+          tmem_ld32(taddr + 32, v + 32);
+          tmem_ld_wait();
+          if (row < len4) {
+            uint8_t* base = ys + j2 * L::kY + row * 128;   // 64 columns = one segment
+#pragma unroll
+            for (int qd = 0; qd < 8; ++qd) {
+              const int phys = (qd ^ (row & 7)) * 16;
+              uint4 w = *reinterpret_cast<uint4*>(base + phys);
+              __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                h[e] = __floats2bfloat162_rn(f.x + v[qd * 8 + 2 * e], f.y + v[qd * 8 + 2 * e + 1]);
+              }
+              *reinterpret_cast<uint4*>(base + phys) = w;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[slot]);
+      if (active) {
+        // this warp's 8 four-row groups: lane -> (group, segment)
+        fence_proxy_async_smem();
+        __syncwarp();
+        const int grp = quarter * 8 + (lane & 7), seg = lane >> 3;
+        if (grp * 4 < len4 && seg < L::kSeg) {
+          const int4 r4 = *reinterpret_cast<const int4*>(stage_rows(stage) + 4 * grp);
+          tma_scatter4(&p.mod[info.x].tm_y, ys + seg * L::kY + grp * 512, info.z * BN + seg * 64, r4.x, r4.y, r4.z,
+                       r4.w);
+        }
+      }
+      bulk_commit();
+      if (EAGER) {
+        bulk_wait_read<0>();                  // this item's scatters have read the stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+      } else {
+        bulk_wait_read<1>();                  // this warp's previous item has been read out of smem
+        __syncwarp();
+        if (lane == 0 && prev_stage >= 0) mbar_arrive(&empty[prev_stage]);
+        prev_stage = stage;
+      }
+    }
+    bulk_wait_read<0>();
+    __syncwarp();
+    if (lane == 0 && prev_stage >= 0) mbar_arrive(&empty[prev_stage]);
+    bulk_wait0();                             // this warp's global writes complete before exit
   }
-  tc_fence_before();
-  fence_proxy_async_smem();
   __syncthreads();
-  if (warp == 0) {
-    for (int g = lane; g < ngroups; g += 32)
-      for (int s = 0; s < nseg; ++s)
-        tma_scatter4(&tm_y, sY + s * L::kY + g * 512, n0 + s * 64, rows[4 * g], rows[4 * g + 1],
-                     rows[4 * g + 2], rows[4 * g + 3]);
-    bulk_commit();
-    bulk_wait_read0();
-  }
-  if (warp == 2) tmem_dealloc<L::kTmemCols>(tmem);
+  if (warp == kMmaWarp) tmem_dealloc<L::kTmemCols>(tmem);
 }
 
 }  // namespace cts

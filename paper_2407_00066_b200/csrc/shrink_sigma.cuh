@@ -2,200 +2,279 @@
 // cluster tiles) fused with the per-token Sigma_i matvec t_t = scale * Sigma_i s_t.
 //
 // Paper: App D broadcast product "V^T x" then "Sigma (V^T x)"; Punica BGMV #1/#2 of
-// add_lora_slice_with_sigma with fp32 buffers.  Here both live in ONE kernel and
-// the rank-r intermediate never round-trips through HBM as fp32.
+// add_lora_slice_with_sigma with fp32 buffers.  Here both live in ONE kernel and the
+// rank-r intermediate never round-trips through HBM as fp32.
 //
-// Work decomposition: one thread-block cluster of KS CTAs per 128-token tile of one cluster c.
-// CTA q of the cluster owns the K-slice [q*K/KS, (q+1)*K/KS) of d_in (split-K), so decode-sized
-// tiles (~41 tokens) still spread the x stream over >= 148 SMs.
-//   warp 0      TMA producer: x rows gathered by token index (tile::gather4, 128B swizzle) and the
-//               in_basis K-slab (tile), STAGES-deep mbarrier ring
-//   warp 1      one elected lane issues tcgen05.mma (M=128 tokens, N=r_pad, K=16) into TMEM
-//   warps 0-3   epilogue: tcgen05.ld (thread = token row) -> smem partials -> cluster barrier ->
-//               CTA q reduces rows q, q+KS, ... over the KS partials through DSMEM in rank order
-//               (deterministic) -> Sigma_i row gather (L2-resident, 16-byte loads) + r x r matvec
-//               -> t split into bf16 hi + lo (t ~= hi + lo to ~2^-16 relative) for the expand.
-// Rows past the tile's valid length up to a multiple of 4 duplicate the last valid token (so the
-// expand's 4-row TMA scatter writes identical bytes for duplicates).
+// Persistent, grouped: one launch covers a group of modules (e.g. q,k,v which share x); the grid is
+// one CTA per SM and every CTA walks a static round-robin list of work items
+//     item = (module g, 128-token tile of one cluster, K-chunk kc of d_in)
+// so the TMA ring keeps streaming across item boundaries (no per-tile launch/prologue latency).
+//   warps 0-3   TMA producers: x rows gathered by token index (tile::gather4, 128B swizzle) and
+//               the in_basis K-slab (tile) into a kStages-deep mbarrier ring shared by all items;
+//               K blocks are dealt round-robin to the 4 warps because one warp's gather4 issue
+//               rate caps at ~2 TB/s per GPU (measured, profiles/microbench), four reach the
+//               tile-load rate
+//   warp 4      one elected lane issues tcgen05.mma (M=128 tokens, N=r_pad, K=16) into one of
+//               kAccSlots TMEM accumulators, commit -> acc_full[slot]
+//   warps 5-8   epilogue, thread = token row (TMEM lane quarter w%4): tcgen05.ld the partial s;
+//               split-K: the partial goes to an fp32 workspace, the LAST CTA to finish a tile
+//               (per-tile arrival counter) sums the KS partials in kc order (deterministic),
+//               gathers Sigma_i (L2-resident, 16-byte loads) and writes t = scale*Sigma_i s as a
+//               bf16 hi + lo pair (t ~= hi + lo to ~2^-16 relative) for the expand.
+// Rows of a tile past its length, up to a multiple of 4, duplicate the last valid token, so the
+// expand's 4-row TMA scatter writes identical bytes for duplicates.
 #pragma once
 #include "sm100.cuh"
 #include "segment.cuh"
 
 namespace cts {
 
-constexpr int kShrinkStages = 4;
-constexpr int kBK = 64;                      // bf16 elements per K block = one 128-byte row
-constexpr int kShrinkThreads = 128;
+constexpr int kBK = 64;                 // bf16 elements per K block = one 128-byte swizzle row
+constexpr int kMaxGroup = 16;           // modules per grouped launch
+constexpr int kProducerWarps = 4;
+constexpr int kMmaWarp = kProducerWarps;
+constexpr int kEpiWarp0 = kProducerWarps + 1;
+constexpr int kShrinkThreads = 32 * (kProducerWarps + 1 + 4);   // producers, MMA, 4 epilogue warps
+constexpr int kShrinkAccSlots = 4;
 
-struct ShrinkArgs {
-  const int4* tiles;                // this module's tile list
-  const int32_t* n_tiles;           // -> count for this module's map
-  const int32_t* perm;              // this module's permutation
-  const int32_t* tok_adapter;       // plan copy of token -> adapter
-  const __nv_bfloat16* sigma;       // [N][RP][RP], row = out index
-  __nv_bfloat16* tbuf;              // [max_tiles*128][2*RP]  (hi | lo)
-  int kblocks;                      // d_in / 64
+struct alignas(64) ShrinkMod {
+  CUtensorMap tm_x;                     // x [T][d_in], box {64, 1}, 128B swizzle (per call)
+  const CUtensorMap* tm_in;             // in_basis [C*rp][d_in], box {64, rp} (bank, global mem)
+  const int4* tiles;                    // (cluster, start, len, -)
+  const int32_t* n_tiles;
+  const int32_t* perm;
+  const __nv_bfloat16* sigma;           // [N][rp][rp], row = out index
+  __nv_bfloat16* tbuf;                  // [max_tiles*128][2*rp]  (hi | lo)
+  float* ws;                            // [ks][max_tiles*128][rp] split-K partials
+  int32_t* counters;                    // [max_tiles] arrivals per tile (self-resetting)
+  int kblocks;                          // d_in / 64
+  int ks;                               // K chunks per tile
+  int ws_rows;                          // max_tiles * 128
   float scale;
 };
 
-template <int RP>
-struct ShrinkSmem {
-  static constexpr int kA = kTileM * 128;          // bytes per A stage
-  static constexpr int kB = RP * 128;              // bytes per B stage
-  static constexpr int kRed = kTileM * (RP + 1) * 4;
-  static constexpr int kOffA = 0;
-  static constexpr int kOffB = kOffA + kShrinkStages * kA;
-  static constexpr int kOffRed = kOffB + kShrinkStages * kB;
-  static constexpr int kOffSred = kOffRed + kRed;
-  static constexpr int kOffRows = kOffSred + kRed;
-  static constexpr int kOffBar = kOffRows + kTileM * 4;
-  static constexpr int kOffTmem = kOffBar + (2 * kShrinkStages + 1) * 8;
-  static constexpr int kBytes = kOffTmem + 16 + 1024;  // + alignment slack
-  static constexpr uint32_t kTmemCols = RP <= 32 ? 32 : 64;
+struct ShrinkParams {
+  ShrinkMod mod[kMaxGroup];
+  const int32_t* tok_adapter;
+  int n_mod;
 };
 
 template <int RP>
-__global__ void __launch_bounds__(kShrinkThreads, 1)
-    shrink_sigma_kernel(const __grid_constant__ CUtensorMap tm_x,
-                        const __grid_constant__ CUtensorMap tm_in, ShrinkArgs a) {
-  using L = ShrinkSmem<RP>;
+struct ShrinkCfg {
+  static constexpr int kStages = 8;
+  static constexpr int kA = kTileM * 128;           // bytes per A stage (x rows)
+  static constexpr int kB = RP * 128;               // bytes per B stage (in_basis rows)
+  static constexpr int kOffA = 0;
+  static constexpr int kOffB = kOffA + kStages * kA;
+  static constexpr int kOffBar = kOffB + kStages * kB;
+  static constexpr int kNumBars = 2 * kStages + 2 * kShrinkAccSlots;
+  static constexpr int kOffMisc = kOffBar + kNumBars * 8;
+  static constexpr int kBytes = kOffMisc + 64 + 1024;
+  static constexpr uint32_t kSlotCols = RP < 32 ? 32 : RP;
+  static constexpr uint32_t kTmemCols = kSlotCols * kShrinkAccSlots;   // 128 or 256
+};
+
+// item -> (module g, local index j) through the per-module item prefix sums kept in smem
+__device__ __forceinline__ int find_module(const int* prefix, int n_mod, int item) {
+  int g = 0;
+  while (g + 1 < n_mod && item >= prefix[g + 1]) ++g;
+  return g;
+}
+
+template <int RP>
+__global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const __grid_constant__ ShrinkParams p) {
+  using L = ShrinkCfg<RP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem + L::kOffA;
   uint8_t* sB = smem + L::kOffB;
-  float* red = reinterpret_cast<float*>(smem + L::kOffRed);
-  float* sred = reinterpret_cast<float*>(smem + L::kOffSred);
-  int* rows = reinterpret_cast<int*>(smem + L::kOffRows);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-  uint64_t* empty = full + kShrinkStages;
-  uint64_t* acc_bar = empty + kShrinkStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kOffTmem);
+  uint64_t* empty = full + L::kStages;
+  uint64_t* acc_full = empty + L::kStages;
+  uint64_t* acc_empty = acc_full + kShrinkAccSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);
+  int* s_last = reinterpret_cast<int*>(smem + L::kOffMisc + 16);
+  __shared__ int prefix[kMaxGroup + 1];
 
-  const int tile_idx = blockIdx.y;
-  if (tile_idx >= *a.n_tiles) return;              // uniform across the cluster
-  const int4 tile = a.tiles[tile_idx];             // (c, start, len, -)
-  const int c = tile.x, start = tile.y, len = tile.z;
-  const int len4 = min(kTileM, (len + 3) & ~3);
-  const int ngroups = len4 >> 2;
-  const int ks = gridDim.x;
-  const int q = static_cast<int>(cluster_ctarank());
-  const int kb0 = q * a.kblocks / ks, kb1 = (q + 1) * a.kblocks / ks;
-  const int nkb = kb1 - kb0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  for (int j = threadIdx.x; j < kTileM; j += kShrinkThreads) rows[j] = a.perm[start + min(j, len - 1)];
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kShrinkStages; ++s) {
+    prefix[0] = 0;
+    for (int g = 0; g < p.n_mod; ++g) prefix[g + 1] = prefix[g] + *p.mod[g].n_tiles * p.mod[g].ks;
+    for (int s = 0; s < L::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_bar, 1);
+    for (int s = 0; s < kShrinkAccSlots; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 4);       // one arrival per epilogue warp
+    }
     fence_barrier_init();
-    tma_prefetch_desc(&tm_x);
-    tma_prefetch_desc(&tm_in);
   }
-  if (warp == 2) tmem_alloc<L::kTmemCols>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<L::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int total = prefix[p.n_mod];
 
-  if (warp == 0) {
-    // ---------------- TMA producer
-    const uint32_t stage_bytes = static_cast<uint32_t>(ngroups * 512 + L::kB);
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % kShrinkStages;
-      const uint32_t ph = (i / kShrinkStages) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], stage_bytes);
-      __syncwarp();
-      const int k0 = (kb0 + i) * kBK;
-      uint8_t* dstA = sA + s * L::kA;
-      for (int g = lane; g < ngroups; g += 32)
-        tma_gather4(dstA + g * 512, &tm_x, &full[s], k0, rows[4 * g], rows[4 * g + 1],
-                    rows[4 * g + 2], rows[4 * g + 3]);
-      if (lane == 0) tma_load_2d(sB + s * L::kB, &tm_in, &full[s], k0, c * RP);
-      __syncwarp();
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(kTileM, RP);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % kShrinkStages;
-        const uint32_t ph = (i / kShrinkStages) & 1;
-        mbar_wait(&full[s], ph);
-        tc_fence_after();
-        const uint32_t a_base = smem_u32(sA + s * L::kA);
-        const uint32_t b_base = smem_u32(sB + s * L::kB);
+  if (warp < kProducerWarps) {
+    // ------------------------------------------------------------ TMA producers (K blocks dealt round-robin)
+    int li = 0;
+    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+      const int g = find_module(prefix, p.n_mod, item);
+      const ShrinkMod& m = p.mod[g];
+      const int tile = (item - prefix[g]) / m.ks, kc = (item - prefix[g]) % m.ks;
+      const int4 t4 = m.tiles[tile];
+      const int len4 = min(kTileM, (t4.z + 3) & ~3);
+      const int ngroups = len4 >> 2;
+      const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
+      const uint32_t bytes = static_cast<uint32_t>(ngroups * 512 + L::kB);
+      // token rows of this tile (4 per lane, clamped duplicates past len)
+      int r4[4];
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k)
-          umma_bf16(tmem, umma_desc_kmajor(a_base + k * 32, 128), umma_desc_kmajor(b_base + k * 32, 128),
-                    idesc, (i | k) != 0);
-        umma_commit(&empty[s]);
+      for (int q = 0; q < 4; ++q) r4[q] = m.perm[t4.y + min(4 * lane + q, t4.z - 1)];
+      for (int kb = kb0; kb < kb1; ++kb, ++li) {
+        if (li % kProducerWarps != warp) continue;
+        const int stage = li % L::kStages;
+        const uint32_t phase = (li / L::kStages) & 1;
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
+        __syncwarp();
+        uint8_t* dA = sA + stage * L::kA;
+        if (lane < ngroups) tma_gather4(dA + lane * 512, &m.tm_x, &full[stage], kb * kBK, r4[0], r4[1], r4[2], r4[3]);
+        if (lane == 0) tma_load_2d(sB + stage * L::kB, m.tm_in, &full[stage], kb * kBK, t4.x * RP);
       }
-      umma_commit(acc_bar);
     }
-    __syncwarp();
-  }
-
-  // ---------------- epilogue 1: TMEM -> smem partial sums (thread = token row)
-  mbar_wait(acc_bar, 0);
-  tc_fence_after();
-  {
-    const int row = warp * 32 + lane;
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(kTileM, RP);
+    int stage = 0, slot = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+      const int g = find_module(prefix, p.n_mod, item);
+      const ShrinkMod& m = p.mod[g];
+      const int kc = (item - prefix[g]) % m.ks;
+      const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
+      mbar_wait(&acc_empty[slot], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t acc = tmem + slot * L::kSlotCols;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_base = smem_u32(sA + stage * L::kA);
+          const uint32_t b_base = smem_u32(sB + stage * L::kB);
 #pragma unroll
-    for (int col = 0; col < RP; col += 16) {
-      float v[16];
-      tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + col, v);
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_bf16(acc, umma_desc_kmajor(a_base + k * 32, 128), umma_desc_kmajor(b_base + k * 32, 128), idesc,
+                      (kb > kb0 || k > 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == L::kStages) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) umma_commit(&acc_full[slot]);
+      __syncwarp();
+      if (++slot == kShrinkAccSlots) { slot = 0; aphase ^= 1; }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 5..8)
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int ep_tid = threadIdx.x - 32 * kEpiWarp0;
+    int slot = 0;
+    uint32_t aphase = 0;
+    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+      const int g = find_module(prefix, p.n_mod, item);
+      const ShrinkMod& m = p.mod[g];
+      const int tile = (item - prefix[g]) / m.ks, kc = (item - prefix[g]) % m.ks;
+      const int4 t4 = m.tiles[tile];
+      const int len4 = min(kTileM, (t4.z + 3) & ~3);
+      mbar_wait(&acc_full[slot], aphase);
+      tc_fence_after();
+      float s[RP];
+#pragma unroll
+      for (int c = 0; c < RP; c += 16) tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * L::kSlotCols + c, s + c);
       tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) red[row * (RP + 1) + col + i] = v[i];
-    }
-  }
-  tc_fence_before();
-  cluster_sync();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[slot]);
+      if (++slot == kShrinkAccSlots) { slot = 0; aphase ^= 1; }
 
-  // ---------------- epilogue 2: deterministic split-K reduction through DSMEM
-  const int my_rows = (len4 - q + ks - 1) / ks;     // rows q, q+ks, ... < len4
-  const uint32_t red_base = smem_u32(red);
-  for (int idx = threadIdx.x; idx < my_rows * RP; idx += kShrinkThreads) {
-    const int row = q + (idx / RP) * ks, col = idx % RP;
-    const uint32_t off = red_base + static_cast<uint32_t>((row * (RP + 1) + col) * 4);
-    float sum = 0.f;
-    for (int p = 0; p < ks; ++p) sum += ld_dsmem_f32(mapa_shared(off, p));
-    sred[row * (RP + 1) + col] = sum;
+      bool finisher = true;
+      if (m.ks > 1) {
+        // split-K: publish this chunk's partial, the last arriving CTA reduces in kc order
+        if (row < len4) {
+          float4* dst = reinterpret_cast<float4*>(m.ws + (static_cast<size_t>(kc) * m.ws_rows + tile * kTileM + row) * RP);
+#pragma unroll
+          for (int c = 0; c < RP / 4; ++c) dst[c] = make_float4(s[4 * c], s[4 * c + 1], s[4 * c + 2], s[4 * c + 3]);
+        }
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (ep_tid == 0) *s_last = (atomicAdd(&m.counters[tile], 1) == m.ks - 1);
+        named_bar_sync(1, 128);
+        finisher = *s_last != 0;
+        if (finisher) {
+          __threadfence();
+          if (row < len4) {
+#pragma unroll
+            for (int c = 0; c < RP; ++c) s[c] = 0.f;
+            for (int q = 0; q < m.ks; ++q) {
+              const float4* src = reinterpret_cast<const float4*>(
+                  m.ws + (static_cast<size_t>(q) * m.ws_rows + tile * kTileM + row) * RP);
+#pragma unroll
+              for (int c = 0; c < RP / 4; ++c) {
+                const float4 v = __ldcg(src + c);
+                s[4 * c] += v.x; s[4 * c + 1] += v.y; s[4 * c + 2] += v.z; s[4 * c + 3] += v.w;
+              }
+            }
+          }
+          if (ep_tid == 0) m.counters[tile] = 0;       // ready for the next launch
+        }
+      }
+      if (finisher && row < len4) {
+        // t = scale * Sigma_i s ; thread = token row
+        const int adapter = p.tok_adapter[m.perm[t4.y + min(row, t4.z - 1)]];
+        const uint4* srow = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
+        __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP);
+#pragma unroll 1
+        for (int o0 = 0; o0 < RP; o0 += 8) {
+          float t8[8];
+#pragma unroll
+          for (int oo = 0; oo < 8; ++oo) {
+            const int o = o0 + oo;
+            float acc = 0.f;
+#pragma unroll
+            for (int v8 = 0; v8 < RP / 8; ++v8) {
+              const uint4 w = __ldg(srow + (o * RP) / 8 + v8);
+              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                acc = fmaf(f.x, s[v8 * 8 + 2 * e], acc);
+                acc = fmaf(f.y, s[v8 * 8 + 2 * e + 1], acc);
+              }
+            }
+            t8[oo] = acc * m.scale;
+          }
+          uint4 hi, lo;
+          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&hi);
+          __nv_bfloat162* ll = reinterpret_cast<__nv_bfloat162*>(&lo);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(t8[2 * e], t8[2 * e + 1]);
+            const float2 hf = __bfloat1622float2(h2);
+            hh[e] = h2;
+            ll[e] = __floats2bfloat162_rn(t8[2 * e] - hf.x, t8[2 * e + 1] - hf.y);
+          }
+          *reinterpret_cast<uint4*>(dst + o0) = hi;
+          *reinterpret_cast<uint4*>(dst + RP + o0) = lo;
+        }
+      }
+    }
   }
   __syncthreads();
-
-  // ---------------- epilogue 3: t = scale * Sigma_i s  -> bf16 hi/lo
-  for (int idx = threadIdx.x; idx < my_rows * RP; idx += kShrinkThreads) {
-    const int row = q + (idx / RP) * ks, o = idx % RP;
-    const int adapter = a.tok_adapter[rows[row]];
-    const uint4* srow = reinterpret_cast<const uint4*>(a.sigma + (static_cast<size_t>(adapter) * RP + o) * RP);
-    const float* sv = sred + row * (RP + 1);
-    float t = 0.f;
-#pragma unroll
-    for (int v8 = 0; v8 < RP / 8; ++v8) {
-      const uint4 w = __ldg(srow + v8);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h[e]);
-        t = fmaf(f.x, sv[v8 * 8 + 2 * e], t);
-        t = fmaf(f.y, sv[v8 * 8 + 2 * e + 1], t);
-      }
-    }
-    t *= a.scale;
-    const __nv_bfloat16 hi = __float2bfloat16_rn(t);
-    const __nv_bfloat16 lo = __float2bfloat16_rn(t - __bfloat162float(hi));
-    __nv_bfloat16* dst = a.tbuf + (static_cast<size_t>(tile_idx) * kTileM + row) * (2 * RP);
-    dst[o] = hi;
-    dst[RP + o] = lo;
-  }
-
-  cluster_sync();                                  // remote reads of `red` are done
-  if (warp == 2) tmem_dealloc<L::kTmemCols>(tmem);
+  if (warp == kMmaWarp) tmem_dealloc<L::kTmemCols>(tmem);
 }
 
 }  // namespace cts

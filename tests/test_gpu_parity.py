@@ -286,3 +286,31 @@ def test_host_validation(cts):
     with pytest.raises(cts.CtsError):
         plan.segment(torch.zeros(9, dtype=torch.int32, device="cuda"))     # T > T_max
     assert bank.bytes > 0 and bank.params(0) == 1 * (64 + 64) * 4 + 4 * 16
+
+
+def test_grouped_qkv_shared_x_and_mlp(cts):
+    """cts_apply_group: q,k,v in one launch pair reading one x; gate,up in another; per-module maps."""
+    N, C, r, T = 200, 6, 16, 777
+    shapes = [(512, 512), (512, 128), (512, 128), (512, 1024), (512, 1024)]
+    banks, f64s = [], []
+    for m, (di, do) in enumerate(shapes):
+        b, f = quantized_bank(di, do, N, C, r, seed=300 + m, cluster_of=cluster_map(N, C, 400 + m))
+        banks.append(b)
+        f64s.append(f)
+    bank = make_bank(cts, banks)
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, N, 31, frac_none=0.05)
+    plan.segment(torch.from_numpy(ta).cuda())
+    xa = bf16_round(activations(T, 512, 32))
+    xm = bf16_round(activations(T, 512, 33))
+    x_attn, x_mlp = dev_bf16(xa), dev_bf16(xm)
+    ys = [torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes]
+    plan.apply_group([0, 1, 2], [x_attn] * 3, ys[:3], 2.0)
+    plan.apply_group([3, 4], [x_mlp] * 2, ys[3:], 2.0)
+    torch.cuda.synchronize()
+    for m in range(5):
+        check_delta(ta, host_bits(ys[m]), f64s[m], xa if m < 3 else xm, 2.0)
+    with pytest.raises(cts.CtsError):                                      # repeated module
+        plan.apply_group([0, 0], [x_attn] * 2, ys[:2], 1.0)
+    with pytest.raises(cts.CtsError):                                      # y aliases another y
+        plan.apply_group([1, 2], [x_attn] * 2, [ys[1], ys[1]], 1.0)
