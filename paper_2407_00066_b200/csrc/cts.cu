@@ -134,6 +134,8 @@ struct cts_plan_s {
   int32_t* offsets;       // [n_maps][C+1]
   int4* tiles;            // [n_maps][max_tiles]
   int32_t* n_tiles;       // [n_maps]
+  int32_t* tile_rows;     // [n_maps][max_tiles*128]
+  int32_t* tile_adapters; // [n_maps][max_tiles*128]
   int32_t* err;           // [2]
   __nv_bfloat16* tbuf;    // [n_modules][max_tiles*128][2*rp]  rank-r intermediate (t hi | t lo)
   CUtensorMap* d_tm_t;    // [n_modules] device copies
@@ -157,7 +159,16 @@ bool aligned16(const T* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-constexpr int kTargetItemsPerSM = 3;
+constexpr int kTargetItemsPerSMMax = 4;   // sizes the split-K workspace
+
+// split-K target (tuning aid): CTS_ITEMS_PER_SM shrink work items per SM per launch
+int target_items_per_sm() {
+  static int v = [] {
+    const char* e = std::getenv("CTS_ITEMS_PER_SM");
+    return e ? std::max(1, std::min(kTargetItemsPerSMMax, std::atoi(e))) : 2;
+  }();
+  return v;
+}
 
 template <int RP>
 cudaError_t set_kernel_attrs() {
@@ -169,30 +180,37 @@ cudaError_t set_kernel_attrs() {
   return once;
 }
 
-template <int RP, int BN, bool EAGER>
+template <int RP>
 cudaError_t set_expand_attrs() {
-  static cudaError_t once = cudaFuncSetAttribute(expand_kernel<RP, BN, EAGER>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, ExpandCfg<RP, BN>::kBytes);
+  static cudaError_t once = cudaFuncSetAttribute(expand_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 ExpandCfg<RP>::kBytes);
   return once;
 }
 
-// expand variant knob (tuning aid): CTS_EXPAND_VARIANT = 0 (BN 128, lazy release), 1 (BN 128,
-// eager), 2 (BN 64, lazy), 3 (BN 64, eager).
-int expand_variant() {
-  static int v = [] {
-    const char* e = std::getenv("CTS_EXPAND_VARIANT");
-    return e ? (std::atoi(e) & 3) : 1;   // measured best: BN 128, eager release
-  }();
-  return v;
+// Launch with programmatic stream serialization (PDL): the kernel may start while the previous
+// kernel in the stream drains; every kernel calls griddep_wait() before touching dependent data.
+template <typename Kern, typename... Args>
+cudaError_t launch_pdl(Kern kernel, int grid, int block, size_t smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 __nv_bfloat16* module_tbuf(cts_plan_t p, int module) {
   return p->tbuf + size_t(module) * p->max_tiles * kTileM * 2 * p->bank->rp;
 }
 
-// K chunks per tile for a group: aim for >= kTargetItemsPerSM items per SM, each >= 4 K blocks.
+// K chunks per tile for a group: aim for ~target_items_per_sm() items per SM, each >= 4 K blocks.
 int choose_ks(int tiles_total, int min_kblocks) {
-  const int want = (kTargetItemsPerSM * sm_count() + tiles_total - 1) / std::max(tiles_total, 1);
+  const int want = (target_items_per_sm() * sm_count() + tiles_total - 1) / std::max(tiles_total, 1);
   return std::max(1, std::min({want, 16, std::max(1, min_kblocks / 4)}));
 }
 
@@ -210,7 +228,7 @@ cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const vo
   ShrinkParams prm;
   std::memset(&prm, 0, sizeof(prm));
   prm.n_mod = n;
-  prm.tok_adapter = p->tok_adapter;
+  prm.prefix[0] = 0;
   for (int i = 0; i < n; ++i) {
     const Module& m = b->mods[modules[i]];
     ShrinkMod& sm = prm.mod[i];
@@ -219,7 +237,8 @@ cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const vo
     const size_t mid = m.map_id;
     sm.tiles = p->tiles + mid * p->max_tiles;
     sm.n_tiles = p->n_tiles + mid;
-    sm.perm = p->perm + mid * p->T_max;
+    sm.tile_rows = p->tile_rows + mid * p->max_tiles * kTileM;
+    sm.tile_adapters = p->tile_adapters + mid * p->max_tiles * kTileM;
     sm.sigma = m.sigma;
     sm.tbuf = module_tbuf(p, modules[i]);
     sm.ws = p->ws + size_t(i) * p->ws_cap_rows * b->rp;
@@ -228,24 +247,24 @@ cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const vo
     sm.ks = ks;
     sm.ws_rows = tiles_bound * kTileM;
     sm.scale = scale;
+    prm.prefix[i + 1] = prm.prefix[i] + tiles_bound * ks;
   }
   const int grid = std::min(sm_count(), tiles_bound * n * ks);
-  shrink_sigma_kernel<RP><<<grid, kShrinkThreads, ShrinkCfg<RP>::kBytes, stream>>>(prm);
-  CTS_CUDA(cudaGetLastError());
+  CTS_CUDA(launch_pdl(shrink_sigma_kernel<RP>, grid, kShrinkThreads, ShrinkCfg<RP>::kBytes, stream, prm));
   return CTS_OK;
 }
 
-template <int RP, int BN, bool EAGER>
+template <int RP>
 cts_status_t launch_expand(cts_plan_t p, int n, const int32_t* modules, void* const* ys, const int64_t* ld_y,
                            cudaStream_t stream) {
   const cts_bank_t b = p->bank;
   const int T = p->T;
   const int tiles_bound = cts_plan_max_tiles(p, T);
-  CTS_CUDA((set_expand_attrs<RP, BN, EAGER>()));
+  CTS_CUDA(set_expand_attrs<RP>());
   ExpandParams prm;
   std::memset(&prm, 0, sizeof(prm));
   prm.n_mod = n;
-  int items = 0;
+  prm.prefix[0] = 0;
   for (int i = 0; i < n; ++i) {
     const Module& m = b->mods[modules[i]];
     ExpandMod& em = prm.mod[i];
@@ -255,14 +274,13 @@ cts_status_t launch_expand(cts_plan_t p, int n, const int32_t* modules, void* co
     const size_t mid = m.map_id;
     em.tiles = p->tiles + mid * p->max_tiles;
     em.n_tiles = p->n_tiles + mid;
-    em.perm = p->perm + mid * p->T_max;
-    em.nblk = (m.d_out + BN - 1) / BN;
+    em.tile_rows = p->tile_rows + mid * p->max_tiles * kTileM;
+    em.nblk = (m.d_out + kBN - 1) / kBN;
     em.d_out = m.d_out;
-    items += tiles_bound * em.nblk;
+    prm.prefix[i + 1] = prm.prefix[i] + tiles_bound * em.nblk;
   }
-  const int grid = std::min(sm_count(), items);
-  expand_kernel<RP, BN, EAGER><<<grid, kExpandThreads, ExpandCfg<RP, BN>::kBytes, stream>>>(prm);
-  CTS_CUDA(cudaGetLastError());
+  const int grid = std::min(sm_count(), prm.prefix[n]);
+  CTS_CUDA(launch_pdl(expand_kernel<RP>, grid, kExpandThreads, ExpandCfg<RP>::kBytes, stream, prm));
   return CTS_OK;
 }
 
@@ -291,21 +309,11 @@ cts_status_t do_shrink(cts_plan_t p, int n, const int32_t* mods, const void* con
   }
 }
 
-template <int RP>
-cts_status_t expand_rp(cts_plan_t p, int n, const int32_t* mods, void* const* ys, const int64_t* ld, cudaStream_t s) {
-  switch (expand_variant()) {
-    case 1: return launch_expand<RP, 128, true>(p, n, mods, ys, ld, s);
-    case 2: return launch_expand<RP, 64, false>(p, n, mods, ys, ld, s);
-    case 3: return launch_expand<RP, 64, true>(p, n, mods, ys, ld, s);
-    default: return launch_expand<RP, 128, false>(p, n, mods, ys, ld, s);
-  }
-}
-
 cts_status_t do_expand(cts_plan_t p, int n, const int32_t* mods, void* const* ys, const int64_t* ld, cudaStream_t s) {
   switch (p->bank->rp) {
-    case 16: return expand_rp<16>(p, n, mods, ys, ld, s);
-    case 32: return expand_rp<32>(p, n, mods, ys, ld, s);
-    default: return expand_rp<64>(p, n, mods, ys, ld, s);
+    case 16: return launch_expand<16>(p, n, mods, ys, ld, s);
+    case 32: return launch_expand<32>(p, n, mods, ys, ld, s);
+    default: return launch_expand<64>(p, n, mods, ys, ld, s);
   }
 }
 
@@ -470,7 +478,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->T = 0;
   p->max_tiles = cts_plan_max_tiles(p, T_max);
   // split-K workspace rows per group slot: ks * tiles_bound * 128 <= (target items + tiles) * 128
-  p->ws_cap_rows = size_t(kTargetItemsPerSM * sm_count() + p->max_tiles) * kTileM;
+  p->ws_cap_rows = size_t(kTargetItemsPerSMMax * sm_count() + p->max_tiles) * kTileM;
   const size_t nm = b->n_maps;
   size_t off = 0;
   const size_t o_tok = off; off = align_up(off + size_t(T_max) * 4, 256);
@@ -478,6 +486,8 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   const size_t o_offs = off; off = align_up(off + nm * (b->C + 1) * 4, 256);
   const size_t o_tiles = off; off = align_up(off + nm * p->max_tiles * 16, 256);
   const size_t o_nt = off; off = align_up(off + nm * 4, 256);
+  const size_t o_trows = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
+  const size_t o_tads = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
   const size_t o_err = off; off = align_up(off + 16, 256);
   const size_t o_cnt = off; off = align_up(off + size_t(kMaxGroup) * p->max_tiles * 4, 1024);
   const size_t o_tm = off; off = align_up(off + size_t(b->n_modules) * sizeof(CUtensorMap), 1024);
@@ -490,6 +500,8 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->offsets = reinterpret_cast<int32_t*>(base + o_offs);
   p->tiles = reinterpret_cast<int4*>(base + o_tiles);
   p->n_tiles = reinterpret_cast<int32_t*>(base + o_nt);
+  p->tile_rows = reinterpret_cast<int32_t*>(base + o_trows);
+  p->tile_adapters = reinterpret_cast<int32_t*>(base + o_tads);
   p->err = reinterpret_cast<int32_t*>(base + o_err);
   p->counters = reinterpret_cast<int32_t*>(base + o_cnt);
   p->d_tm_t = reinterpret_cast<CUtensorMap*>(base + o_tm);
@@ -497,6 +509,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->tbuf = reinterpret_cast<__nv_bfloat16*>(base + o_t);
   const int32_t init_err[2] = {0, -1};
   bool ok = cudaMemset(p->n_tiles, 0, nm * 4) == cudaSuccess &&
+            cudaMemset(p->tiles, 0, nm * p->max_tiles * 16) == cudaSuccess &&
             cudaMemset(p->counters, 0, size_t(kMaxGroup) * p->max_tiles * 4) == cudaSuccess &&
             cudaMemcpy(p->err, init_err, 8, cudaMemcpyHostToDevice) == cudaSuccess;
   std::vector<CUtensorMap> h_tm(b->n_modules);
@@ -533,6 +546,8 @@ cts_status_t cts_segment(cts_plan_t p, const int32_t* token_adapter, int32_t T, 
   a.offsets = p->offsets;
   a.tiles = p->tiles;
   a.n_tiles = p->n_tiles;
+  a.tile_rows = p->tile_rows;
+  a.tile_adapters = p->tile_adapters;
   a.err = p->err;
   a.T = T;
   a.T_max = p->T_max;
@@ -542,8 +557,7 @@ cts_status_t cts_segment(cts_plan_t p, const int32_t* token_adapter, int32_t T, 
   static const cudaError_t seg_attr = cudaFuncSetAttribute(
       segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (kSegWarps + 2) * 1024 * 4);
   CTS_CUDA(seg_attr);
-  segment_kernel<<<b->n_maps, kSegThreads, (kSegWarps + 2) * b->C * 4, stream>>>(a);
-  CTS_CUDA(cudaGetLastError());
+  CTS_CUDA(launch_pdl(segment_kernel, b->n_maps, kSegThreads, size_t(kSegWarps + 2) * b->C * 4, stream, a));
   p->T = T;
   return CTS_OK;
 }
@@ -626,6 +640,13 @@ cts_status_t cts_apply(cts_plan_t p, int32_t module, const void* x, int64_t ld_x
                        cudaStream_t stream) {
   return cts_apply_group(p, 1, &module, &x, &ld_x, &y, &ld_y, scale, stream);
 }
+
+#ifdef CTS_TRACE
+// debug-only (not part of cts.h): copy the per-CTA timeline of the last traced launch
+int cts_debug_trace(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_cts_trace, std::min<size_t>(n, sizeof(g_cts_trace) / 8) * 8) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 cts_status_t cts_plan_error(cts_plan_t p, int32_t* code, int32_t* first_bad_token) {
   if (!p || !code || !first_bad_token) return CTS_ERR_INVALID_ARGUMENT;

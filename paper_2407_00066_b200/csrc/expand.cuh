@@ -5,20 +5,21 @@
 // update y" with `scale` -- here scale was already folded into t by kernel 1.
 //
 // Persistent, grouped (same scheme as the shrink): one CTA per SM walks a static round-robin list
-// of work items item = (module g, 128-token tile, BN-column block of d_out):
+// of work items item = (module g, 128-token tile slot, BN-column block of d_out), laid out over the
+// host-known tile bound (empty slots skipped):
 //   warps 0-3   TMA producers (items dealt round-robin, one warp's gather4 issue rate is not
 //               enough): t_hi / t_lo tile (A operand, K-major), the out_basis block (B operand,
 //               K-major) and the tile's y rows gathered by token index (tile::gather4, 64-column
-//               segments, 128B swizzle) into a kStages-deep ring -- y streams in while earlier
-//               items are multiplied and stored.  The producer also leaves the item's token rows
-//               and tile descriptor in the stage, so the epilogue never waits on L2.
+//               segments, 128B swizzle) into a kStages-deep ring.  The producer also leaves the
+//               item's token rows and tile descriptor in the stage.
 //   warp 4      one lane issues D = t_hi U^T + t_lo U^T (M=128 tokens, N=BN, K=16 per MMA) into
 //               one of kAccSlots TMEM accumulators.
 //   warps 5-12  epilogue: two sets of 4 warps take alternate items; in a set each warp owns one
-//               32-row quarter (its TMEM lanes), thread = token row: tcgen05.ld 64 fp32 columns at
-//               a time, add y_base from smem, round to bf16 (RNE) in place, then the warp itself
-//               TMA-scatters its 8 four-row groups to y.  A stage is released when the set's 4
-//               warps have seen their scatters read it (bulk-group wait, one item behind).
+//               32-row quarter (its TMEM lanes).  Thread = token row: tcgen05.ld 64 fp32 columns at
+//               a time, add y_base from smem, round to bf16 (RNE) in place; then the warp itself
+//               TMA-scatters its 8 four-row groups to y and releases the stage as soon as the
+//               scatter has read it (eager release; measured faster than deferring the release by
+//               an item, and faster than coalesced STG row stores from smem).
 #pragma once
 #include "sm100.cuh"
 #include "segment.cuh"
@@ -26,49 +27,47 @@
 
 namespace cts {
 
-constexpr int kEpiSets = 2;
 constexpr int kExpandThreads = 32 * (kProducerWarps + 1 + 4 * kEpiSets);
-constexpr int kBNMax = 128;              // largest d_out block per work item
+constexpr int kBN = 128;                 // d_out columns per work item
 constexpr int kExpandAccSlots = 4;       // 4 x 128 fp32 columns = all of TMEM
 
 struct alignas(64) ExpandMod {
   CUtensorMap tm_y;                      // y [T][d_out], box {64, 1}, 128B swizzle (per call)
   const CUtensorMap* tm_t;               // tbuf [max_tiles*128][2*rp], box {rp, 128} (plan, global mem)
   const CUtensorMap* tm_out;             // out_basis [C*d_out][rp], box {rp, 64} (bank, global mem)
-  const int4* tiles;
-  const int32_t* n_tiles;
-  const int32_t* perm;
-  int nblk;                              // ceil(d_out / BN)
+  const int4* tiles;                     // (cluster, start, len, -); len 0 = empty slot
+  const int32_t* n_tiles;                // real tile count of this module's map
+  const int32_t* tile_rows;              // [tile*128 + row] token index
+  int nblk;                              // ceil(d_out / kBN)
   int d_out;
 };
 
 struct ExpandParams {
   ExpandMod mod[kMaxGroup];
+  int prefix[kMaxGroup + 1];             // item prefix over modules (tile bound * nblk each)
   int n_mod;
 };
 
-template <int RP, int BN>
+template <int RP>
 struct ExpandCfg {
   static constexpr int kY = kTileM * 128;                    // one 64-column segment of y rows (16 KB)
-  static constexpr int kSeg = BN / 64;
+  static constexpr int kSeg = kBN / 64;
   static constexpr int kA = kTileM * RP * 2;                 // t_hi (or t_lo) tile
-  static constexpr int kB = BN * RP * 2;                     // out_basis block
-  static constexpr int kMeta = kTileM * 4 + 16;              // token rows + (g, tile, nb, len4)
+  static constexpr int kB = kBN * RP * 2;                    // out_basis block
+  static constexpr int kMeta = kTileM * 4 + 16;              // token rows + (g, cluster, nb, len)
   static constexpr int kStage = kSeg * kY + 2 * kA + kB;
-  static constexpr int kStages = (200 * 1024) / (kStage + kMeta);   // rp=16: 4 (BN 128) / 7 (BN 64)
+  static constexpr int kStages = (200 * 1024) / (kStage + kMeta);   // 4 at rp=16, 3 at rp=32, 2 at rp=64
   static constexpr int kOffMeta = kStages * kStage;
   static constexpr int kOffBar = kOffMeta + kStages * kMeta;
   static constexpr int kNumBars = 2 * kStages + 2 * kExpandAccSlots;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kBytes = kOffMisc + 64 + 1024;
-  static constexpr uint32_t kTmemCols = kBNMax * kExpandAccSlots;
+  static constexpr uint32_t kTmemCols = kBN * kExpandAccSlots;
 };
 
-// EAGER: release a stage as soon as this warp's scatter has read it (blocking wait) instead of
-// one item later.
-template <int RP, int BN, bool EAGER>
+template <int RP>
 __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_constant__ ExpandParams p) {
-  using L = ExpandCfg<RP, BN>;
+  using L = ExpandCfg<RP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
@@ -76,12 +75,10 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
   uint64_t* acc_full = empty + L::kStages;
   uint64_t* acc_empty = acc_full + kExpandAccSlots;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);
-  __shared__ int prefix[kMaxGroup + 1];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    prefix[0] = 0;
-    for (int g = 0; g < p.n_mod; ++g) prefix[g + 1] = prefix[g] + *p.mod[g].n_tiles * p.mod[g].nblk;
+    CTS_STAMP(0);
     for (int s = 0; s < L::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 4);            // one arrival per epilogue warp of the owning set
@@ -97,7 +94,14 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int total = prefix[p.n_mod];
+  const int total = p.prefix[p.n_mod];
+  griddep_wait();                         // t (previous kernel) and y are ready past this point
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) CTS_STAMP(1);
+  // real tile count of each module's map: lane g holds module g's (one load per warp); work items
+  // over the tile bound with tile >= count are empty and skipped without touching memory
+  const int nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
+  auto tile_count = [&](int g) { return __shfl_sync(0xffffffffu, nt_lane, g); };
 
   auto stage_y = [&](int s) { return smem + s * L::kStage; };
   auto stage_a = [&](int s) { return smem + s * L::kStage + L::kSeg * L::kY; };
@@ -107,23 +111,23 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
 
   if (warp < kProducerWarps) {
     // ------------------------------------------------------------ TMA producers (items round-robin)
-    int li = 0;
-    for (int item = blockIdx.x; item < total; item += gridDim.x, ++li) {
-      if (li % kProducerWarps != warp) continue;
-      const int stage = li % L::kStages;
-      const uint32_t phase = (li / L::kStages) & 1;
-      const int g = find_module(prefix, p.n_mod, item);
+    int li = 0;                                   // index over this CTA's non-empty items
+    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+      const int g = find_module(p.prefix, p.n_mod, item);
       const ExpandMod& m = p.mod[g];
-      const int tile = (item - prefix[g]) / m.nblk, nb = (item - prefix[g]) % m.nblk;
+      const int tile = (item - p.prefix[g]) / m.nblk, nb = (item - p.prefix[g]) % m.nblk;
+      if (tile >= tile_count(g)) continue;
+      const int my = li++;
+      if (my % kProducerWarps != warp) continue;
       const int4 t4 = m.tiles[tile];
+      const int4 r4 = *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
+      const int stage = my % L::kStages;
+      const uint32_t phase = (my / L::kStages) & 1;
       const int len4 = min(kTileM, (t4.z + 3) & ~3);
       const int ngroups = len4 >> 2;
-      int r4[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) r4[q] = m.perm[t4.y + min(4 * lane + q, t4.z - 1)];
       mbar_wait(&empty[stage], phase ^ 1);
-      *reinterpret_cast<int4*>(stage_rows(stage) + 4 * lane) = make_int4(r4[0], r4[1], r4[2], r4[3]);
-      if (lane == 0) *stage_info(stage) = make_int4(g, t4.x, nb, len4);
+      *reinterpret_cast<int4*>(stage_rows(stage) + 4 * lane) = r4;
+      if (lane == 0) *stage_info(stage) = make_int4(g, t4.x, nb, t4.z);
       __syncwarp();
       if (lane == 0) {
         mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(2 * L::kA + L::kB + L::kSeg * ngroups * 512));
@@ -131,27 +135,31 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
         tma_load_2d(stage_a(stage) + L::kA, m.tm_t, &full[stage], RP, tile * kTileM);
 #pragma unroll
         for (int s = 0; s < L::kSeg; ++s)
-          tma_load_2d(stage_b(stage) + s * 64 * RP * 2, m.tm_out, &full[stage], 0, t4.x * m.d_out + nb * BN + s * 64);
+          tma_load_2d(stage_b(stage) + s * 64 * RP * 2, m.tm_out, &full[stage], 0, t4.x * m.d_out + nb * kBN + s * 64);
       }
       __syncwarp();
       if (lane < ngroups) {
 #pragma unroll
         for (int s = 0; s < L::kSeg; ++s)
-          tma_gather4(stage_y(stage) + s * L::kY + lane * 512, &m.tm_y, &full[stage], nb * BN + s * 64, r4[0], r4[1],
-                      r4[2], r4[3]);
+          tma_gather4(stage_y(stage) + s * L::kY + lane * 512, &m.tm_y, &full[stage], nb * kBN + s * 64, r4.x, r4.y,
+                      r4.z, r4.w);
       }
+      if (lane == 0 && my < 4) CTS_STAMP(10 + my);
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc_bf16(kTileM, BN);
+    constexpr uint32_t idesc = umma_idesc_bf16(kTileM, kBN);
     int stage = 0, slot = 0;
     uint32_t phase = 0, aphase = 0;
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
+      const int g = find_module(p.prefix, p.n_mod, item);
+      const ExpandMod& m = p.mod[g];
+      if ((item - p.prefix[g]) / m.nblk >= tile_count(g)) continue;
       mbar_wait(&acc_empty[slot], aphase ^ 1);
       mbar_wait(&full[stage], phase);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t acc = tmem + slot * kBNMax;
+        const uint32_t acc = tmem + slot * kBN;
         const uint32_t hi = smem_u32(stage_a(stage)), lo = hi + L::kA, b = smem_u32(stage_b(stage));
 #pragma unroll
         for (int k = 0; k < RP / 16; ++k)
@@ -160,6 +168,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
         for (int k = 0; k < RP / 16; ++k)
           umma_bf16(acc, umma_desc_kmajor(lo + k * 32, RP * 2), umma_desc_kmajor(b + k * 32, RP * 2), idesc, 1);
         umma_commit(&acc_full[slot]);
+        if (item == static_cast<int>(blockIdx.x)) CTS_STAMP(14);
       }
       __syncwarp();
       if (++stage == L::kStages) { stage = 0; phase ^= 1; }
@@ -171,27 +180,32 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
     const int set = ew >> 2;
     const int quarter = warp & 3;              // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
-    int prev_stage = -1;
-    int li = set;
-    for (int item = blockIdx.x + set * gridDim.x; item < total; item += kEpiSets * gridDim.x, li += kEpiSets) {
-      const int stage = li % L::kStages, slot = li % kExpandAccSlots;
-      const uint32_t phase = (li / L::kStages) & 1, aphase = (li / kExpandAccSlots) & 1;
+    int li = 0;
+    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+      const int g = find_module(p.prefix, p.n_mod, item);
+      const ExpandMod& m = p.mod[g];
+      if ((item - p.prefix[g]) / m.nblk >= tile_count(g)) continue;
+      const int my = li++;
+      if (my % kEpiSets != set) continue;
+      const int stage = my % L::kStages, slot = my % kExpandAccSlots;
+      const uint32_t phase = (my / L::kStages) & 1, aphase = (my / kExpandAccSlots) & 1;
       mbar_wait(&acc_full[slot], aphase);
       mbar_wait(&full[stage], phase);        // y rows + metadata landed (acquire for this thread)
       tc_fence_after();
-      const int4 info = *stage_info(stage);   // (g, cluster, nb, len4)
-      const int len4 = info.w;
+      const int4 info = *stage_info(stage);   // (g, cluster, nb, len)
+      const int len = info.w;
       uint8_t* ys = stage_y(stage);
-      const bool active = quarter * 32 < len4;   // warp-uniform: this quarter holds valid rows
+      const int len4 = min(kTileM, (len + 3) & ~3);
+      const bool active = quarter * 32 < len;    // warp-uniform: this quarter holds valid rows
       if (active) {
 #pragma unroll 1
-        for (int j2 = 0; j2 < BN / 64; ++j2) {
+        for (int j2 = 0; j2 < kBN / 64; ++j2) {
           float v[64];
-          const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * kBNMax + j2 * 64;
+          const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * kBN + j2 * 64;
           tmem_ld32(taddr, v);
           tmem_ld32(taddr + 32, v + 32);
           tmem_ld_wait();
-          if (row < len4) {
+          if (row < len4) {                  // rows len..len4 duplicate the last token: identical bytes
             uint8_t* base = ys + j2 * L::kY + row * 128;   // 64 columns = one segment
 #pragma unroll
             for (int qd = 0; qd < 8; ++qd) {
@@ -212,35 +226,27 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[slot]);
       if (active) {
-        // this warp's 8 four-row groups: lane -> (group, segment)
+        // this warp's 8 four-row groups: lane -> (group, segment); TMA scatter of the rows
         fence_proxy_async_smem();
         __syncwarp();
         const int grp = quarter * 8 + (lane & 7), seg = lane >> 3;
-        if (grp * 4 < len4 && seg < L::kSeg) {
+        if (grp * 4 < len && seg < L::kSeg) {
           const int4 r4 = *reinterpret_cast<const int4*>(stage_rows(stage) + 4 * grp);
-          tma_scatter4(&p.mod[info.x].tm_y, ys + seg * L::kY + grp * 512, info.z * BN + seg * 64, r4.x, r4.y, r4.z,
+          tma_scatter4(&p.mod[info.x].tm_y, ys + seg * L::kY + grp * 512, info.z * kBN + seg * 64, r4.x, r4.y, r4.z,
                        r4.w);
         }
+        bulk_commit();
+        bulk_wait_read<0>();                  // the scatter has read this warp's rows out of the stage
       }
-      bulk_commit();
-      if (EAGER) {
-        bulk_wait_read<0>();                  // this item's scatters have read the stage
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-      } else {
-        bulk_wait_read<1>();                  // this warp's previous item has been read out of smem
-        __syncwarp();
-        if (lane == 0 && prev_stage >= 0) mbar_arrive(&empty[prev_stage]);
-        prev_stage = stage;
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (lane == 0 && quarter == 0 && my < 8) CTS_STAMP(2 + my);
     }
-    bulk_wait_read<0>();
-    __syncwarp();
-    if (lane == 0 && prev_stage >= 0) mbar_arrive(&empty[prev_stage]);
     bulk_wait0();                             // this warp's global writes complete before exit
   }
   __syncthreads();
   if (warp == kMmaWarp) tmem_dealloc<L::kTmemCols>(tmem);
+  if (threadIdx.x == 0) CTS_STAMP(15);
 }
 
 }  // namespace cts

@@ -16,6 +16,7 @@
 // within-chunk rank counts lower lanes (= lower token indices) only.
 #pragma once
 #include <cstdint>
+#include "sm100.cuh"
 
 namespace cts {
 
@@ -29,8 +30,10 @@ struct SegArgs {
   const int32_t* maps;           // [n_maps][N]
   int32_t* perm;                 // [n_maps][T_max]
   int32_t* offsets;              // [n_maps][C+1]
-  int4* tiles;                   // [n_maps][max_tiles]  (c, start, len, 0)
+  int4* tiles;                   // [n_maps][max_tiles]  (c, start, len, 0); len = 0 past n_tiles
   int32_t* n_tiles;              // [n_maps]
+  int32_t* tile_rows;            // [n_maps][max_tiles*128] token of each tile row (dup of last past len)
+  int32_t* tile_adapters;        // [n_maps][max_tiles*128] adapter of that token
   int32_t* err;                  // [2] code, first bad token
   int T, T_max, N, C, max_tiles;
 };
@@ -78,6 +81,8 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
   int32_t* offsets = a.offsets + static_cast<size_t>(map_id) * (a.C + 1);
   int4* tiles = a.tiles + static_cast<size_t>(map_id) * a.max_tiles;
 
+  griddep_wait();                                   // previous step's applies still read the plan
+  griddep_launch_dependents();
   if (threadIdx.x == 0) s_bad = 0x7fffffff;
   for (int i = threadIdx.x; i < kSegWarps * a.C; i += kSegThreads) hist[i] = 0;
   __syncthreads();
@@ -90,6 +95,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
   }
   __syncthreads();
   if (s_bad != 0x7fffffff) {                       // poison: no tiles for any module
+    for (int i = threadIdx.x; i < a.max_tiles; i += kSegThreads) tiles[i] = make_int4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
       a.n_tiles[map_id] = 0;
       if (map_id == 0) {
@@ -177,11 +183,24 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
     __syncwarp();
   }
 
-  // D. tile list.
+  // D. tile list (empty descriptors past n_tiles: kernels map work statically over the bound).
   for (int c = threadIdx.x; c < a.C; c += kSegThreads) {
     const int n = cnt[c], base = tile_base[c], off = offsets[c];
     for (int j = 0; j * kTileM < n; ++j)
       tiles[base + j] = make_int4(c, off + j * kTileM, min(kTileM, n - j * kTileM), 0);
+  }
+  for (int i = tcarry + threadIdx.x; i < a.max_tiles; i += kSegThreads) tiles[i] = make_int4(0, 0, 0, 0);
+  __syncthreads();                                 // perm and tiles complete (block scope)
+
+  // E. per-tile row lists: token and adapter of every tile row, so the GEMM kernels fetch a tile's
+  //    rows with one dependent load instead of two.
+  int32_t* trows = a.tile_rows + static_cast<size_t>(map_id) * a.max_tiles * kTileM;
+  int32_t* tads = a.tile_adapters + static_cast<size_t>(map_id) * a.max_tiles * kTileM;
+  for (int i = threadIdx.x; i < tcarry * kTileM; i += kSegThreads) {
+    const int4 tl = tiles[i / kTileM];
+    const int tok = perm[tl.y + min(i % kTileM, tl.z - 1)];
+    trows[i] = tok;
+    tads[i] = a.token_adapter[tok];
   }
 }
 

@@ -7,55 +7,66 @@
 //
 // Persistent, grouped: one launch covers a group of modules (e.g. q,k,v which share x); the grid is
 // one CTA per SM and every CTA walks a static round-robin list of work items
-//     item = (module g, 128-token tile of one cluster, K-chunk kc of d_in)
-// so the TMA ring keeps streaming across item boundaries (no per-tile launch/prologue latency).
+//     item = (module g, 128-token tile slot of one cluster, K-chunk kc of d_in)
+// laid out over the host-known tile BOUND (tile slots past the real count are empty and skipped), so
+// no CTA waits on a device-side count before issuing its first load; the TMA ring keeps streaming
+// across item boundaries.
 //   warps 0-3   TMA producers: x rows gathered by token index (tile::gather4, 128B swizzle) and
 //               the in_basis K-slab (tile) into a kStages-deep mbarrier ring shared by all items;
 //               K blocks are dealt round-robin to the 4 warps because one warp's gather4 issue
 //               rate caps at ~2 TB/s per GPU (measured, profiles/microbench), four reach the
-//               tile-load rate
+//               tile-load rate.  Token rows come from the segment kernel's per-tile row list.
 //   warp 4      one elected lane issues tcgen05.mma (M=128 tokens, N=r_pad, K=16) into one of
 //               kAccSlots TMEM accumulators, commit -> acc_full[slot]
-//   warps 5-8   epilogue, thread = token row (TMEM lane quarter w%4): tcgen05.ld the partial s;
+//   warps 5-12  epilogue, two sets of 4 warps on alternate items, thread = token row (TMEM lane
+//               quarter w%4): tcgen05.ld the partial s;
 //               split-K: the partial goes to an fp32 workspace, the LAST CTA to finish a tile
-//               (per-tile arrival counter) sums the KS partials in kc order (deterministic),
+//               (acq_rel per-tile arrival counter) sums the KS partials in kc order (deterministic),
 //               gathers Sigma_i (L2-resident, 16-byte loads) and writes t = scale*Sigma_i s as a
 //               bf16 hi + lo pair (t ~= hi + lo to ~2^-16 relative) for the expand.
-// Rows of a tile past its length, up to a multiple of 4, duplicate the last valid token, so the
-// expand's 4-row TMA scatter writes identical bytes for duplicates.
+// Rows of a tile past its length, up to a multiple of 4, duplicate the last valid token.
 #pragma once
 #include "sm100.cuh"
 #include "segment.cuh"
 
 namespace cts {
 
+#ifdef CTS_TRACE
+__device__ unsigned long long g_cts_trace[kTraceCtas][kTraceSlots];
+#define CTS_STAMP(slot) do { if (blockIdx.x < kTraceCtas) g_cts_trace[blockIdx.x][slot] = globaltimer(); } while (0)
+#else
+#define CTS_STAMP(slot) do {} while (0)
+#endif
+
 constexpr int kBK = 64;                 // bf16 elements per K block = one 128-byte swizzle row
 constexpr int kMaxGroup = 16;           // modules per grouped launch
 constexpr int kProducerWarps = 4;
 constexpr int kMmaWarp = kProducerWarps;
 constexpr int kEpiWarp0 = kProducerWarps + 1;
-constexpr int kShrinkThreads = 32 * (kProducerWarps + 1 + 4);   // producers, MMA, 4 epilogue warps
+constexpr int kEpiSets = 2;             // epilogue warp-sets working on alternate items
+constexpr int kShrinkThreads = 32 * (kProducerWarps + 1 + 4 * kEpiSets);   // producers, MMA, epilogue
 constexpr int kShrinkAccSlots = 4;
 
 struct alignas(64) ShrinkMod {
   CUtensorMap tm_x;                     // x [T][d_in], box {64, 1}, 128B swizzle (per call)
   const CUtensorMap* tm_in;             // in_basis [C*rp][d_in], box {64, rp} (bank, global mem)
-  const int4* tiles;                    // (cluster, start, len, -)
-  const int32_t* n_tiles;
-  const int32_t* perm;
+  const int4* tiles;                    // (cluster, start, len, -); len 0 = empty slot
+  const int32_t* n_tiles;               // real tile count of this module's map
+  const int32_t* tile_rows;             // [tile*128 + row] token index
+  const int32_t* tile_adapters;         // [tile*128 + row] adapter id
   const __nv_bfloat16* sigma;           // [N][rp][rp], row = out index
   __nv_bfloat16* tbuf;                  // [max_tiles*128][2*rp]  (hi | lo)
-  float* ws;                            // [ks][max_tiles*128][rp] split-K partials
+  float* ws;                            // [ks][ws_rows][rp] split-K partials
   int32_t* counters;                    // [max_tiles] arrivals per tile (self-resetting)
   int kblocks;                          // d_in / 64
   int ks;                               // K chunks per tile
-  int ws_rows;                          // max_tiles * 128
+  int ws_rows;                          // tile bound * 128
   float scale;
 };
 
 struct ShrinkParams {
   ShrinkMod mod[kMaxGroup];
-  const int32_t* tok_adapter;
+  int prefix[kMaxGroup + 1];            // item prefix over modules (tile bound * ks each)
   int n_mod;
 };
 
@@ -74,7 +85,7 @@ struct ShrinkCfg {
   static constexpr uint32_t kTmemCols = kSlotCols * kShrinkAccSlots;   // 128 or 256
 };
 
-// item -> (module g, local index j) through the per-module item prefix sums kept in smem
+// item -> module g through the per-module item prefix sums
 __device__ __forceinline__ int find_module(const int* prefix, int n_mod, int item) {
   int g = 0;
   while (g + 1 < n_mod && item >= prefix[g + 1]) ++g;
@@ -93,20 +104,18 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
   uint64_t* acc_full = empty + L::kStages;
   uint64_t* acc_empty = acc_full + kShrinkAccSlots;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);
-  int* s_last = reinterpret_cast<int*>(smem + L::kOffMisc + 16);
-  __shared__ int prefix[kMaxGroup + 1];
+  int* s_last = reinterpret_cast<int*>(smem + L::kOffMisc + 16);   // [kEpiSets]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    prefix[0] = 0;
-    for (int g = 0; g < p.n_mod; ++g) prefix[g + 1] = prefix[g] + *p.mod[g].n_tiles * p.mod[g].ks;
+    CTS_STAMP(0);
     for (int s = 0; s < L::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kShrinkAccSlots; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], 4);       // one arrival per epilogue warp
+      mbar_init(&acc_empty[s], 4);       // one arrival per epilogue warp of the owning set
     }
     fence_barrier_init();
   }
@@ -115,24 +124,31 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int total = prefix[p.n_mod];
+  const int total = p.prefix[p.n_mod];
+  // the prologue above overlaps the previous kernel's tail under PDL; everything below reads data
+  // produced by earlier kernels in the stream
+  griddep_wait();
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) CTS_STAMP(1);
+  // real tile count of each module's map: lane g holds module g's (one load per warp); work items
+  // over the tile bound with tile >= count are empty and skipped without touching memory
+  const int nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
+  auto tile_count = [&](int g) { return __shfl_sync(0xffffffffu, nt_lane, g); };
 
   if (warp < kProducerWarps) {
     // ------------------------------------------------------------ TMA producers (K blocks dealt round-robin)
-    int li = 0;
+    int li = 0;                                   // K-block sequence index over this CTA's items
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
-      const int g = find_module(prefix, p.n_mod, item);
+      const int g = find_module(p.prefix, p.n_mod, item);
       const ShrinkMod& m = p.mod[g];
-      const int tile = (item - prefix[g]) / m.ks, kc = (item - prefix[g]) % m.ks;
+      const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
+      if (tile >= tile_count(g)) continue;        // empty tile slot
       const int4 t4 = m.tiles[tile];
+      const int4 r4 = *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
       const int len4 = min(kTileM, (t4.z + 3) & ~3);
       const int ngroups = len4 >> 2;
       const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
       const uint32_t bytes = static_cast<uint32_t>(ngroups * 512 + L::kB);
-      // token rows of this tile (4 per lane, clamped duplicates past len)
-      int r4[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) r4[q] = m.perm[t4.y + min(4 * lane + q, t4.z - 1)];
       for (int kb = kb0; kb < kb1; ++kb, ++li) {
         if (li % kProducerWarps != warp) continue;
         const int stage = li % L::kStages;
@@ -141,19 +157,22 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
         if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
         __syncwarp();
         uint8_t* dA = sA + stage * L::kA;
-        if (lane < ngroups) tma_gather4(dA + lane * 512, &m.tm_x, &full[stage], kb * kBK, r4[0], r4[1], r4[2], r4[3]);
+        if (lane < ngroups) tma_gather4(dA + lane * 512, &m.tm_x, &full[stage], kb * kBK, r4.x, r4.y, r4.z, r4.w);
         if (lane == 0) tma_load_2d(sB + stage * L::kB, m.tm_in, &full[stage], kb * kBK, t4.x * RP);
+        if (li == 0 && lane == 0) CTS_STAMP(2);
       }
     }
+    if (lane == 0 && warp == 0) CTS_STAMP(3);
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = umma_idesc_bf16(kTileM, RP);
     int stage = 0, slot = 0;
     uint32_t phase = 0, aphase = 0;
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
-      const int g = find_module(prefix, p.n_mod, item);
+      const int g = find_module(p.prefix, p.n_mod, item);
       const ShrinkMod& m = p.mod[g];
-      const int kc = (item - prefix[g]) % m.ks;
+      const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
+      if (tile >= tile_count(g)) continue;
       const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
       mbar_wait(&acc_empty[slot], aphase ^ 1);
       tc_fence_after();
@@ -161,6 +180,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (kb == kb0 && lane == 0 && item == static_cast<int>(blockIdx.x)) CTS_STAMP(4);
         if (lane == 0) {
           const uint32_t a_base = smem_u32(sA + stage * L::kA);
           const uint32_t b_base = smem_u32(sB + stage * L::kB);
@@ -175,23 +195,33 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
       }
       if (lane == 0) umma_commit(&acc_full[slot]);
       __syncwarp();
+      if (lane == 0) CTS_STAMP(5);
       if (++slot == kShrinkAccSlots) { slot = 0; aphase ^= 1; }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 5..8)
-    const int quarter = warp & 3;
+    // ------------------------------------------------------------ epilogue (2 sets x 4 warps, alternate items)
+    const int ew = warp - kEpiWarp0;          // 0..7
+    const int set = ew >> 2;
+    const int quarter = warp & 3;              // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
-    const int ep_tid = threadIdx.x - 32 * kEpiWarp0;
-    int slot = 0;
-    uint32_t aphase = 0;
+    const int set_tid = (ew & 3) * 32 + lane;  // 0..127 within the set
+    int li = 0;                                // index over this CTA's non-empty items
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
-      const int g = find_module(prefix, p.n_mod, item);
+      const int g = find_module(p.prefix, p.n_mod, item);
       const ShrinkMod& m = p.mod[g];
-      const int tile = (item - prefix[g]) / m.ks, kc = (item - prefix[g]) % m.ks;
+      const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
+      if (tile >= tile_count(g)) continue;
+      const bool mine = (li % kEpiSets) == set;
+      const int slot = li % kShrinkAccSlots;
+      const uint32_t aphase = (li / kShrinkAccSlots) & 1;
+      ++li;
+      if (!mine) continue;
       const int4 t4 = m.tiles[tile];
       const int len4 = min(kTileM, (t4.z + 3) & ~3);
+      const int adapter = row < len4 ? m.tile_adapters[tile * kTileM + row] : 0;
       mbar_wait(&acc_full[slot], aphase);
       tc_fence_after();
+      if (set_tid == 0) CTS_STAMP(li <= kEpiSets ? 6 : 7);
       float s[RP];
 #pragma unroll
       for (int c = 0; c < RP; c += 16) tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * L::kSlotCols + c, s + c);
@@ -199,23 +229,25 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[slot]);
-      if (++slot == kShrinkAccSlots) { slot = 0; aphase ^= 1; }
 
       bool finisher = true;
       if (m.ks > 1) {
-        // split-K: publish this chunk's partial, the last arriving CTA reduces in kc order
+        // split-K: publish this chunk's partial; the LAST arriving CTA (acq_rel counter) sums the
+        // ks partials in kc order, so the result does not depend on scheduling
         if (row < len4) {
           float4* dst = reinterpret_cast<float4*>(m.ws + (static_cast<size_t>(kc) * m.ws_rows + tile * kTileM + row) * RP);
 #pragma unroll
           for (int c = 0; c < RP / 4; ++c) dst[c] = make_float4(s[4 * c], s[4 * c + 1], s[4 * c + 2], s[4 * c + 3]);
         }
-        __threadfence();
-        named_bar_sync(1, 128);
-        if (ep_tid == 0) *s_last = (atomicAdd(&m.counters[tile], 1) == m.ks - 1);
-        named_bar_sync(1, 128);
-        finisher = *s_last != 0;
+        named_bar_sync(1 + set, 128);
+        if (set_tid == 0) {
+          CTS_STAMP(8);
+          s_last[set] = (atom_add_acq_rel_gpu(&m.counters[tile], 1) == m.ks - 1);
+          CTS_STAMP(9);
+        }
+        named_bar_sync(1 + set, 128);
+        finisher = s_last[set] != 0;
         if (finisher) {
-          __threadfence();
           if (row < len4) {
 #pragma unroll
             for (int c = 0; c < RP; ++c) s[c] = 0.f;
@@ -229,12 +261,11 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
               }
             }
           }
-          if (ep_tid == 0) m.counters[tile] = 0;       // ready for the next launch
+          if (set_tid == 0) m.counters[tile] = 0;       // ready for the next launch
         }
       }
       if (finisher && row < len4) {
         // t = scale * Sigma_i s ; thread = token row
-        const int adapter = p.tok_adapter[m.perm[t4.y + min(row, t4.z - 1)]];
         const uint4* srow = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
         __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP);
 #pragma unroll 1
@@ -273,8 +304,10 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
       }
     }
   }
+  if (threadIdx.x == 32 * kEpiWarp0) CTS_STAMP(10);
   __syncthreads();
   if (warp == kMmaWarp) tmem_dealloc<L::kTmemCols>(tmem);
+  if (threadIdx.x == 0) CTS_STAMP(11);
 }
 
 }  // namespace cts

@@ -201,4 +201,32 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t cluster_addr) {
   return v;
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// griddep_wait: block until the preceding kernel in the stream has completed and its memory is
+// visible (no-op when launched without the PDL attribute).  griddep_launch_dependents: allow the
+// next kernel to be scheduled now (its CTAs run their prologue, then block in griddep_wait).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ global synchronization
+// Fetch-and-add with acquire-release semantics at GPU scope: publishes this CTA's prior writes
+// (cumulatively, after a CTA barrier) and acquires the other arrivals' writes -- no SC fence.
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* addr, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
+  return old;
+}
+
+// ------------------------------------------------------------------ debug timeline (off unless traced)
+// A kernel built with CTS_TRACE records %globaltimer stamps per CTA into g_cts_trace[cta][slot].
+constexpr int kTraceSlots = 16;
+constexpr int kTraceCtas = 160;
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 }  // namespace cts
