@@ -75,6 +75,20 @@ def aggregate(values_ms, units_per_rank, world):
     return units_per_rank * world / (t / 1e3), t
 
 
+def rank_seeds(rank):
+    """Data-parallel request sharding: every rank draws its own token stream and activations; the
+    bank seeds are shared (replicated bank)."""
+    return {"tokens": 1 + rank, "activations": 2 + rank, "bank": 0}
+
+
+def reduce_max(values, dist, device):
+    """Max over ranks of per-rank timings (one all-reduce; the only collective of the bench)."""
+    import torch
+    t = torch.tensor(values, device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -270,8 +284,9 @@ def run_gpu(args, cfg):
     del srcs
     torch.cuda.empty_cache()
     # --- this rank's batch (request sharding: its own token stream) and activations
-    tokens = tokens_torch(T, N, 1 + rank, cfg["prefill"], dev)
-    g = torch.Generator(device=dev).manual_seed(2 + rank)
+    seeds = rank_seeds(rank)
+    tokens = tokens_torch(T, N, seeds["tokens"], cfg["prefill"], dev)
+    g = torch.Generator(device=dev).manual_seed(seeds["activations"])
     xs, ys = [], []
     xbuf = {}
     for (layer, name, di, do) in mods:
@@ -396,9 +411,7 @@ def run_gpu(args, cfg):
     # --- aggregate over ranks
     per_step = ms_total / args.steps
     if world > 1:
-        t = torch.tensor([per_step, ms_e2e, ms_shrink, ms_expand], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        per_step, ms_e2e, ms_shrink, ms_expand = t.tolist()
+        per_step, ms_e2e, ms_shrink, ms_expand = reduce_max([per_step, ms_e2e, ms_shrink, ms_expand], dist, dev)
     value = T * world / (per_step / 1e3)
     e2e_value = T * world / (ms_e2e / 1e3)
 
