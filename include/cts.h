@@ -110,7 +110,9 @@ cts_status_t cts_segment(cts_plan_t plan, const int32_t* token_adapter, int32_t 
 
 /* Test hook: copy module m's segmentation to HOST buffers after the segment completed.
  * perm: host int32 [T] (entries past the bound count are unspecified), offsets: host int32
- * [C+1], tiles: host int32 [max_tiles*3] as (cluster, start, len) rows, n_tiles: host int32.
+ * [C+1], tiles: host int32 [max_tiles*3] as (cluster, start, len) rows -- the logical 128-token
+ * tiles in cluster order (on device they are packed two-per-slot when <= 64 tokens), n_tiles:
+ * host int32 count of those tiles.
  * Any output pointer may be NULL.  Synchronizes the stream. */
 cts_status_t cts_segment_readback(cts_plan_t plan, int32_t module, int32_t* perm, int32_t* offsets,
                                   int32_t* tiles, int32_t* n_tiles, cudaStream_t stream);

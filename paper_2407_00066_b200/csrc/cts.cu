@@ -235,7 +235,7 @@ cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const vo
     if (!make_tmap(&sm.tm_x, xs[i], m.d_in, T, ld_x[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
     sm.tm_in = b->d_tm_in + modules[i];
     const size_t mid = m.map_id;
-    sm.tiles = p->tiles + mid * p->max_tiles;
+    sm.tiles = p->tiles + mid * p->max_tiles * 2;
     sm.n_tiles = p->n_tiles + mid;
     sm.tile_rows = p->tile_rows + mid * p->max_tiles * kTileM;
     sm.tile_adapters = p->tile_adapters + mid * p->max_tiles * kTileM;
@@ -272,7 +272,7 @@ cts_status_t launch_expand(cts_plan_t p, int n, const int32_t* modules, void* co
     em.tm_t = p->d_tm_t + modules[i];
     em.tm_out = b->d_tm_out + modules[i];
     const size_t mid = m.map_id;
-    em.tiles = p->tiles + mid * p->max_tiles;
+    em.tiles = p->tiles + mid * p->max_tiles * 2;
     em.n_tiles = p->n_tiles + mid;
     em.tile_rows = p->tile_rows + mid * p->max_tiles * kTileM;
     em.nblk = (m.d_out + kBN - 1) / kBN;
@@ -484,7 +484,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   const size_t o_tok = off; off = align_up(off + size_t(T_max) * 4, 256);
   const size_t o_perm = off; off = align_up(off + nm * T_max * 4, 256);
   const size_t o_offs = off; off = align_up(off + nm * (b->C + 1) * 4, 256);
-  const size_t o_tiles = off; off = align_up(off + nm * p->max_tiles * 16, 256);
+  const size_t o_tiles = off; off = align_up(off + nm * p->max_tiles * 32, 256);
   const size_t o_nt = off; off = align_up(off + nm * 4, 256);
   const size_t o_trows = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
   const size_t o_tads = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
@@ -509,7 +509,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->tbuf = reinterpret_cast<__nv_bfloat16*>(base + o_t);
   const int32_t init_err[2] = {0, -1};
   bool ok = cudaMemset(p->n_tiles, 0, nm * 4) == cudaSuccess &&
-            cudaMemset(p->tiles, 0, nm * p->max_tiles * 16) == cudaSuccess &&
+            cudaMemset(p->tiles, 0, nm * p->max_tiles * 32) == cudaSuccess &&
             cudaMemset(p->counters, 0, size_t(kMaxGroup) * p->max_tiles * 4) == cudaSuccess &&
             cudaMemcpy(p->err, init_err, 8, cudaMemcpyHostToDevice) == cudaSuccess;
   std::vector<CUtensorMap> h_tm(b->n_modules);
@@ -554,10 +554,15 @@ cts_status_t cts_segment(cts_plan_t p, const int32_t* token_adapter, int32_t T, 
   a.N = b->N;
   a.C = b->C;
   a.max_tiles = p->max_tiles;
+  static const int pack = [] {
+    const char* e = std::getenv("CTS_PACK");   // tuning aid: 0 disables slot packing
+    return e ? std::atoi(e) : 1;
+  }();
+  a.pack = pack;
   static const cudaError_t seg_attr = cudaFuncSetAttribute(
-      segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (kSegWarps + 2) * 1024 * 4);
+      segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (kSegWarps + 3) * 1024 * 4);
   CTS_CUDA(seg_attr);
-  CTS_CUDA(launch_pdl(segment_kernel, b->n_maps, kSegThreads, size_t(kSegWarps + 2) * b->C * 4, stream, a));
+  CTS_CUDA(launch_pdl(segment_kernel, b->n_maps, kSegThreads, size_t(kSegWarps + 3) * b->C * 4, stream, a));
   p->T = T;
   return CTS_OK;
 }
@@ -573,16 +578,22 @@ cts_status_t cts_segment_readback(cts_plan_t p, int32_t module, int32_t* perm, i
     CTS_CUDA(cudaMemcpy(perm, p->perm + mid * p->T_max, size_t(p->T) * 4, cudaMemcpyDeviceToHost));
   if (offsets)
     CTS_CUDA(cudaMemcpy(offsets, p->offsets + mid * (b->C + 1), size_t(b->C + 1) * 4, cudaMemcpyDeviceToHost));
-  int32_t nt = 0;
-  CTS_CUDA(cudaMemcpy(&nt, p->n_tiles + mid, 4, cudaMemcpyDeviceToHost));
-  if (n_tiles) *n_tiles = nt;
-  if (tiles && nt > 0) {
-    std::vector<int4> tmp(nt);
-    CTS_CUDA(cudaMemcpy(tmp.data(), p->tiles + mid * p->max_tiles, size_t(nt) * 16, cudaMemcpyDeviceToHost));
-    for (int i = 0; i < nt; ++i) {
-      tiles[3 * i] = tmp[i].x;
-      tiles[3 * i + 1] = tmp[i].y;
-      tiles[3 * i + 2] = tmp[i].z;
+  int32_t ns = 0;
+  CTS_CUDA(cudaMemcpy(&ns, p->n_tiles + mid, 4, cudaMemcpyDeviceToHost));
+  // slots -> the logical tile list (every tile is one perm range; sorted by start = cluster order)
+  std::vector<int4> slots(size_t(ns) * 2);
+  if (ns > 0)
+    CTS_CUDA(cudaMemcpy(slots.data(), p->tiles + mid * p->max_tiles * 2, size_t(ns) * 32, cudaMemcpyDeviceToHost));
+  std::vector<int4> logical;
+  for (const int4& t : slots)
+    if (t.z > 0) logical.push_back(t);
+  std::sort(logical.begin(), logical.end(), [](const int4& a, const int4& b) { return a.y < b.y; });
+  if (n_tiles) *n_tiles = static_cast<int32_t>(logical.size());
+  if (tiles) {
+    for (size_t i = 0; i < logical.size(); ++i) {
+      tiles[3 * i] = logical[i].x;
+      tiles[3 * i + 1] = logical[i].y;
+      tiles[3 * i + 2] = logical[i].z;
     }
   }
   return CTS_OK;

@@ -5,8 +5,9 @@
 // update y" with `scale` -- here scale was already folded into t by kernel 1.
 //
 // Persistent, grouped (same scheme as the shrink): one CTA per SM walks a static round-robin list
-// of work items item = (module g, 128-token tile slot, BN-column block of d_out), laid out over the
-// host-known tile bound (empty slots skipped):
+// of work items item = (module g, 128-row tile slot, BN-column block of d_out), laid out over the
+// host-known tile bound (empty slots skipped); a slot holds one cluster's tile or two <=64-token
+// tiles (one per 64-row half, two MMAs against the two clusters' out_basis blocks):
 //   warps 0-3   TMA producers (items dealt round-robin, one warp's gather4 issue rate is not
 //               enough): t_hi / t_lo tile (A operand, K-major), the out_basis block (B operand,
 //               K-major) and the tile's y rows gathered by token index (tile::gather4, 64-column
@@ -29,13 +30,13 @@ namespace cts {
 
 constexpr int kExpandThreads = 32 * (kProducerWarps + 1 + 4 * kEpiSets);
 constexpr int kBN = 128;                 // d_out columns per work item
-constexpr int kExpandAccSlots = 4;       // 4 x 128 fp32 columns = all of TMEM
+constexpr int kExpandAccSlots = 2;       // 2 x (D0 | D1) x 128 fp32 columns = all of TMEM
 
 struct alignas(64) ExpandMod {
   CUtensorMap tm_y;                      // y [T][d_out], box {64, 1}, 128B swizzle (per call)
   const CUtensorMap* tm_t;               // tbuf [max_tiles*128][2*rp], box {rp, 128} (plan, global mem)
   const CUtensorMap* tm_out;             // out_basis [C*d_out][rp], box {rp, 64} (bank, global mem)
-  const int4* tiles;                     // (cluster, start, len, -); len 0 = empty slot
+  const int4* tiles;                     // [slot][2]: (cluster, start, len, -) per 64-row half
   const int32_t* n_tiles;                // real tile count of this module's map
   const int32_t* tile_rows;              // [tile*128 + row] token index
   int nblk;                              // ceil(d_out / kBN)
@@ -53,8 +54,9 @@ struct ExpandCfg {
   static constexpr int kY = kTileM * 128;                    // one 64-column segment of y rows (16 KB)
   static constexpr int kSeg = kBN / 64;
   static constexpr int kA = kTileM * RP * 2;                 // t_hi (or t_lo) tile
-  static constexpr int kB = kBN * RP * 2;                    // out_basis block
-  static constexpr int kMeta = kTileM * 4 + 16;              // token rows + (g, cluster, nb, len)
+  static constexpr int kB1 = kBN * RP * 2;                   // one out_basis block
+  static constexpr int kB = 2 * kB1;                         // one block per slot half
+  static constexpr int kMeta = kTileM * 4 + 32;              // token rows + 2 x int4 descriptors
   static constexpr int kStage = kSeg * kY + 2 * kA + kB;
   static constexpr int kStages = (200 * 1024) / (kStage + kMeta);   // 4 at rp=16, 3 at rp=32, 2 at rp=64
   static constexpr int kOffMeta = kStages * kStage;
@@ -62,7 +64,8 @@ struct ExpandCfg {
   static constexpr int kNumBars = 2 * kStages + 2 * kExpandAccSlots;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kBytes = kOffMisc + 64 + 1024;
-  static constexpr uint32_t kTmemCols = kBN * kExpandAccSlots;
+  static constexpr uint32_t kSlotCols = 2 * kBN;            // D0 | D1
+  static constexpr uint32_t kTmemCols = kSlotCols * kExpandAccSlots;
 };
 
 template <int RP>
@@ -119,26 +122,36 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
       if (tile >= tile_count(g)) continue;
       const int my = li++;
       if (my % kProducerWarps != warp) continue;
-      const int4 t4 = m.tiles[tile];
+      const int4 t0 = m.tiles[2 * tile], t1 = m.tiles[2 * tile + 1];
       const int4 r4 = *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
       const int stage = my % L::kStages;
       const uint32_t phase = (my / L::kStages) & 1;
-      const int len4 = min(kTileM, (t4.z + 3) & ~3);
-      const int ngroups = len4 >> 2;
+      const bool shared = t1.z > 0;
+      const int l0 = (t0.z + 3) & ~3, l1 = (t1.z + 3) & ~3;
+      const bool gvalid = shared ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
+      const int ngroups = (l0 + l1) >> 2;
       mbar_wait(&empty[stage], phase ^ 1);
       *reinterpret_cast<int4*>(stage_rows(stage) + 4 * lane) = r4;
-      if (lane == 0) *stage_info(stage) = make_int4(g, t4.x, nb, t4.z);
+      if (lane == 0) {
+        stage_info(stage)[0] = make_int4(g, t0.x, nb, t0.z);
+        stage_info(stage)[1] = make_int4(t1.x, t1.z, 0, 0);
+      }
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(2 * L::kA + L::kB + L::kSeg * ngroups * 512));
+        mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(2 * L::kA + (shared ? 2 : 1) * L::kB1 +
+                                                                   L::kSeg * ngroups * 512));
         tma_load_2d(stage_a(stage), m.tm_t, &full[stage], 0, tile * kTileM);
         tma_load_2d(stage_a(stage) + L::kA, m.tm_t, &full[stage], RP, tile * kTileM);
 #pragma unroll
-        for (int s = 0; s < L::kSeg; ++s)
-          tma_load_2d(stage_b(stage) + s * 64 * RP * 2, m.tm_out, &full[stage], 0, t4.x * m.d_out + nb * kBN + s * 64);
+        for (int s = 0; s < L::kSeg; ++s) {
+          tma_load_2d(stage_b(stage) + s * 64 * RP * 2, m.tm_out, &full[stage], 0, t0.x * m.d_out + nb * kBN + s * 64);
+          if (shared)
+            tma_load_2d(stage_b(stage) + L::kB1 + s * 64 * RP * 2, m.tm_out, &full[stage], 0,
+                        t1.x * m.d_out + nb * kBN + s * 64);
+        }
       }
       __syncwarp();
-      if (lane < ngroups) {
+      if (gvalid) {
 #pragma unroll
         for (int s = 0; s < L::kSeg; ++s)
           tma_gather4(stage_y(stage) + s * L::kY + lane * 512, &m.tm_y, &full[stage], nb * kBN + s * 64, r4.x, r4.y,
@@ -148,7 +161,10 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc_bf16(kTileM, kBN);
+    // N = 2 kBN: the two halves' out_basis blocks are contiguous in the B stage (256 rows), so one
+    // MMA per K step gives D0 = t U_c0^T (cols [0,128)) and D1 = t U_c1^T (cols [128,256)); for an
+    // unshared slot the second block is stale and D1 is never read.
+    constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * kBN);
     int stage = 0, slot = 0;
     uint32_t phase = 0, aphase = 0;
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
@@ -159,7 +175,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
       mbar_wait(&full[stage], phase);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t acc = tmem + slot * kBN;
+        const uint32_t acc = tmem + slot * L::kSlotCols;
         const uint32_t hi = smem_u32(stage_a(stage)), lo = hi + L::kA, b = smem_u32(stage_b(stage));
 #pragma unroll
         for (int k = 0; k < RP / 16; ++k)
@@ -192,16 +208,19 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
       mbar_wait(&acc_full[slot], aphase);
       mbar_wait(&full[stage], phase);        // y rows + metadata landed (acquire for this thread)
       tc_fence_after();
-      const int4 info = *stage_info(stage);   // (g, cluster, nb, len)
-      const int len = info.w;
+      const int4 info = stage_info(stage)[0];   // (g, cluster0, nb, len0)
+      const int4 info1 = stage_info(stage)[1];  // (cluster1, len1, -, -)
+      const int sub = (info1.y > 0 && quarter >= 2) ? 1 : 0;   // which half's tile these rows hold
+      const int sbase = sub * (kTileM / 2);                    // first slot row of that tile
+      const int len4 = sbase + (((sub ? info1.y : info.w) + 3) & ~3);   // rows < len4 are live
       uint8_t* ys = stage_y(stage);
-      const int len4 = min(kTileM, (len + 3) & ~3);
-      const bool active = quarter * 32 < len;    // warp-uniform: this quarter holds valid rows
+      const bool active = quarter * 32 < len4;  // warp-uniform: this quarter holds live rows
       if (active) {
 #pragma unroll 1
         for (int j2 = 0; j2 < kBN / 64; ++j2) {
           float v[64];
-          const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * kBN + j2 * 64;
+          const uint32_t taddr =
+              tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * L::kSlotCols + sub * kBN + j2 * 64;
           tmem_ld32(taddr, v);
           tmem_ld32(taddr + 32, v + 32);
           tmem_ld_wait();
@@ -230,7 +249,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
         fence_proxy_async_smem();
         __syncwarp();
         const int grp = quarter * 8 + (lane & 7), seg = lane >> 3;
-        if (grp * 4 < len && seg < L::kSeg) {
+        if (grp * 4 < len4 && seg < L::kSeg) {
           const int4 r4 = *reinterpret_cast<const int4*>(stage_rows(stage) + 4 * grp);
           tma_scatter4(&p.mod[info.x].tm_y, ys + seg * L::kY + grp * 512, info.z * kBN + seg * 64, r4.x, r4.y, r4.z,
                        r4.w);

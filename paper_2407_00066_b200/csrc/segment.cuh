@@ -14,6 +14,11 @@
 //   C. each warp re-walks its range: a token's slot = base[w][key] + popc(peers & lanes_below).
 // Stable by construction: warps own increasing token ranges, chunks are walked in order, and the
 // within-chunk rank counts lower lanes (= lower token indices) only.
+//   D. tiles: each cluster's group is cut into 128-token tiles in order; the GEMM kernels see SLOTS
+//      of 128 rows: a whole tile (full, or a remainder of 65..127 tokens) or two remainders of
+//      <= 64 tokens, one per 64-row half ("packing": at decode ~41 tokens per cluster, so a 128-row
+//      MMA tile is otherwise 2/3 empty).  Halves are paired in cluster order.  Every logical tile is
+//      still one contiguous perm range (c, start, len), as in oracle.segment_ref.
 #pragma once
 #include <cstdint>
 #include "sm100.cuh"
@@ -30,12 +35,14 @@ struct SegArgs {
   const int32_t* maps;           // [n_maps][N]
   int32_t* perm;                 // [n_maps][T_max]
   int32_t* offsets;              // [n_maps][C+1]
-  int4* tiles;                   // [n_maps][max_tiles]  (c, start, len, 0); len = 0 past n_tiles
-  int32_t* n_tiles;              // [n_maps]
+  int4* tiles;                   // [n_maps][max_tiles][2] slots: (c, start, len, 0) per 64-row half;
+                                 //   second half len = 0 for a whole tile; both 0 past n_tiles
+  int32_t* n_tiles;              // [n_maps] number of slots
   int32_t* tile_rows;            // [n_maps][max_tiles*128] token of each tile row (dup of last past len)
   int32_t* tile_adapters;        // [n_maps][max_tiles*128] adapter of that token
   int32_t* err;                  // [2] code, first bad token
   int T, T_max, N, C, max_tiles;
+  int pack;                      // 1: pair <=64-token remainders into shared slots
 };
 
 __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int& total) {
@@ -70,7 +77,8 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
   extern __shared__ int seg_smem[];
   int* hist = seg_smem;                            // [kSegWarps][C]
   int* cnt = hist + kSegWarps * a.C;               // [C]
-  int* tile_base = cnt + a.C;                      // [C]
+  int* tile_base = cnt + a.C;                      // [C] first whole slot of the cluster
+  int* half_base = tile_base + a.C;                // [C] index of the cluster's half remainder
   __shared__ int warp_sums[33];
   __shared__ int s_bad;
 
@@ -79,7 +87,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
   const int* cmap = a.maps + static_cast<size_t>(map_id) * a.N;
   int32_t* perm = a.perm + static_cast<size_t>(map_id) * a.T_max;
   int32_t* offsets = a.offsets + static_cast<size_t>(map_id) * (a.C + 1);
-  int4* tiles = a.tiles + static_cast<size_t>(map_id) * a.max_tiles;
+  int4* tiles = a.tiles + static_cast<size_t>(map_id) * a.max_tiles * 2;
 
   griddep_wait();                                   // previous step's applies still read the plan
   griddep_launch_dependents();
@@ -95,7 +103,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
   }
   __syncthreads();
   if (s_bad != 0x7fffffff) {                       // poison: no tiles for any module
-    for (int i = threadIdx.x; i < a.max_tiles; i += kSegThreads) tiles[i] = make_int4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < 2 * a.max_tiles; i += kSegThreads) tiles[i] = make_int4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
       a.n_tiles[map_id] = 0;
       if (map_id == 0) {
@@ -141,25 +149,33 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
     }
   }
   __syncthreads();
-  int carry = 0, tcarry = 0;
+  int carry = 0, tcarry = 0, hcarry = 0;
   for (int c0 = 0; c0 < a.C; c0 += kSegThreads) {
     const int c = c0 + threadIdx.x;
     const int v = c < a.C ? cnt[c] : 0;
-    const int nt = (v + kTileM - 1) / kTileM;
-    int tot, ttot;
+    const int rem = v % kTileM;
+    const int lim = a.pack ? kTileM / 2 : 0;
+    const int whole = v / kTileM + (rem > lim ? 1 : 0);           // slots owned outright
+    const int half = (rem > 0 && rem <= lim) ? 1 : 0;             // a remainder that shares a slot
+    int tot, wtot, htot;
     const int ex = block_exclusive_scan(v, warp_sums, tot);
-    const int tex = block_exclusive_scan(nt, warp_sums, ttot);
+    const int wex = block_exclusive_scan(whole, warp_sums, wtot);
+    const int hex = block_exclusive_scan(half, warp_sums, htot);
     if (c < a.C) {
       offsets[c] = carry + ex;
-      tile_base[c] = tcarry + tex;
+      tile_base[c] = tcarry + wex;
+      half_base[c] = half ? hcarry + hex : -1;
       cnt[c] = v;
     }
     carry += tot;
-    tcarry += ttot;
+    tcarry += wtot;
+    hcarry += htot;
   }
+  const int n_whole = tcarry, n_half = hcarry;
+  const int n_slots = n_whole + (n_half + 1) / 2;
   if (threadIdx.x == 0) {
     offsets[a.C] = carry;
-    a.n_tiles[map_id] = tcarry;
+    a.n_tiles[map_id] = n_slots;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kSegWarps * a.C; i += kSegThreads) hist[i] += offsets[i % a.C];
@@ -183,22 +199,39 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
     __syncwarp();
   }
 
-  // D. tile list (empty descriptors past n_tiles: kernels map work statically over the bound).
+  // D. slots (empty descriptors past n_slots: kernels map work statically over the bound).
   for (int c = threadIdx.x; c < a.C; c += kSegThreads) {
-    const int n = cnt[c], base = tile_base[c], off = offsets[c];
-    for (int j = 0; j * kTileM < n; ++j)
-      tiles[base + j] = make_int4(c, off + j * kTileM, min(kTileM, n - j * kTileM), 0);
+    const int n = cnt[c], off = offsets[c], full = n / kTileM, rem = n % kTileM;
+    int slot = tile_base[c];
+    for (int j = 0; j < full; ++j, ++slot) {
+      tiles[2 * slot] = make_int4(c, off + j * kTileM, kTileM, 0);
+      tiles[2 * slot + 1] = make_int4(0, 0, 0, 0);
+    }
+    if (rem > (a.pack ? kTileM / 2 : 0)) {
+      tiles[2 * slot] = make_int4(c, off + full * kTileM, rem, 0);
+      tiles[2 * slot + 1] = make_int4(0, 0, 0, 0);
+    } else if (rem > 0) {
+      const int k = half_base[c];
+      const int hs = n_whole + k / 2;
+      tiles[2 * hs + (k & 1)] = make_int4(c, off + full * kTileM, rem, 0);
+      if ((k & 1) == 0 && k == n_half - 1) tiles[2 * hs + 1] = make_int4(0, 0, 0, 0);
+    }
   }
-  for (int i = tcarry + threadIdx.x; i < a.max_tiles; i += kSegThreads) tiles[i] = make_int4(0, 0, 0, 0);
-  __syncthreads();                                 // perm and tiles complete (block scope)
+  for (int i = 2 * n_slots + threadIdx.x; i < 2 * a.max_tiles; i += kSegThreads) tiles[i] = make_int4(0, 0, 0, 0);
+  __syncthreads();                                 // perm and slots complete (block scope)
 
-  // E. per-tile row lists: token and adapter of every tile row, so the GEMM kernels fetch a tile's
-  //    rows with one dependent load instead of two.
+  // E. per-slot row lists: token and adapter of every slot row (rows 64..127 belong to the second
+  //    half when the slot is shared; rows past a tile's length repeat its last token), so the GEMM
+  //    kernels fetch a slot's rows with one dependent load.
   int32_t* trows = a.tile_rows + static_cast<size_t>(map_id) * a.max_tiles * kTileM;
   int32_t* tads = a.tile_adapters + static_cast<size_t>(map_id) * a.max_tiles * kTileM;
-  for (int i = threadIdx.x; i < tcarry * kTileM; i += kSegThreads) {
-    const int4 tl = tiles[i / kTileM];
-    const int tok = perm[tl.y + min(i % kTileM, tl.z - 1)];
+  for (int i = threadIdx.x; i < n_slots * kTileM; i += kSegThreads) {
+    const int slot = i / kTileM, r = i % kTileM;
+    const int4 s1 = tiles[2 * slot + 1];
+    const bool second = s1.z > 0 && r >= kTileM / 2;
+    const int4 tl = second ? s1 : tiles[2 * slot];
+    const int local = second ? r - kTileM / 2 : r;
+    const int tok = perm[tl.y + min(local, tl.z - 1)];
     trows[i] = tok;
     tads[i] = a.token_adapter[tok];
   }

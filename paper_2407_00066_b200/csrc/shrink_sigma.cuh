@@ -7,7 +7,9 @@
 //
 // Persistent, grouped: one launch covers a group of modules (e.g. q,k,v which share x); the grid is
 // one CTA per SM and every CTA walks a static round-robin list of work items
-//     item = (module g, 128-token tile slot of one cluster, K-chunk kc of d_in)
+//     item = (module g, 128-row tile slot, K-chunk kc of d_in)
+// where a slot holds one cluster's tile or two <=64-token tiles of two clusters (one per half; one
+// N = 2 r_pad MMA per K step against both clusters' stacked basis slabs; segment.cuh "packing")
 // laid out over the host-known tile BOUND (tile slots past the real count are empty and skipped), so
 // no CTA waits on a device-side count before issuing its first load; the TMA ring keeps streaming
 // across item boundaries.
@@ -50,7 +52,7 @@ constexpr int kShrinkAccSlots = 4;
 struct alignas(64) ShrinkMod {
   CUtensorMap tm_x;                     // x [T][d_in], box {64, 1}, 128B swizzle (per call)
   const CUtensorMap* tm_in;             // in_basis [C*rp][d_in], box {64, rp} (bank, global mem)
-  const int4* tiles;                    // (cluster, start, len, -); len 0 = empty slot
+  const int4* tiles;                    // [slot][2]: (cluster, start, len, -) per 64-row half
   const int32_t* n_tiles;               // real tile count of this module's map
   const int32_t* tile_rows;             // [tile*128 + row] token index
   const int32_t* tile_adapters;         // [tile*128 + row] adapter id
@@ -72,17 +74,18 @@ struct ShrinkParams {
 
 template <int RP>
 struct ShrinkCfg {
-  static constexpr int kStages = 8;
   static constexpr int kA = kTileM * 128;           // bytes per A stage (x rows)
-  static constexpr int kB = RP * 128;               // bytes per B stage (in_basis rows)
+  static constexpr int kB1 = RP * 128;              // one in_basis K-slab (rp rows x 64 cols)
+  static constexpr int kB = 2 * kB1;                // bytes per B stage: one slab per slot half
+  static constexpr int kStages = (200 * 1024) / (kA + kB) < 8 ? (200 * 1024) / (kA + kB) : 8;  // 8 / 8 / 6
   static constexpr int kOffA = 0;
   static constexpr int kOffB = kOffA + kStages * kA;
   static constexpr int kOffBar = kOffB + kStages * kB;
   static constexpr int kNumBars = 2 * kStages + 2 * kShrinkAccSlots;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kBytes = kOffMisc + 64 + 1024;
-  static constexpr uint32_t kSlotCols = RP < 32 ? 32 : RP;
-  static constexpr uint32_t kTmemCols = kSlotCols * kShrinkAccSlots;   // 128 or 256
+  static constexpr uint32_t kSlotCols = 2 * RP < 32 ? 32 : 2 * RP;   // D0 | D1 (one per slot half)
+  static constexpr uint32_t kTmemCols = kSlotCols * kShrinkAccSlots;  // 128 / 256 / 512
 };
 
 // item -> module g through the per-module item prefix sums
@@ -143,12 +146,14 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
       const ShrinkMod& m = p.mod[g];
       const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
       if (tile >= tile_count(g)) continue;        // empty tile slot
-      const int4 t4 = m.tiles[tile];
+      const int4 t0 = m.tiles[2 * tile], t1 = m.tiles[2 * tile + 1];
       const int4 r4 = *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
-      const int len4 = min(kTileM, (t4.z + 3) & ~3);
-      const int ngroups = len4 >> 2;
+      const bool shared = t1.z > 0;               // two <=64-token tiles, one per half
+      const int l0 = (t0.z + 3) & ~3, l1 = (t1.z + 3) & ~3;
+      const bool gvalid = shared ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
+      const int ngroups = (l0 + l1) >> 2;
       const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
-      const uint32_t bytes = static_cast<uint32_t>(ngroups * 512 + L::kB);
+      const uint32_t bytes = static_cast<uint32_t>(ngroups * 512 + (shared ? 2 : 1) * L::kB1);
       for (int kb = kb0; kb < kb1; ++kb, ++li) {
         if (li % kProducerWarps != warp) continue;
         const int stage = li % L::kStages;
@@ -157,15 +162,22 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
         if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
         __syncwarp();
         uint8_t* dA = sA + stage * L::kA;
-        if (lane < ngroups) tma_gather4(dA + lane * 512, &m.tm_x, &full[stage], kb * kBK, r4.x, r4.y, r4.z, r4.w);
-        if (lane == 0) tma_load_2d(sB + stage * L::kB, m.tm_in, &full[stage], kb * kBK, t4.x * RP);
+        if (gvalid) tma_gather4(dA + lane * 512, &m.tm_x, &full[stage], kb * kBK, r4.x, r4.y, r4.z, r4.w);
+        if (lane == 0) {
+          tma_load_2d(sB + stage * L::kB, m.tm_in, &full[stage], kb * kBK, t0.x * RP);
+          if (shared) tma_load_2d(sB + stage * L::kB + L::kB1, m.tm_in, &full[stage], kb * kBK, t1.x * RP);
+        }
         if (li == 0 && lane == 0) CTS_STAMP(2);
       }
     }
     if (lane == 0 && warp == 0) CTS_STAMP(3);
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc_bf16(kTileM, RP);
+    // N = 2 r_pad: the two halves' basis slabs are contiguous in the B stage, so ONE MMA per K step
+    // yields D0 = A B0^T (cols [0, rp)) and D1 = A B1^T (cols [rp, 2rp)); for an unshared slot the
+    // second slab is stale and D1 is never read.  (A second MMA per K step measurably slowed the
+    // single issuing thread.)
+    constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * RP);
     int stage = 0, slot = 0;
     uint32_t phase = 0, aphase = 0;
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
@@ -216,15 +228,18 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
       const uint32_t aphase = (li / kShrinkAccSlots) & 1;
       ++li;
       if (!mine) continue;
-      const int4 t4 = m.tiles[tile];
-      const int len4 = min(kTileM, (t4.z + 3) & ~3);
-      const int adapter = row < len4 ? m.tile_adapters[tile * kTileM + row] : 0;
+      const int4 t0 = m.tiles[2 * tile], t1 = m.tiles[2 * tile + 1];
+      const int sub = (t1.z > 0 && quarter >= 2) ? 1 : 0;   // which half's tile this warp's rows hold
+      const int slen4 = ((sub ? t1.z : t0.z) + 3) & ~3;
+      const bool rvalid = row - sub * (kTileM / 2) < slen4;
+      const int adapter = rvalid ? m.tile_adapters[tile * kTileM + row] : 0;
       mbar_wait(&acc_full[slot], aphase);
       tc_fence_after();
       if (set_tid == 0) CTS_STAMP(li <= kEpiSets ? 6 : 7);
       float s[RP];
 #pragma unroll
-      for (int c = 0; c < RP; c += 16) tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * L::kSlotCols + c, s + c);
+      for (int c = 0; c < RP; c += 16)
+        tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * L::kSlotCols + sub * RP + c, s + c);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
@@ -234,7 +249,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
       if (m.ks > 1) {
         // split-K: publish this chunk's partial; the LAST arriving CTA (acq_rel counter) sums the
         // ks partials in kc order, so the result does not depend on scheduling
-        if (row < len4) {
+        if (rvalid) {
           float4* dst = reinterpret_cast<float4*>(m.ws + (static_cast<size_t>(kc) * m.ws_rows + tile * kTileM + row) * RP);
 #pragma unroll
           for (int c = 0; c < RP / 4; ++c) dst[c] = make_float4(s[4 * c], s[4 * c + 1], s[4 * c + 2], s[4 * c + 3]);
@@ -248,7 +263,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
         named_bar_sync(1 + set, 128);
         finisher = s_last[set] != 0;
         if (finisher) {
-          if (row < len4) {
+          if (rvalid) {
 #pragma unroll
             for (int c = 0; c < RP; ++c) s[c] = 0.f;
             for (int q = 0; q < m.ks; ++q) {
@@ -264,7 +279,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const _
           if (set_tid == 0) m.counters[tile] = 0;       // ready for the next launch
         }
       }
-      if (finisher && row < len4) {
+      if (finisher && rvalid) {
         // t = scale * Sigma_i s ; thread = token row
         const uint4* srow = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
         __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP);
