@@ -39,6 +39,8 @@ struct alignas(64) ExpandMod {
   const int4* tiles;                     // [slot][2]: (cluster, start, len, -) per 64-row half
   const int32_t* n_tiles;                // real tile count of this module's map
   const int32_t* tile_rows;              // [tile*128 + row] token index
+  __nv_bfloat16* y;                      // y base (register-direct store variant)
+  int64_t ld_y;                          // elements
   int nblk;                              // ceil(d_out / kBN)
   int d_out;
 };
@@ -68,7 +70,10 @@ struct ExpandCfg {
   static constexpr uint32_t kTmemCols = kSlotCols * kExpandAccSlots;
 };
 
-template <int RP>
+// DIRECT = false: results go back into the stage and each warp TMA-scatters its rows, releasing the
+// stage once the scatter has read it.  DIRECT = true: each thread stores its row's 16-byte chunks
+// straight from registers (st.global) and the stage is released right after the y_base reads.
+template <int RP, bool DIRECT>
 __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_constant__ ExpandParams p) {
   using L = ExpandCfg<RP>;
   extern __shared__ uint8_t smem_raw[];
@@ -224,8 +229,14 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
           tmem_ld32(taddr, v);
           tmem_ld32(taddr + 32, v + 32);
           tmem_ld_wait();
-          if (row < len4) {                  // rows len..len4 duplicate the last token: identical bytes
+          // rows len..len4 duplicate the last token (identical bytes for the 4-row scatter);
+          // the direct variant stores real rows only
+          const bool live = DIRECT ? (row - sbase < (sub ? info1.y : info.w)) : (row < len4);
+          if (live) {
             uint8_t* base = ys + j2 * L::kY + row * 128;   // 64 columns = one segment
+            const ExpandMod& mo = p.mod[info.x];
+            const int col0 = info.z * kBN + j2 * 64;
+            __nv_bfloat16* yrow = DIRECT ? mo.y + static_cast<size_t>(stage_rows(stage)[row]) * mo.ld_y + col0 : nullptr;
 #pragma unroll
             for (int qd = 0; qd < 8; ++qd) {
               const int phys = (qd ^ (row & 7)) * 16;
@@ -236,7 +247,11 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
                 const float2 f = __bfloat1622float2(h[e]);
                 h[e] = __floats2bfloat162_rn(f.x + v[qd * 8 + 2 * e], f.y + v[qd * 8 + 2 * e + 1]);
               }
-              *reinterpret_cast<uint4*>(base + phys) = w;
+              if (DIRECT) {
+                if (col0 + qd * 8 < mo.d_out) *reinterpret_cast<uint4*>(yrow + qd * 8) = w;
+              } else {
+                *reinterpret_cast<uint4*>(base + phys) = w;
+              }
             }
           }
         }
@@ -244,7 +259,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) expand_kernel(const __grid_
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[slot]);
-      if (active) {
+      if (!DIRECT && active) {
         // this warp's 8 four-row groups: lane -> (group, segment); TMA scatter of the rows
         fence_proxy_async_smem();
         __syncwarp();
