@@ -1,0 +1,108 @@
+// apply_fused.cuh -- the whole apply of a module group in ONE persistent launch: phase 1 runs the
+// shrink + Sigma roles (shrink_sigma.cuh) over all shrink work items, phase 2 the expand + residual
+// roles (expand.cuh) over all expand work items.
+//
+// Why: at decode each grouped launch moves only a few MB, so a separate expand launch pays its own
+// launch latency, prologue (barrier init, TMEM alloc) and tile-metadata round trips, and cannot
+// start any item before the last shrink CTA has finished its split-K reduction.  Here an expand
+// item waits only for ITS slot: the split-K finisher publishes a per-slot "t ready" flag
+// (st.release after fence.proxy.async, so the TMA reads of other CTAs see the bf16 t rows) and the
+// expand producer polls it (ld.acquire) before loading t.  Progress is guaranteed because the grid
+// is at most one CTA per SM (all CTAs co-resident) and every CTA finishes all its shrink items --
+// which never wait on anything -- before starting expand items.
+//
+// Shared memory: the two phases reuse one operand arena (a CTA barrier separates them) and keep
+// separate mbarrier sets; TMEM is allocated once (512 columns) and reused.  The ready flags are
+// cleared by the last CTA to exit (per-plan exit counter), so the next launch starts from zero even
+// when replayed from a CUDA graph.
+#pragma once
+#include "expand.cuh"
+#include "shrink_sigma.cuh"
+
+namespace cts {
+
+struct FusedParams {
+  ShrinkParams s;
+  ExpandParams e;
+  int32_t* exit_count;                   // per plan; self-resetting
+};
+
+template <int RP>
+struct FusedSmem {
+  static constexpr int kArena = ShrinkCfg<RP>::kArena > ExpandCfg<RP>::kArena ? ShrinkCfg<RP>::kArena
+                                                                                : ExpandCfg<RP>::kArena;
+  static constexpr int kOffBarS = kArena;
+  static constexpr int kOffBarE = kOffBarS + ShrinkCfg<RP>::kNumBars * 8;
+  static constexpr int kOffMisc = kOffBarE + ExpandCfg<RP>::kNumBars * 8;
+  static constexpr int kBytes = kOffMisc + 64 + 1024;
+  static constexpr uint32_t kTmemCols = 512;
+  static_assert(ShrinkCfg<RP>::kTmemCols <= kTmemCols && ExpandCfg<RP>::kTmemCols <= kTmemCols, "TMEM");
+};
+
+template <int RP, bool DIRECT>
+__global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __grid_constant__ FusedParams p) {
+  using S = FusedSmem<RP>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kOffMisc);
+  int* s_last_exit = reinterpret_cast<int*>(smem + S::kOffMisc + 32);
+  ShrinkRing RS = shrink_ring<RP>(smem, reinterpret_cast<uint64_t*>(smem + S::kOffBarS),
+                                  reinterpret_cast<int*>(smem + S::kOffMisc + 16));
+  ExpandRing RE = expand_ring<RP>(smem, reinterpret_cast<uint64_t*>(smem + S::kOffBarE));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    CTS_STAMP(0);
+    shrink_init_barriers<RP>(RS);
+    expand_init_barriers<RP>(RE);
+    fence_barrier_init();
+  }
+  if (warp == kMmaWarp) tmem_alloc<S::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  RS.tmem = RE.tmem = *tmem_slot;
+  // shrink and expand items cover the same modules, so one per-module slot count serves both
+  int nt_lane = 0;
+  if (p.s.meta_ready) nt_lane = lane < p.s.n_mod ? *p.s.mod[lane].n_tiles : 0;
+  griddep_wait();
+  if (threadIdx.x == 0) griddep_launch_dependents();
+  if (!p.s.meta_ready) nt_lane = lane < p.s.n_mod ? *p.s.mod[lane].n_tiles : 0;
+  if (threadIdx.x == 0) CTS_STAMP(1);
+
+  // ---------------------------------------------------------------- phase 1: shrink + Sigma
+  if (warp < kProducerWarps) shrink_producer<RP>(p.s, RS, nt_lane, warp, lane);
+  else if (warp == kMmaWarp) shrink_mma<RP>(p.s, RS, nt_lane, lane);
+  else shrink_epilogue<RP>(p.s, RS, nt_lane, warp, lane);
+  if (threadIdx.x == 0) CTS_STAMP(3);                 // producers done issuing
+  if (warp == kMmaWarp && lane == 0) CTS_STAMP(4);    // last shrink MMA issued
+  if (threadIdx.x == 32 * kEpiWarp0) CTS_STAMP(5);    // epilogue set 0 done
+  if (threadIdx.x == 32 * (kEpiWarp0 + 4)) CTS_STAMP(6);   // epilogue set 1 done
+  tc_fence_before();
+  __syncthreads();                          // arena and TMEM free: all shrink stages consumed
+  tc_fence_after();
+  if (threadIdx.x == 0) CTS_STAMP(7);
+
+  // ---------------------------------------------------------------- phase 2: expand + residual
+  if (warp < kProducerWarps) expand_producer<RP>(p.e, RE, nt_lane, warp, lane);
+  else if (warp == kMmaWarp) expand_mma<RP>(p.e, RE, nt_lane, lane);
+  else expand_epilogue<RP, DIRECT>(p.e, RE, nt_lane, warp, lane);
+
+  // ---------------------------------------------------------------- exit: last CTA clears flags
+  if (threadIdx.x == 0) CTS_STAMP(9);
+  if (threadIdx.x == 32 * kEpiWarp0) CTS_STAMP(10);
+  __syncthreads();
+  if (threadIdx.x == 0) CTS_STAMP(11);
+  if (threadIdx.x == 0) *s_last_exit = atomicAdd(p.exit_count, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (*s_last_exit) {
+    for (int g = 0; g < p.s.n_mod; ++g) {
+      const ShrinkMod& m = p.s.mod[g];
+      const int slots = (p.s.prefix[g + 1] - p.s.prefix[g]) / m.ks;
+      for (int i = threadIdx.x; i < slots; i += blockDim.x) m.ready[i] = 0;
+    }
+    if (threadIdx.x == 0) *p.exit_count = 0;
+  }
+  if (warp == kMmaWarp) tmem_dealloc<S::kTmemCols>(RS.tmem);
+}
+
+}  // namespace cts

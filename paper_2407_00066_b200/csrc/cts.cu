@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/cts.h"
+#include "apply_fused.cuh"
 #include "expand.cuh"
 #include "segment.cuh"
 #include "shrink_sigma.cuh"
@@ -142,6 +143,9 @@ struct cts_plan_s {
   float* ws;              // [kMaxGroup][ws_cap rows][rp]  split-K partials
   size_t ws_cap_rows;
   int32_t* counters;      // [kMaxGroup][max_tiles]
+  int32_t* ready;         // [kMaxGroup][max_tiles] per-slot "t ready" flags (fused kernel)
+  int32_t* exit_count;    // fused kernel: CTAs exited (last one clears the flags)
+  int launches_since_segment;  // host view, for meta_ready (see next_meta_ready)
 };
 
 namespace {
@@ -170,21 +174,9 @@ int target_items_per_sm() {
   return v;
 }
 
-template <int RP>
-cudaError_t set_kernel_attrs() {
-  static cudaError_t once = [] {
-    cudaError_t e = cudaFuncSetAttribute(shrink_sigma_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         ShrinkCfg<RP>::kBytes);
-    return e;
-  }();
-  return once;
-}
-
-template <int RP, bool DIRECT>
-cudaError_t set_expand_attrs() {
-  static cudaError_t once = cudaFuncSetAttribute(expand_kernel<RP, DIRECT>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, ExpandCfg<RP>::kBytes);
-  return once;
+template <typename Kern>
+cudaError_t set_smem(Kern kernel, int bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 // expand store path: register-direct st.global when tiles are small (latency-bound, decode: the
@@ -199,6 +191,15 @@ bool expand_direct_store(int T, int C) {
   }();
   if (v >= 0) return v != 0;
   return T < 96 * C;   // mean tokens per cluster < 96
+}
+
+// cts_apply[_group] runs the fused single-launch kernel unless CTS_FUSED=0 (tuning aid).
+bool use_fused() {
+  static bool v = [] {
+    const char* e = std::getenv("CTS_FUSED");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return v;
 }
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while the previous
@@ -222,24 +223,28 @@ __nv_bfloat16* module_tbuf(cts_plan_t p, int module) {
   return p->tbuf + size_t(module) * p->max_tiles * kTileM * 2 * p->bank->rp;
 }
 
-// K chunks per tile for a group: aim for ~target_items_per_sm() items per SM, each >= 4 K blocks.
+// K chunks per tile for a group: aim for ~target_items_per_sm() items per SM over the tile BOUND,
+// each >= 4 K blocks.  (Sizing by the expected packed slot count instead -- more, shorter items --
+// measured slower at decode: 219k -> 189k tok/s, the extra split-K finisher chains end later.)
 int choose_ks(int tiles_total, int min_kblocks) {
   const int want = (target_items_per_sm() * sm_count() + tiles_total - 1) / std::max(tiles_total, 1);
   return std::max(1, std::min({want, 16, std::max(1, min_kblocks / 4)}));
 }
 
-template <int RP>
-cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
-                           float scale, cudaStream_t stream) {
+// Segment outputs may be read before griddep_wait by every kernel but the first after cts_segment:
+// each kernel triggers its dependents only after its own griddep_wait, so when launch k starts,
+// launch k-2 (at the latest cts_segment) has completed.
+int next_meta_ready(cts_plan_t p) { return p->launches_since_segment++ > 0 ? 1 : 0; }
+
+cts_status_t fill_shrink(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
+                         float scale, bool fused, ShrinkParams& prm, int& items) {
   const cts_bank_t b = p->bank;
   const int T = p->T;
   const int tiles_bound = cts_plan_max_tiles(p, T);
-  CTS_CUDA(set_kernel_attrs<RP>());
   int min_kb = 1 << 30;
   for (int i = 0; i < n; ++i) min_kb = std::min(min_kb, b->mods[modules[i]].d_in / kBK);
   const int ks = choose_ks(tiles_bound * n, min_kb);
   if (size_t(ks) * tiles_bound * kTileM > p->ws_cap_rows) return CTS_ERR_SHAPE;
-  ShrinkParams prm;
   std::memset(&prm, 0, sizeof(prm));
   prm.n_mod = n;
   prm.prefix[0] = 0;
@@ -257,25 +262,22 @@ cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const vo
     sm.tbuf = module_tbuf(p, modules[i]);
     sm.ws = p->ws + size_t(i) * p->ws_cap_rows * b->rp;
     sm.counters = p->counters + size_t(i) * p->max_tiles;
+    sm.ready = fused ? p->ready + size_t(i) * p->max_tiles : nullptr;
     sm.kblocks = m.d_in / kBK;
     sm.ks = ks;
     sm.ws_rows = tiles_bound * kTileM;
     sm.scale = scale;
     prm.prefix[i + 1] = prm.prefix[i] + tiles_bound * ks;
   }
-  const int grid = std::min(sm_count(), tiles_bound * n * ks);
-  CTS_CUDA(launch_pdl(shrink_sigma_kernel<RP>, grid, kShrinkThreads, ShrinkCfg<RP>::kBytes, stream, prm));
+  items = prm.prefix[n];
   return CTS_OK;
 }
 
-template <int RP, bool DIRECT>
-cts_status_t launch_expand(cts_plan_t p, int n, const int32_t* modules, void* const* ys, const int64_t* ld_y,
-                           cudaStream_t stream) {
+cts_status_t fill_expand(cts_plan_t p, int n, const int32_t* modules, void* const* ys, const int64_t* ld_y,
+                         bool fused, ExpandParams& prm, int& items) {
   const cts_bank_t b = p->bank;
   const int T = p->T;
   const int tiles_bound = cts_plan_max_tiles(p, T);
-  CTS_CUDA((set_expand_attrs<RP, DIRECT>()));
-  ExpandParams prm;
   std::memset(&prm, 0, sizeof(prm));
   prm.n_mod = n;
   prm.prefix[0] = 0;
@@ -289,14 +291,61 @@ cts_status_t launch_expand(cts_plan_t p, int n, const int32_t* modules, void* co
     em.tiles = p->tiles + mid * p->max_tiles * 2;
     em.n_tiles = p->n_tiles + mid;
     em.tile_rows = p->tile_rows + mid * p->max_tiles * kTileM;
+    em.ready = fused ? p->ready + size_t(i) * p->max_tiles : nullptr;
     em.y = static_cast<__nv_bfloat16*>(ys[i]);
     em.ld_y = ld_y[i];
     em.nblk = (m.d_out + kBN - 1) / kBN;
     em.d_out = m.d_out;
     prm.prefix[i + 1] = prm.prefix[i] + tiles_bound * em.nblk;
   }
-  const int grid = std::min(sm_count(), prm.prefix[n]);
-  CTS_CUDA(launch_pdl(expand_kernel<RP, DIRECT>, grid, kExpandThreads, ExpandCfg<RP>::kBytes, stream, prm));
+  items = prm.prefix[n];
+  return CTS_OK;
+}
+
+template <int RP>
+cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
+                           float scale, cudaStream_t stream) {
+  static const cudaError_t attr = set_smem(shrink_sigma_kernel<RP>, ShrinkKernelSmem<RP>::kBytes);
+  CTS_CUDA(attr);
+  ShrinkParams prm;
+  int items = 0;
+  cts_status_t st = fill_shrink(p, n, modules, xs, ld_x, scale, false, prm, items);
+  if (st != CTS_OK) return st;
+  prm.meta_ready = next_meta_ready(p);
+  CTS_CUDA(launch_pdl(shrink_sigma_kernel<RP>, std::min(sm_count(), items), kApplyThreads,
+                      ShrinkKernelSmem<RP>::kBytes, stream, prm));
+  return CTS_OK;
+}
+
+template <int RP, bool DIRECT>
+cts_status_t launch_expand(cts_plan_t p, int n, const int32_t* modules, void* const* ys, const int64_t* ld_y,
+                           cudaStream_t stream) {
+  static const cudaError_t attr = set_smem(expand_kernel<RP, DIRECT>, ExpandKernelSmem<RP>::kBytes);
+  CTS_CUDA(attr);
+  ExpandParams prm;
+  int items = 0;
+  cts_status_t st = fill_expand(p, n, modules, ys, ld_y, false, prm, items);
+  if (st != CTS_OK) return st;
+  prm.meta_ready = next_meta_ready(p);
+  CTS_CUDA(launch_pdl(expand_kernel<RP, DIRECT>, std::min(sm_count(), items), kApplyThreads,
+                      ExpandKernelSmem<RP>::kBytes, stream, prm));
+  return CTS_OK;
+}
+
+template <int RP, bool DIRECT>
+cts_status_t launch_fused(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
+                          void* const* ys, const int64_t* ld_y, float scale, cudaStream_t stream) {
+  static const cudaError_t attr = set_smem(apply_fused_kernel<RP, DIRECT>, FusedSmem<RP>::kBytes);
+  CTS_CUDA(attr);
+  FusedParams prm;
+  int items_s = 0, items_e = 0;
+  cts_status_t st = fill_shrink(p, n, modules, xs, ld_x, scale, true, prm.s, items_s);
+  if (st != CTS_OK) return st;
+  if ((st = fill_expand(p, n, modules, ys, ld_y, true, prm.e, items_e)) != CTS_OK) return st;
+  prm.s.meta_ready = prm.e.meta_ready = next_meta_ready(p);
+  prm.exit_count = p->exit_count;
+  CTS_CUDA(launch_pdl(apply_fused_kernel<RP, DIRECT>, std::min(sm_count(), std::max(items_s, items_e)), kApplyThreads,
+                      FusedSmem<RP>::kBytes, stream, prm));
   return CTS_OK;
 }
 
@@ -334,6 +383,19 @@ cts_status_t do_expand(cts_plan_t p, int n, const int32_t* mods, void* const* ys
                            : launch_expand<32, false>(p, n, mods, ys, ld, s);
     default: return direct ? launch_expand<64, true>(p, n, mods, ys, ld, s)
                            : launch_expand<64, false>(p, n, mods, ys, ld, s);
+  }
+}
+
+cts_status_t do_fused(cts_plan_t p, int n, const int32_t* mods, const void* const* xs, const int64_t* ldx,
+                      void* const* ys, const int64_t* ldy, float scale, cudaStream_t s) {
+  const bool direct = expand_direct_store(p->T, p->bank->C);
+  switch (p->bank->rp) {
+    case 16: return direct ? launch_fused<16, true>(p, n, mods, xs, ldx, ys, ldy, scale, s)
+                           : launch_fused<16, false>(p, n, mods, xs, ldx, ys, ldy, scale, s);
+    case 32: return direct ? launch_fused<32, true>(p, n, mods, xs, ldx, ys, ldy, scale, s)
+                           : launch_fused<32, false>(p, n, mods, xs, ldx, ys, ldy, scale, s);
+    default: return direct ? launch_fused<64, true>(p, n, mods, xs, ldx, ys, ldy, scale, s)
+                           : launch_fused<64, false>(p, n, mods, xs, ldx, ys, ldy, scale, s);
   }
 }
 
@@ -496,6 +558,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->bank = b;
   p->T_max = T_max;
   p->T = 0;
+  p->launches_since_segment = 0;
   p->max_tiles = cts_plan_max_tiles(p, T_max);
   // split-K workspace rows per group slot: ks * tiles_bound * 128 <= (target items + tiles) * 128
   p->ws_cap_rows = size_t(kTargetItemsPerSMMax * sm_count() + p->max_tiles) * kTileM;
@@ -510,6 +573,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   const size_t o_tads = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
   const size_t o_err = off; off = align_up(off + 16, 256);
   const size_t o_cnt = off; off = align_up(off + size_t(kMaxGroup) * p->max_tiles * 4, 1024);
+  const size_t o_rdy = off; off = align_up(off + size_t(kMaxGroup) * p->max_tiles * 4 + 16, 1024);
   const size_t o_tm = off; off = align_up(off + size_t(b->n_modules) * sizeof(CUtensorMap), 1024);
   const size_t o_ws = off; off = align_up(off + size_t(kMaxGroup) * p->ws_cap_rows * b->rp * 4, 1024);
   const size_t o_t = off; off = align_up(off + size_t(b->n_modules) * p->max_tiles * kTileM * 2 * b->rp * 2, 1024);
@@ -524,6 +588,8 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->tile_adapters = reinterpret_cast<int32_t*>(base + o_tads);
   p->err = reinterpret_cast<int32_t*>(base + o_err);
   p->counters = reinterpret_cast<int32_t*>(base + o_cnt);
+  p->ready = reinterpret_cast<int32_t*>(base + o_rdy);
+  p->exit_count = p->ready + size_t(kMaxGroup) * p->max_tiles;
   p->d_tm_t = reinterpret_cast<CUtensorMap*>(base + o_tm);
   p->ws = reinterpret_cast<float*>(base + o_ws);
   p->tbuf = reinterpret_cast<__nv_bfloat16*>(base + o_t);
@@ -531,6 +597,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   bool ok = cudaMemset(p->n_tiles, 0, nm * 4) == cudaSuccess &&
             cudaMemset(p->tiles, 0, nm * p->max_tiles * 32) == cudaSuccess &&
             cudaMemset(p->counters, 0, size_t(kMaxGroup) * p->max_tiles * 4) == cudaSuccess &&
+            cudaMemset(p->ready, 0, size_t(kMaxGroup) * p->max_tiles * 4 + 16) == cudaSuccess &&
             cudaMemcpy(p->err, init_err, 8, cudaMemcpyHostToDevice) == cudaSuccess;
   std::vector<CUtensorMap> h_tm(b->n_modules);
   for (int m = 0; ok && m < b->n_modules; ++m)
@@ -584,6 +651,7 @@ cts_status_t cts_segment(cts_plan_t p, const int32_t* token_adapter, int32_t T, 
   CTS_CUDA(seg_attr);
   CTS_CUDA(launch_pdl(segment_kernel, b->n_maps, kSegThreads, size_t(kSegWarps + 3) * b->C * 4, stream, a));
   p->T = T;
+  p->launches_since_segment = 0;
   return CTS_OK;
 }
 
@@ -655,6 +723,7 @@ cts_status_t cts_apply_group(cts_plan_t p, int32_t n, const int32_t* modules, co
         return CTS_ERR_INVALID_ARGUMENT;
     }
   }
+  if (use_fused()) return do_fused(p, n, modules, xs, ld_x, ys, ld_y, scale, stream);
   if ((st = do_shrink(p, n, modules, xs, ld_x, scale, stream)) != CTS_OK) return st;
   return do_expand(p, n, modules, ys, ld_y, stream);
 }

@@ -17,16 +17,18 @@
 //               the in_basis K-slab (tile) into a kStages-deep mbarrier ring shared by all items;
 //               K blocks are dealt round-robin to the 4 warps because one warp's gather4 issue
 //               rate caps at ~2 TB/s per GPU (measured, profiles/microbench), four reach the
-//               tile-load rate.  Token rows come from the segment kernel's per-tile row list.
-//   warp 4      one elected lane issues tcgen05.mma (M=128 tokens, N=r_pad, K=16) into one of
+//               tile-load rate.  Token rows come from the segment kernel's per-slot row list.
+//   warp 4      one elected lane issues tcgen05.mma (M=128 tokens, N=2 r_pad, K=16) into one of
 //               kAccSlots TMEM accumulators, commit -> acc_full[slot]
 //   warps 5-12  epilogue, two sets of 4 warps on alternate items, thread = token row (TMEM lane
 //               quarter w%4): tcgen05.ld the partial s;
 //               split-K: the partial goes to an fp32 workspace, the LAST CTA to finish a tile
 //               (acq_rel per-tile arrival counter) sums the KS partials in kc order (deterministic),
 //               gathers Sigma_i (L2-resident, 16-byte loads) and writes t = scale*Sigma_i s as a
-//               bf16 hi + lo pair (t ~= hi + lo to ~2^-16 relative) for the expand.
+//               bf16 hi + lo pair (t ~= hi + lo to ~2^-16 relative) for the expand; in the fused
+//               kernel it then publishes the slot's "t ready" flag.
 // Rows of a tile past its length, up to a multiple of 4, duplicate the last valid token.
+// The roles are device functions so apply_fused.cuh can run them as the first phase of one launch.
 #pragma once
 #include "sm100.cuh"
 #include "segment.cuh"
@@ -46,20 +48,22 @@ constexpr int kProducerWarps = 4;
 constexpr int kMmaWarp = kProducerWarps;
 constexpr int kEpiWarp0 = kProducerWarps + 1;
 constexpr int kEpiSets = 2;             // epilogue warp-sets working on alternate items
-constexpr int kShrinkThreads = 32 * (kProducerWarps + 1 + 4 * kEpiSets);   // producers, MMA, epilogue
+constexpr int kApplyThreads = 32 * (kProducerWarps + 1 + 4 * kEpiSets);   // producers, MMA, epilogue
+constexpr int kShrinkThreads = kApplyThreads;
 constexpr int kShrinkAccSlots = 4;
 
 struct alignas(64) ShrinkMod {
   CUtensorMap tm_x;                     // x [T][d_in], box {64, 1}, 128B swizzle (per call)
   const CUtensorMap* tm_in;             // in_basis [C*rp][d_in], box {64, rp} (bank, global mem)
   const int4* tiles;                    // [slot][2]: (cluster, start, len, -) per 64-row half
-  const int32_t* n_tiles;               // real tile count of this module's map
-  const int32_t* tile_rows;             // [tile*128 + row] token index
-  const int32_t* tile_adapters;         // [tile*128 + row] adapter id
+  const int32_t* n_tiles;               // real slot count of this module's map
+  const int32_t* tile_rows;             // [slot*128 + row] token index
+  const int32_t* tile_adapters;         // [slot*128 + row] adapter id
   const __nv_bfloat16* sigma;           // [N][rp][rp], row = out index
   __nv_bfloat16* tbuf;                  // [max_tiles*128][2*rp]  (hi | lo)
   float* ws;                            // [ks][ws_rows][rp] split-K partials
-  int32_t* counters;                    // [max_tiles] arrivals per tile (self-resetting)
+  int32_t* counters;                    // [max_tiles] arrivals per slot (self-resetting)
+  int32_t* ready;                       // [max_tiles] "t ready" flags (fused kernel only; else null)
   int kblocks;                          // d_in / 64
   int ks;                               // K chunks per tile
   int ws_rows;                          // tile bound * 128
@@ -70,6 +74,7 @@ struct ShrinkParams {
   ShrinkMod mod[kMaxGroup];
   int prefix[kMaxGroup + 1];            // item prefix over modules (tile bound * ks each)
   int n_mod;
+  int meta_ready;                       // 1: segment outputs are complete before griddep_wait
 };
 
 template <int RP>
@@ -80,10 +85,8 @@ struct ShrinkCfg {
   static constexpr int kStages = (200 * 1024) / (kA + kB) < 8 ? (200 * 1024) / (kA + kB) : 8;  // 8 / 8 / 6
   static constexpr int kOffA = 0;
   static constexpr int kOffB = kOffA + kStages * kA;
-  static constexpr int kOffBar = kOffB + kStages * kB;
+  static constexpr int kArena = kOffB + kStages * kB;          // bytes of staged operands
   static constexpr int kNumBars = 2 * kStages + 2 * kShrinkAccSlots;
-  static constexpr int kOffMisc = kOffBar + kNumBars * 8;
-  static constexpr int kBytes = kOffMisc + 64 + 1024;
   static constexpr uint32_t kSlotCols = 2 * RP < 32 ? 32 : 2 * RP;   // D0 | D1 (one per slot half)
   static constexpr uint32_t kTmemCols = kSlotCols * kShrinkAccSlots;  // 128 / 256 / 512
 };
@@ -95,233 +98,294 @@ __device__ __forceinline__ int find_module(const int* prefix, int n_mod, int ite
   return g;
 }
 
+// Shared-memory handles of the shrink pipeline (operand ring in `arena`, barriers elsewhere).
+struct ShrinkRing {
+  uint8_t* sA;
+  uint8_t* sB;
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* acc_full;
+  uint64_t* acc_empty;
+  int* s_last;                          // [kEpiSets]
+  uint32_t tmem;
+};
+
 template <int RP>
-__global__ void __launch_bounds__(kShrinkThreads, 1) shrink_sigma_kernel(const __grid_constant__ ShrinkParams p) {
+__device__ __forceinline__ ShrinkRing shrink_ring(uint8_t* arena, uint64_t* bars, int* s_last) {
   using L = ShrinkCfg<RP>;
+  ShrinkRing R;
+  R.sA = arena + L::kOffA;
+  R.sB = arena + L::kOffB;
+  R.full = bars;
+  R.empty = bars + L::kStages;
+  R.acc_full = R.empty + L::kStages;
+  R.acc_empty = R.acc_full + kShrinkAccSlots;
+  R.s_last = s_last;
+  R.tmem = 0;
+  return R;
+}
+
+template <int RP>
+__device__ __forceinline__ void shrink_init_barriers(const ShrinkRing& R) {   // one thread
+  for (int s = 0; s < ShrinkCfg<RP>::kStages; ++s) {
+    mbar_init(&R.full[s], 1);
+    mbar_init(&R.empty[s], 1);
+  }
+  for (int s = 0; s < kShrinkAccSlots; ++s) {
+    mbar_init(&R.acc_full[s], 1);
+    mbar_init(&R.acc_empty[s], 4);      // one arrival per epilogue warp of the owning set
+  }
+}
+
+// ------------------------------------------------------------------ TMA producers (warps 0-3)
+template <int RP>
+__device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int warp, int lane) {
+  using L = ShrinkCfg<RP>;
+  const int total = p.prefix[p.n_mod];
+  int li = 0;                                     // K-block sequence index over this CTA's items
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int g = find_module(p.prefix, p.n_mod, item);
+    const ShrinkMod& m = p.mod[g];
+    const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
+    if (tile >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;   // empty tile slot
+    const int4 t0 = m.tiles[2 * tile], t1 = m.tiles[2 * tile + 1];
+    const int4 r4 = *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
+    const bool shared = t1.z > 0;                 // two <=64-token tiles, one per half
+    const int l0 = (t0.z + 3) & ~3, l1 = (t1.z + 3) & ~3;
+    const bool gvalid = shared ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
+    const int ngroups = (l0 + l1) >> 2;
+    const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
+    const uint32_t bytes = static_cast<uint32_t>(ngroups * 512 + (shared ? 2 : 1) * L::kB1);
+    for (int kb = kb0; kb < kb1; ++kb, ++li) {
+      if (li % kProducerWarps != warp) continue;
+      const int stage = li % L::kStages;
+      const uint32_t phase = (li / L::kStages) & 1;
+      mbar_wait(&R.empty[stage], phase ^ 1);
+      if (lane == 0) mbar_arrive_expect_tx(&R.full[stage], bytes);
+      __syncwarp();
+      uint8_t* dA = R.sA + stage * L::kA;
+      if (gvalid) tma_gather4(dA + lane * 512, &m.tm_x, &R.full[stage], kb * kBK, r4.x, r4.y, r4.z, r4.w);
+      if (lane == 0) {
+        tma_load_2d(R.sB + stage * L::kB, m.tm_in, &R.full[stage], kb * kBK, t0.x * RP);
+        if (shared) tma_load_2d(R.sB + stage * L::kB + L::kB1, m.tm_in, &R.full[stage], kb * kBK, t1.x * RP);
+      }
+      if (li == 0 && lane == 0) CTS_STAMP(2);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ MMA issuer (warp 4)
+template <int RP>
+__device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int lane) {
+  using L = ShrinkCfg<RP>;
+  // N = 2 r_pad: the two halves' basis slabs are contiguous in the B stage, so ONE MMA per K step
+  // yields D0 = A B0^T (cols [0, rp)) and D1 = A B1^T (cols [rp, 2rp)); for an unshared slot the
+  // second slab is stale and D1 is never read.  (A second MMA per K step measurably slowed the
+  // single issuing thread.)
+  constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * RP);
+  const int total = p.prefix[p.n_mod];
+  int stage = 0, slot = 0;
+  uint32_t phase = 0, aphase = 0;
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int g = find_module(p.prefix, p.n_mod, item);
+    const ShrinkMod& m = p.mod[g];
+    const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
+    if (tile >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;
+    const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
+    mbar_wait(&R.acc_empty[slot], aphase ^ 1);
+    tc_fence_after();
+    const uint32_t acc = R.tmem + slot * L::kSlotCols;
+    for (int kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&R.full[stage], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a_base = smem_u32(R.sA + stage * L::kA);
+        const uint32_t b_base = smem_u32(R.sB + stage * L::kB);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k)
+          umma_bf16(acc, umma_desc_kmajor(a_base + k * 32, 128), umma_desc_kmajor(b_base + k * 32, 128), idesc,
+                    (kb > kb0 || k > 0) ? 1u : 0u);
+        umma_commit(&R.empty[stage]);
+      }
+      __syncwarp();
+      if (++stage == L::kStages) { stage = 0; phase ^= 1; }
+    }
+    if (lane == 0) umma_commit(&R.acc_full[slot]);
+    __syncwarp();
+    if (++slot == kShrinkAccSlots) { slot = 0; aphase ^= 1; }
+  }
+}
+
+// ------------------------------------------------------------------ epilogue (warps 5-12)
+template <int RP>
+__device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int warp, int lane) {
+  using L = ShrinkCfg<RP>;
+  const int total = p.prefix[p.n_mod];
+  const int ew = warp - kEpiWarp0;              // 0..7
+  const int set = ew >> 2;
+  const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
+  const int row = quarter * 32 + lane;
+  const int set_tid = (ew & 3) * 32 + lane;      // 0..127 within the set
+  int li = 0;                                    // index over this CTA's non-empty items
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int g = find_module(p.prefix, p.n_mod, item);
+    const ShrinkMod& m = p.mod[g];
+    const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
+    if (tile >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;
+    const bool mine = (li % kEpiSets) == set;
+    const int slot = li % kShrinkAccSlots;
+    const uint32_t aphase = (li / kShrinkAccSlots) & 1;
+    ++li;
+    if (!mine) continue;
+    const int4 t0 = m.tiles[2 * tile], t1 = m.tiles[2 * tile + 1];
+    const int sub = (t1.z > 0 && quarter >= 2) ? 1 : 0;   // which half's tile this warp's rows hold
+    const int slen4 = ((sub ? t1.z : t0.z) + 3) & ~3;
+    const bool rvalid = row - sub * (kTileM / 2) < slen4;
+    const int adapter = rvalid ? m.tile_adapters[tile * kTileM + row] : 0;
+    if (rvalid) {                                 // warm L2 with this row's Sigma_i while the MMA runs
+      const uint8_t* sp = reinterpret_cast<const uint8_t*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
+#pragma unroll
+      for (int off = 0; off < RP * RP * 2; off += 128) prefetch_l2(sp + off);
+    }
+    mbar_wait(&R.acc_full[slot], aphase);
+    tc_fence_after();
+    float s[RP];
+#pragma unroll
+    for (int c = 0; c < RP; c += 16)
+      tmem_ld16(R.tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * L::kSlotCols + sub * RP + c, s + c);
+    tmem_ld_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&R.acc_empty[slot]);
+
+    bool finisher = true;
+    if (m.ks > 1) {
+      // split-K: publish this chunk's partial; the LAST arriving CTA (acq_rel counter) sums the
+      // ks partials in kc order, so the result does not depend on scheduling
+      if (rvalid) {
+        float4* dst = reinterpret_cast<float4*>(m.ws + (static_cast<size_t>(kc) * m.ws_rows + tile * kTileM + row) * RP);
+#pragma unroll
+        for (int c = 0; c < RP / 4; ++c) dst[c] = make_float4(s[4 * c], s[4 * c + 1], s[4 * c + 2], s[4 * c + 3]);
+      }
+      named_bar_sync(1 + set, 128);
+      if (set_tid == 0) R.s_last[set] = (atom_add_acq_rel_gpu(&m.counters[tile], 1) == m.ks - 1);
+      named_bar_sync(1 + set, 128);
+      finisher = R.s_last[set] != 0;
+      if (finisher) {
+        if (rvalid) {
+          // sum the partials in kc order (deterministic); this CTA's own chunk comes from registers
+          float own[RP];
+#pragma unroll
+          for (int c = 0; c < RP; ++c) { own[c] = s[c]; s[c] = 0.f; }
+          for (int q = 0; q < m.ks; ++q) {
+            if (q == kc) {
+#pragma unroll
+              for (int c = 0; c < RP; ++c) s[c] += own[c];
+              continue;
+            }
+            const float4* src = reinterpret_cast<const float4*>(
+                m.ws + (static_cast<size_t>(q) * m.ws_rows + tile * kTileM + row) * RP);
+#pragma unroll
+            for (int c = 0; c < RP / 4; ++c) {
+              const float4 v = __ldcg(src + c);
+              s[4 * c] += v.x; s[4 * c + 1] += v.y; s[4 * c + 2] += v.z; s[4 * c + 3] += v.w;
+            }
+          }
+        }
+        if (set_tid == 0) m.counters[tile] = 0;       // ready for the next launch
+      }
+    }
+    if (finisher && rvalid) {
+      // t = scale * Sigma_i s ; thread = token row
+      const uint4* srow = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
+      __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP);
+#pragma unroll 1
+      for (int o0 = 0; o0 < RP; o0 += 8) {
+        float t8[8];
+#pragma unroll
+        for (int oo = 0; oo < 8; ++oo) {
+          const int o = o0 + oo;
+          float acc = 0.f;
+#pragma unroll
+          for (int v8 = 0; v8 < RP / 8; ++v8) {
+            const uint4 w = __ldg(srow + (o * RP) / 8 + v8);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h[e]);
+              acc = fmaf(f.x, s[v8 * 8 + 2 * e], acc);
+              acc = fmaf(f.y, s[v8 * 8 + 2 * e + 1], acc);
+            }
+          }
+          t8[oo] = acc * m.scale;
+        }
+        uint4 hi, lo;
+        __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&hi);
+        __nv_bfloat162* ll = reinterpret_cast<__nv_bfloat162*>(&lo);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(t8[2 * e], t8[2 * e + 1]);
+          const float2 hf = __bfloat1622float2(h2);
+          hh[e] = h2;
+          ll[e] = __floats2bfloat162_rn(t8[2 * e] - hf.x, t8[2 * e + 1] - hf.y);
+        }
+        *reinterpret_cast<uint4*>(dst + o0) = hi;
+        *reinterpret_cast<uint4*>(dst + RP + o0) = lo;
+      }
+    }
+    if (finisher && m.ready != nullptr) {
+      // fused kernel: make the slot's t visible to other CTAs' TMA (async proxy), then publish
+      fence_proxy_async_global();
+      named_bar_sync(1 + set, 128);
+      if (set_tid == 0) st_release_gpu(&m.ready[tile], 1);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ standalone kernel
+template <int RP>
+struct ShrinkKernelSmem {
+  using L = ShrinkCfg<RP>;
+  static constexpr int kOffBar = L::kArena;
+  static constexpr int kOffMisc = kOffBar + L::kNumBars * 8;
+  static constexpr int kBytes = kOffMisc + 64 + 1024;
+};
+
+template <int RP>
+__global__ void __launch_bounds__(kApplyThreads, 1) shrink_sigma_kernel(const __grid_constant__ ShrinkParams p) {
+  using S = ShrinkKernelSmem<RP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem + L::kOffA;
-  uint8_t* sB = smem + L::kOffB;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-  uint64_t* empty = full + L::kStages;
-  uint64_t* acc_full = empty + L::kStages;
-  uint64_t* acc_empty = acc_full + kShrinkAccSlots;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);
-  int* s_last = reinterpret_cast<int*>(smem + L::kOffMisc + 16);   // [kEpiSets]
-
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kOffMisc);
+  ShrinkRing R = shrink_ring<RP>(smem, reinterpret_cast<uint64_t*>(smem + S::kOffBar),
+                                 reinterpret_cast<int*>(smem + S::kOffMisc + 16));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     CTS_STAMP(0);
-    for (int s = 0; s < L::kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < kShrinkAccSlots; ++s) {
-      mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], 4);       // one arrival per epilogue warp of the owning set
-    }
+    shrink_init_barriers<RP>(R);
     fence_barrier_init();
   }
-  if (warp == kMmaWarp) tmem_alloc<L::kTmemCols>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<ShrinkCfg<RP>::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int total = p.prefix[p.n_mod];
-  // the prologue above overlaps the previous kernel's tail under PDL; everything below reads data
-  // produced by earlier kernels in the stream
+  R.tmem = *tmem_slot;
+  // the prologue above overlaps the previous kernel's tail under PDL.  Segment outputs may be read
+  // before griddep_wait once another kernel separates this one from cts_segment (meta_ready): the
+  // predecessor only triggers its dependents after its own griddep_wait.
+  int nt_lane = 0;
+  if (p.meta_ready) nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
   griddep_wait();
-  griddep_launch_dependents();
+  if (threadIdx.x == 0) griddep_launch_dependents();
+  if (!p.meta_ready) nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
   if (threadIdx.x == 0) CTS_STAMP(1);
-  // real tile count of each module's map: lane g holds module g's (one load per warp); work items
-  // over the tile bound with tile >= count are empty and skipped without touching memory
-  const int nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
-  auto tile_count = [&](int g) { return __shfl_sync(0xffffffffu, nt_lane, g); };
 
-  if (warp < kProducerWarps) {
-    // ------------------------------------------------------------ TMA producers (K blocks dealt round-robin)
-    int li = 0;                                   // K-block sequence index over this CTA's items
-    for (int item = blockIdx.x; item < total; item += gridDim.x) {
-      const int g = find_module(p.prefix, p.n_mod, item);
-      const ShrinkMod& m = p.mod[g];
-      const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
-      if (tile >= tile_count(g)) continue;        // empty tile slot
-      const int4 t0 = m.tiles[2 * tile], t1 = m.tiles[2 * tile + 1];
-      const int4 r4 = *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
-      const bool shared = t1.z > 0;               // two <=64-token tiles, one per half
-      const int l0 = (t0.z + 3) & ~3, l1 = (t1.z + 3) & ~3;
-      const bool gvalid = shared ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
-      const int ngroups = (l0 + l1) >> 2;
-      const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
-      const uint32_t bytes = static_cast<uint32_t>(ngroups * 512 + (shared ? 2 : 1) * L::kB1);
-      for (int kb = kb0; kb < kb1; ++kb, ++li) {
-        if (li % kProducerWarps != warp) continue;
-        const int stage = li % L::kStages;
-        const uint32_t phase = (li / L::kStages) & 1;
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
-        __syncwarp();
-        uint8_t* dA = sA + stage * L::kA;
-        if (gvalid) tma_gather4(dA + lane * 512, &m.tm_x, &full[stage], kb * kBK, r4.x, r4.y, r4.z, r4.w);
-        if (lane == 0) {
-          tma_load_2d(sB + stage * L::kB, m.tm_in, &full[stage], kb * kBK, t0.x * RP);
-          if (shared) tma_load_2d(sB + stage * L::kB + L::kB1, m.tm_in, &full[stage], kb * kBK, t1.x * RP);
-        }
-        if (li == 0 && lane == 0) CTS_STAMP(2);
-      }
-    }
-    if (lane == 0 && warp == 0) CTS_STAMP(3);
-  } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------ MMA issuer
-    // N = 2 r_pad: the two halves' basis slabs are contiguous in the B stage, so ONE MMA per K step
-    // yields D0 = A B0^T (cols [0, rp)) and D1 = A B1^T (cols [rp, 2rp)); for an unshared slot the
-    // second slab is stale and D1 is never read.  (A second MMA per K step measurably slowed the
-    // single issuing thread.)
-    constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * RP);
-    int stage = 0, slot = 0;
-    uint32_t phase = 0, aphase = 0;
-    for (int item = blockIdx.x; item < total; item += gridDim.x) {
-      const int g = find_module(p.prefix, p.n_mod, item);
-      const ShrinkMod& m = p.mod[g];
-      const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
-      if (tile >= tile_count(g)) continue;
-      const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
-      mbar_wait(&acc_empty[slot], aphase ^ 1);
-      tc_fence_after();
-      const uint32_t acc = tmem + slot * L::kSlotCols;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (kb == kb0 && lane == 0 && item == static_cast<int>(blockIdx.x)) CTS_STAMP(4);
-        if (lane == 0) {
-          const uint32_t a_base = smem_u32(sA + stage * L::kA);
-          const uint32_t b_base = smem_u32(sB + stage * L::kB);
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            umma_bf16(acc, umma_desc_kmajor(a_base + k * 32, 128), umma_desc_kmajor(b_base + k * 32, 128), idesc,
-                      (kb > kb0 || k > 0) ? 1u : 0u);
-          umma_commit(&empty[stage]);
-        }
-        __syncwarp();
-        if (++stage == L::kStages) { stage = 0; phase ^= 1; }
-      }
-      if (lane == 0) umma_commit(&acc_full[slot]);
-      __syncwarp();
-      if (lane == 0) CTS_STAMP(5);
-      if (++slot == kShrinkAccSlots) { slot = 0; aphase ^= 1; }
-    }
-  } else {
-    // ------------------------------------------------------------ epilogue (2 sets x 4 warps, alternate items)
-    const int ew = warp - kEpiWarp0;          // 0..7
-    const int set = ew >> 2;
-    const int quarter = warp & 3;              // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane;
-    const int set_tid = (ew & 3) * 32 + lane;  // 0..127 within the set
-    int li = 0;                                // index over this CTA's non-empty items
-    for (int item = blockIdx.x; item < total; item += gridDim.x) {
-      const int g = find_module(p.prefix, p.n_mod, item);
-      const ShrinkMod& m = p.mod[g];
-      const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
-      if (tile >= tile_count(g)) continue;
-      const bool mine = (li % kEpiSets) == set;
-      const int slot = li % kShrinkAccSlots;
-      const uint32_t aphase = (li / kShrinkAccSlots) & 1;
-      ++li;
-      if (!mine) continue;
-      const int4 t0 = m.tiles[2 * tile], t1 = m.tiles[2 * tile + 1];
-      const int sub = (t1.z > 0 && quarter >= 2) ? 1 : 0;   // which half's tile this warp's rows hold
-      const int slen4 = ((sub ? t1.z : t0.z) + 3) & ~3;
-      const bool rvalid = row - sub * (kTileM / 2) < slen4;
-      const int adapter = rvalid ? m.tile_adapters[tile * kTileM + row] : 0;
-      mbar_wait(&acc_full[slot], aphase);
-      tc_fence_after();
-      if (set_tid == 0) CTS_STAMP(li <= kEpiSets ? 6 : 7);
-      float s[RP];
-#pragma unroll
-      for (int c = 0; c < RP; c += 16)
-        tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * L::kSlotCols + sub * RP + c, s + c);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[slot]);
+  if (warp < kProducerWarps) shrink_producer<RP>(p, R, nt_lane, warp, lane);
+  else if (warp == kMmaWarp) shrink_mma<RP>(p, R, nt_lane, lane);
+  else shrink_epilogue<RP>(p, R, nt_lane, warp, lane);
 
-      bool finisher = true;
-      if (m.ks > 1) {
-        // split-K: publish this chunk's partial; the LAST arriving CTA (acq_rel counter) sums the
-        // ks partials in kc order, so the result does not depend on scheduling
-        if (rvalid) {
-          float4* dst = reinterpret_cast<float4*>(m.ws + (static_cast<size_t>(kc) * m.ws_rows + tile * kTileM + row) * RP);
-#pragma unroll
-          for (int c = 0; c < RP / 4; ++c) dst[c] = make_float4(s[4 * c], s[4 * c + 1], s[4 * c + 2], s[4 * c + 3]);
-        }
-        named_bar_sync(1 + set, 128);
-        if (set_tid == 0) {
-          CTS_STAMP(8);
-          s_last[set] = (atom_add_acq_rel_gpu(&m.counters[tile], 1) == m.ks - 1);
-          CTS_STAMP(9);
-        }
-        named_bar_sync(1 + set, 128);
-        finisher = s_last[set] != 0;
-        if (finisher) {
-          if (rvalid) {
-#pragma unroll
-            for (int c = 0; c < RP; ++c) s[c] = 0.f;
-            for (int q = 0; q < m.ks; ++q) {
-              const float4* src = reinterpret_cast<const float4*>(
-                  m.ws + (static_cast<size_t>(q) * m.ws_rows + tile * kTileM + row) * RP);
-#pragma unroll
-              for (int c = 0; c < RP / 4; ++c) {
-                const float4 v = __ldcg(src + c);
-                s[4 * c] += v.x; s[4 * c + 1] += v.y; s[4 * c + 2] += v.z; s[4 * c + 3] += v.w;
-              }
-            }
-          }
-          if (set_tid == 0) m.counters[tile] = 0;       // ready for the next launch
-        }
-      }
-      if (finisher && rvalid) {
-        // t = scale * Sigma_i s ; thread = token row
-        const uint4* srow = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
-        __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP);
-#pragma unroll 1
-        for (int o0 = 0; o0 < RP; o0 += 8) {
-          float t8[8];
-#pragma unroll
-          for (int oo = 0; oo < 8; ++oo) {
-            const int o = o0 + oo;
-            float acc = 0.f;
-#pragma unroll
-            for (int v8 = 0; v8 < RP / 8; ++v8) {
-              const uint4 w = __ldg(srow + (o * RP) / 8 + v8);
-              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h[e]);
-                acc = fmaf(f.x, s[v8 * 8 + 2 * e], acc);
-                acc = fmaf(f.y, s[v8 * 8 + 2 * e + 1], acc);
-              }
-            }
-            t8[oo] = acc * m.scale;
-          }
-          uint4 hi, lo;
-          __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&hi);
-          __nv_bfloat162* ll = reinterpret_cast<__nv_bfloat162*>(&lo);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const __nv_bfloat162 h2 = __floats2bfloat162_rn(t8[2 * e], t8[2 * e + 1]);
-            const float2 hf = __bfloat1622float2(h2);
-            hh[e] = h2;
-            ll[e] = __floats2bfloat162_rn(t8[2 * e] - hf.x, t8[2 * e + 1] - hf.y);
-          }
-          *reinterpret_cast<uint4*>(dst + o0) = hi;
-          *reinterpret_cast<uint4*>(dst + RP + o0) = lo;
-        }
-      }
-    }
-  }
-  if (threadIdx.x == 32 * kEpiWarp0) CTS_STAMP(10);
   __syncthreads();
-  if (warp == kMmaWarp) tmem_dealloc<L::kTmemCols>(tmem);
+  if (warp == kMmaWarp) tmem_dealloc<ShrinkCfg<RP>::kTmemCols>(R.tmem);
   if (threadIdx.x == 0) CTS_STAMP(11);
 }
 

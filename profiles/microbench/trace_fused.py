@@ -1,0 +1,45 @@
+"""Per-CTA timeline of fused apply launches at decode (q,k,v group; gate,up group) from a CTS_TRACE
+build: when phase 1 (shrink) issues, finishes, when phase 2 (expand) gets its first t, ends."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import paper_2407_00066_b200 as cts  # noqa: E402
+from workloads.gen_torch import direct_bank_torch, tokens_torch  # noqa: E402
+
+T, N, C, r = int(os.environ.get("T", 1024)), 1000, 25, 16
+dev = torch.device("cuda")
+mods = [(4096, 4096), (4096, 1024), (4096, 1024), (4096, 14336), (4096, 14336)]
+banks = [direct_bank_torch(di, do, N, C, r, seed=m, device=dev, cluster_seed=50 + m) for m, (di, do) in enumerate(mods)]
+bank = cts.Bank([b["in_basis"] for b in banks], [b["out_basis"] for b in banks], [b["sigma"] for b in banks],
+                [b["cluster_of"] for b in banks])
+plan = cts.Plan(bank, T)
+plan.segment(tokens_torch(T, N, 1, T > 4096, dev))
+x = torch.randn(T, 4096, device=dev).to(torch.bfloat16)
+ys = [torch.randn(T, do, device=dev).to(torch.bfloat16) for (_, do) in mods]
+big = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+L = cts.lib()
+L.cts_debug_trace.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+names = {0: "start", 1: "prologue+wait", 2: "shrink first TMA", 3: "shrink producers done", 4: "shrink MMA done",
+         5: "shrink epi set0 done", 6: "shrink epi set1 done", 7: "phase barrier", 8: "expand first t ready",
+         9: "expand producers done", 10: "expand epi done", 11: "end"}
+for grp in ([0, 1, 2], [3, 4]):
+    for rep in range(3):
+        big.zero_()
+        plan.apply_group(grp, [x] * len(grp), [ys[m] for m in grp], 2.0)
+        torch.cuda.synchronize()
+    buf = (ctypes.c_ulonglong * (160 * 16))()
+    L.cts_debug_trace(buf, 160 * 16)
+    a = np.array(buf, dtype=np.int64).reshape(160, 16)[:148].astype(np.float64)
+    t0 = a[:, 0].min()
+    rel = (a - t0) / 1e3
+    print(f"fused group {grp} (T={T}): us after first CTA start: min / median / max over CTAs")
+    for i, n in names.items():
+        col = rel[:, i]
+        col = col[(col >= 0) & (col < 1e4)]
+        if col.size:
+            print(f"  {n:24s} {col.min():8.2f} {np.median(col):8.2f} {col.max():8.2f}  (n={col.size})")
