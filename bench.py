@@ -323,11 +323,25 @@ def run_gpu(args, cfg):
         if args.profile:                         # ncu mode: exactly one more eager step, no timing
             step()
             torch.cuda.synchronize()
-            print(f"profile mode: 2 eager steps of {1 + 2 * len(groups)} launches each", file=sys.stderr)
+            # algorithmic bytes of every apply launch of the step, in launch order (for
+            # profiles/make_traffic.py, which divides ncu's dram bytes of the same launches by them)
+            bs, be = algorithmic_bytes(tokens.cpu().numpy(), cmaps, mods, r)
+            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+            with open(os.path.join(ROOT, "gpurun_out", f"{cfg['workload']}_alg_bytes.json"), "w") as f:
+                json.dump({"workload": cfg["workload"], "groups": groups,
+                           "shrink": [float(bs[gm].sum()) for gm in groups],
+                           "expand": [float(be[gm].sum()) for gm in groups]}, f)
+            print(f"profile mode: 2 eager steps of {1 + len(groups)} launches each (fused)", file=sys.stderr)
             return 0
         graph = torch.cuda.CUDAGraph()
+        n0 = cts.cts_launch_count()
         with torch.cuda.graph(graph, stream=stream):
             step()
+        launches_per_step = cts.cts_launch_count() - n0       # counted by libcts, not assumed
+        g_apply = torch.cuda.CUDAGraph()                      # the step minus its segment launch
+        with torch.cuda.graph(g_apply, stream=stream):
+            for gm in groups:
+                plan.apply_group(gm, [xs[m] for m in gm], [ys[m] for m in gm], SCALE)
         g_shrink = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_shrink, stream=stream):
             for gm in groups:
@@ -356,7 +370,8 @@ def run_gpu(args, cfg):
             dist.barrier()
         ms_total = e0.elapsed_time(e1)
 
-        # --- per-kernel timing: all 224 shrinks / all 224 expands as their own graphs
+        # --- per-kernel timing: all applies (the fused kernel), and the split path's shrinks /
+        #     expands, each as its own graph of NL launches
         def time_graph(gr, reps):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             gr.replay()
@@ -367,6 +382,7 @@ def run_gpu(args, cfg):
             b.synchronize()
             return a.elapsed_time(b) / reps
         kreps = max(3, min(args.steps, 50))
+        ms_apply = time_graph(g_apply, kreps)
         ms_shrink = time_graph(g_shrink, kreps)
         ms_expand = time_graph(g_expand, kreps)
 
@@ -411,7 +427,8 @@ def run_gpu(args, cfg):
     # --- aggregate over ranks
     per_step = ms_total / args.steps
     if world > 1:
-        per_step, ms_e2e, ms_shrink, ms_expand = reduce_max([per_step, ms_e2e, ms_shrink, ms_expand], dist, dev)
+        per_step, ms_e2e, ms_apply, ms_shrink, ms_expand = reduce_max(
+            [per_step, ms_e2e, ms_apply, ms_shrink, ms_expand], dist, dev)
     value = T * world / (per_step / 1e3)
     e2e_value = T * world / (ms_e2e / 1e3)
 
@@ -419,8 +436,13 @@ def run_gpu(args, cfg):
     tok_np = tokens.cpu().numpy()
     b_shrink, b_expand = algorithmic_bytes(tok_np, cmaps, mods, r)
     hbm, bf16_peak, peak_src = measured_peaks()
+    fused = launches_per_step == 1 + NL
     kern = {"shrink_sigma_kernel": (b_shrink.sum(), ms_shrink), "expand_kernel": (b_expand.sum(), ms_expand)}
-    dom = max(kern, key=lambda k: kern[k][1])
+    if fused:                            # the step launches segment + one apply_fused_kernel per group
+        kern["apply_fused_kernel"] = (b_shrink.sum() + b_expand.sum(), ms_apply)
+        dom = "apply_fused_kernel"
+    else:
+        dom = max(kern, key=lambda k: kern[k][1])
     dom_bytes, dom_ms = kern[dom]
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     traffic, traffic_alg = ncu_traffic(cfg["workload"], dom)
@@ -437,12 +459,14 @@ def run_gpu(args, cfg):
                      "launches_per_step": NL,
                      "path": {"algorithmic_bytes_per_step": b_shrink.sum() + b_expand.sum(),
                               "achieved_gbs": path_gbs, "frac": path_gbs / hbm},
+                     "step_share": dom_ms / per_step,
                      "kernels": {k: {"algorithmic_bytes_per_launch": v[0] / NL, "avg_launch_us": v[1] / NL * 1e3,
                                      "achieved_gbs": v[0] / (v[1] / 1e3) / 1e9,
                                      "frac": v[0] / (v[1] / 1e3) / 1e9 / hbm} for k, v in kern.items()}},
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "note": "public API with pinned host buffers; H2D of ids, x and y_base, D2H of y, per step"},
-        "gpu_launches": args.steps * (1 + 2 * len(groups)),
+        "gpu_launches": args.steps * launches_per_step,
+        "launches_per_step": launches_per_step,
         "clocks": clocks.result(),
     }
     if world > 1:

@@ -163,6 +163,13 @@ cts_status_t cts_plan_error(cts_plan_t plan, int32_t* code, int32_t* first_bad_t
 /* Static description of a status code. */
 const char* cts_status_string(cts_status_t status);
 
+/* Number of kernels this library has enqueued since it was loaded (process-wide, all banks and
+ * plans; launches recorded into a CUDA graph under stream capture count once, at capture).  The
+ * difference across a call sequence is that sequence's kernel count: cts_segment = 1,
+ * cts_apply / cts_apply_group = 1 (fused kernel; 2 with CTS_FUSED=0), cts_shrink* = cts_expand* = 1,
+ * cts_bank_load = 3 per module.  Never fails. */
+uint64_t cts_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

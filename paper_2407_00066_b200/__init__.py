@@ -9,6 +9,7 @@ from .api import (  # noqa: F401
     cts_expand_group,
     cts_shrink_group,
     cts_expand,
+    cts_launch_count,
     cts_shrink,
     cts_bank_bytes,
     cts_bank_free,

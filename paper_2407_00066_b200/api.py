@@ -174,6 +174,11 @@ def cts_plan_error(plan):
     return code.value, bad.value
 
 
+def cts_launch_count():
+    """Kernels libcts has enqueued since load (graph captures count once, at capture)."""
+    return int(lib().cts_launch_count())
+
+
 class Bank:
     """Owner of a resident compressed bank (frees it on close / garbage collection)."""
 

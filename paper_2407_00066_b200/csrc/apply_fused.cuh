@@ -8,11 +8,12 @@
 // item waits only for ITS slot: the split-K finisher publishes a per-slot "t ready" flag
 // (st.release after fence.proxy.async, so the TMA reads of other CTAs see the bf16 t rows) and the
 // expand producer polls it (ld.acquire) before loading t.  Progress is guaranteed because the grid
-// is at most one CTA per SM (all CTAs co-resident) and every CTA finishes all its shrink items --
-// which never wait on anything -- before starting expand items.
+// is at most one CTA per SM (all CTAs co-resident), every role of a CTA finishes its shrink work
+// before it takes expand work, and no shrink step ever waits on an expand step.
 //
-// Shared memory: the two phases reuse one operand arena (a CTA barrier separates them) and keep
-// separate mbarrier sets; TMEM is allocated once (512 columns) and reused.  The ready flags are
+// Shared memory: the two phases reuse one operand arena and keep separate mbarrier sets; TMEM is
+// allocated once (512 columns) and reused.  The phase change is per role (see below), not a CTA
+// barrier, so a CTA's expand loads overlap its own split-K finisher work.  The ready flags are
 // cleared by the last CTA to exit (per-plan exit counter), so the next launch starts from zero even
 // when replayed from a CUDA graph.
 #pragma once
@@ -33,7 +34,8 @@ struct FusedSmem {
                                                                                 : ExpandCfg<RP>::kArena;
   static constexpr int kOffBarS = kArena;
   static constexpr int kOffBarE = kOffBarS + ShrinkCfg<RP>::kNumBars * 8;
-  static constexpr int kOffMisc = kOffBarE + ExpandCfg<RP>::kNumBars * 8;
+  static constexpr int kOffBarF = kOffBarE + ExpandCfg<RP>::kNumBars * 8;   // "shrink operands consumed"
+  static constexpr int kOffMisc = kOffBarF + 8;
   static constexpr int kBytes = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;
   static_assert(ShrinkCfg<RP>::kTmemCols <= kTmemCols && ExpandCfg<RP>::kTmemCols <= kTmemCols, "TMEM");
@@ -49,11 +51,13 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   ShrinkRing RS = shrink_ring<RP>(smem, reinterpret_cast<uint64_t*>(smem + S::kOffBarS),
                                   reinterpret_cast<int*>(smem + S::kOffMisc + 16));
   ExpandRing RE = expand_ring<RP>(smem, reinterpret_cast<uint64_t*>(smem + S::kOffBarE));
+  uint64_t* arena_free = reinterpret_cast<uint64_t*>(smem + S::kOffBarF);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     CTS_STAMP(0);
-    shrink_init_barriers<RP>(RS);
+    shrink_init_barriers<RP>(RS, p.s.x_cpasync);
     expand_init_barriers<RP>(RE);
+    mbar_init(arena_free, 1);
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<S::kTmemCols>(tmem_slot);
@@ -63,29 +67,43 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   RS.tmem = RE.tmem = *tmem_slot;
   // shrink and expand items cover the same modules, so one per-module slot count serves both
   int nt_lane = 0;
-  if (p.s.meta_ready) nt_lane = lane < p.s.n_mod ? *p.s.mod[lane].n_tiles : 0;
+  ShrinkFirst first;
+  if (p.s.meta_ready) {
+    nt_lane = lane < p.s.n_mod ? *p.s.mod[lane].n_tiles : 0;
+    if (warp < kProducerWarps) first = shrink_first_meta(p.s, nt_lane, lane);
+  }
   griddep_wait();
   if (threadIdx.x == 0) griddep_launch_dependents();
   if (!p.s.meta_ready) nt_lane = lane < p.s.n_mod ? *p.s.mod[lane].n_tiles : 0;
   if (threadIdx.x == 0) CTS_STAMP(1);
 
-  // ---------------------------------------------------------------- phase 1: shrink + Sigma
-  if (warp < kProducerWarps) shrink_producer<RP>(p.s, RS, nt_lane, warp, lane);
-  else if (warp == kMmaWarp) shrink_mma<RP>(p.s, RS, nt_lane, lane);
-  else shrink_epilogue<RP>(p.s, RS, nt_lane, warp, lane);
-  if (threadIdx.x == 0) CTS_STAMP(3);                 // producers done issuing
-  if (warp == kMmaWarp && lane == 0) CTS_STAMP(4);    // last shrink MMA issued
-  if (threadIdx.x == 32 * kEpiWarp0) CTS_STAMP(5);    // epilogue set 0 done
-  if (threadIdx.x == 32 * (kEpiWarp0 + 4)) CTS_STAMP(6);   // epilogue set 1 done
-  tc_fence_before();
-  __syncthreads();                          // arena and TMEM free: all shrink stages consumed
-  tc_fence_after();
-  if (threadIdx.x == 0) CTS_STAMP(7);
-
-  // ---------------------------------------------------------------- phase 2: expand + residual
-  if (warp < kProducerWarps) expand_producer<RP>(p.e, RE, nt_lane, warp, lane);
-  else if (warp == kMmaWarp) expand_mma<RP>(p.e, RE, nt_lane, lane);
-  else expand_epilogue<RP, DIRECT>(p.e, RE, nt_lane, warp, lane);
+  // ---------------------------------------------------------------- phase 1 -> phase 2, per role
+  // No CTA-wide barrier between the phases: each role moves on as soon as what it reuses is free.
+  //   producers: the operand arena, once the shrink MMAs have consumed every stage (arena_free,
+  //              committed by the MMA warp after its last MMA);
+  //   MMA warp:  the TMEM columns, once the epilogue has read every shrink accumulator;
+  //   epilogue:  nothing -- it takes expand items after its own split-K / Sigma work, so expand
+  //              loads and MMAs of this CTA overlap its shrink finisher chain.
+  if (warp < kProducerWarps) {
+    shrink_producer<RP>(p.s, RS, nt_lane, warp, lane, first);
+    if (threadIdx.x == 0) CTS_STAMP(3);               // producers done issuing
+    mbar_wait(arena_free, 0);
+    if (threadIdx.x == 0) CTS_STAMP(7);
+    expand_producer<RP>(p.e, RE, nt_lane, warp, lane);
+  } else if (warp == kMmaWarp) {
+    int slot = 0;
+    uint32_t aphase = 0;
+    shrink_mma<RP>(p.s, RS, nt_lane, lane, &slot, &aphase);
+    if (lane == 0) { umma_commit(arena_free); CTS_STAMP(4); }
+    __syncwarp();
+    shrink_drain_tmem(RS, slot, aphase);
+    expand_mma<RP>(p.e, RE, nt_lane, lane);
+  } else {
+    shrink_epilogue<RP>(p.s, RS, nt_lane, warp, lane);
+    if (threadIdx.x == 32 * kEpiWarp0) CTS_STAMP(5);        // epilogue set 0 done
+    if (threadIdx.x == 32 * (kEpiWarp0 + 4)) CTS_STAMP(6);  // epilogue set 1 done
+    expand_epilogue<RP, DIRECT>(p.e, RE, nt_lane, warp, lane);
+  }
 
   // ---------------------------------------------------------------- exit: last CTA clears flags
   if (threadIdx.x == 0) CTS_STAMP(9);

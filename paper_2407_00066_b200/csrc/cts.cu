@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -193,6 +194,28 @@ bool expand_direct_store(int T, int C) {
   return T < 96 * C;   // mean tokens per cluster < 96
 }
 
+// fused kernel, expand producer: poll the slot's t-ready flag before (1) or after (0) issuing the
+// item's out_basis / y loads.  CTS_POLL_FIRST overrides (tuning aid).
+int poll_first_default(int T, int C) {
+  static int v = [] {
+    const char* e = std::getenv("CTS_POLL_FIRST");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (v >= 0) return v != 0;
+  return T < 96 * C ? 0 : 1;
+}
+
+// shrink x rows: per-thread cp.async (1) or TMA tile::gather4 (0).  Measured on B200 (fused step):
+// gather4 235k / 584k tok/s (decode / prefill) vs cp.async 197k / 554k, so gather4 is the default;
+// CTS_X_CPASYNC=1 selects cp.async (tuning aid; both paths pass the parity suite).
+int x_cpasync_default() {
+  static int v = [] {
+    const char* e = std::getenv("CTS_X_CPASYNC");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
 // cts_apply[_group] runs the fused single-launch kernel unless CTS_FUSED=0 (tuning aid).
 bool use_fused() {
   static bool v = [] {
@@ -204,6 +227,8 @@ bool use_fused() {
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while the previous
 // kernel in the stream drains; every kernel calls griddep_wait() before touching dependent data.
+std::atomic<uint64_t> g_launches{0};          // kernels this library enqueued (cts_launch_count)
+
 template <typename Kern, typename... Args>
 cudaError_t launch_pdl(Kern kernel, int grid, int block, size_t smem, cudaStream_t stream, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -216,7 +241,9 @@ cudaError_t launch_pdl(Kern kernel, int grid, int block, size_t smem, cudaStream
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, args...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
+  return e;
 }
 
 __nv_bfloat16* module_tbuf(cts_plan_t p, int module) {
@@ -252,6 +279,8 @@ cts_status_t fill_shrink(cts_plan_t p, int n, const int32_t* modules, const void
     const Module& m = b->mods[modules[i]];
     ShrinkMod& sm = prm.mod[i];
     if (!make_tmap(&sm.tm_x, xs[i], m.d_in, T, ld_x[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
+    sm.x = static_cast<const __nv_bfloat16*>(xs[i]);
+    sm.ld_x = ld_x[i];
     sm.tm_in = b->d_tm_in + modules[i];
     const size_t mid = m.map_id;
     sm.tiles = p->tiles + mid * p->max_tiles * 2;
@@ -269,6 +298,7 @@ cts_status_t fill_shrink(cts_plan_t p, int n, const int32_t* modules, const void
     sm.scale = scale;
     prm.prefix[i + 1] = prm.prefix[i] + tiles_bound * ks;
   }
+  prm.x_cpasync = x_cpasync_default();
   items = prm.prefix[n];
   return CTS_OK;
 }
@@ -343,6 +373,7 @@ cts_status_t launch_fused(cts_plan_t p, int n, const int32_t* modules, const voi
   if (st != CTS_OK) return st;
   if ((st = fill_expand(p, n, modules, ys, ld_y, true, prm.e, items_e)) != CTS_OK) return st;
   prm.s.meta_ready = prm.e.meta_ready = next_meta_ready(p);
+  prm.e.poll_first = poll_first_default(p->T, p->bank->C);
   prm.exit_count = p->exit_count;
   CTS_CUDA(launch_pdl(apply_fused_kernel<RP, DIRECT>, std::min(sm_count(), std::max(items_s, items_e)), kApplyThreads,
                       FusedSmem<RP>::kBytes, stream, prm));
@@ -421,6 +452,8 @@ const char* cts_status_string(cts_status_t s) {
   }
   return "unknown status";
 }
+
+uint64_t cts_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_bank_t* out) {
   if (!out) return CTS_ERR_INVALID_ARGUMENT;
@@ -508,6 +541,7 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
       if (k == 1) relayout_pad_kernel<<<1184, 256, 0, stream>>>(src, mod.out, size_t(C) * mod.d_out, r, rp);
       if (k == 2) relayout_sigma_kernel<<<1184, 256, 0, stream>>>(src, mod.sigma, N, r, rp);
       if (cudaGetLastError() != cudaSuccess) return fail(CTS_ERR_CUDA);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
       if (!d->sources_on_device && cudaStreamSynchronize(stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
     }
     if (!make_tmap(&h_tm[m], mod.in_t, mod.d_in, uint64_t(C) * rp, uint64_t(mod.d_in) * 2, 64, rp,

@@ -54,6 +54,7 @@ struct ExpandParams {
   int prefix[kMaxGroup + 1];             // item prefix over modules (tile bound * nblk each)
   int n_mod;
   int meta_ready;                        // 1: segment outputs are complete before griddep_wait
+  int poll_first;                        // fused: 1 = wait for t before issuing the item's loads
 };
 
 template <int RP>
@@ -144,12 +145,14 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
     const int l0 = (t0.z + 3) & ~3, l1 = (t1.z + 3) & ~3;
     const bool gvalid = shared ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
     const int ngroups = (l0 + l1) >> 2;
-    if (m.ready != nullptr) {                     // fused kernel: t of this slot published?
-      if (lane == 0)
+    const bool poll_late = m.ready != nullptr && !p.poll_first;
+    if (m.ready != nullptr && p.poll_first) {
+      if (lane == 0) {
         while (ld_acquire_gpu(m.ready + tile) == 0) nanosleep_ns(64);
+        fence_proxy_async_global();
+        if (my == 0) CTS_STAMP(8);
+      }
       __syncwarp();
-      fence_proxy_async_global();
-      if (lane == 0 && my == 0) CTS_STAMP(8);      // first expand item's t available
     }
     mbar_wait(&R.empty[stage], phase ^ 1);
     *reinterpret_cast<int4*>(stage_rows<RP>(R, stage) + 4 * lane) = r4;
@@ -158,11 +161,11 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
       stage_info<RP>(R, stage)[1] = make_int4(t1.x, t1.z, 0, 0);
     }
     __syncwarp();
+    // out_basis blocks and y rows do not depend on the shrink: issue them first, so in the fused
+    // kernel they stream in while this slot's t is still being reduced
     if (lane == 0) {
       mbar_arrive_expect_tx(&R.full[stage], static_cast<uint32_t>(2 * L::kA + (shared ? 2 : 1) * L::kB1 +
                                                                    L::kSeg * ngroups * 512));
-      tma_load_2d(stage_a<RP>(R, stage), m.tm_t, &R.full[stage], 0, tile * kTileM);
-      tma_load_2d(stage_a<RP>(R, stage) + L::kA, m.tm_t, &R.full[stage], RP, tile * kTileM);
 #pragma unroll
       for (int s = 0; s < L::kSeg; ++s) {
         tma_load_2d(stage_b<RP>(R, stage) + s * 64 * RP * 2, m.tm_out, &R.full[stage], 0,
@@ -179,6 +182,16 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
         tma_gather4(stage_y<RP>(R, stage) + s * L::kY + lane * 512, &m.tm_y, &R.full[stage], nb * kBN + s * 64, r4.x,
                     r4.y, r4.z, r4.w);
     }
+    if (lane == 0) {
+      if (poll_late) {                            // fused kernel: t of this slot published?
+        while (ld_acquire_gpu(m.ready + tile) == 0) nanosleep_ns(64);
+        fence_proxy_async_global();
+        if (my == 0) CTS_STAMP(8);                // first expand item's t available
+      }
+      tma_load_2d(stage_a<RP>(R, stage), m.tm_t, &R.full[stage], 0, tile * kTileM);
+      tma_load_2d(stage_a<RP>(R, stage) + L::kA, m.tm_t, &R.full[stage], RP, tile * kTileM);
+    }
+    __syncwarp();
   }
 }
 

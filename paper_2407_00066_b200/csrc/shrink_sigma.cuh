@@ -54,6 +54,8 @@ constexpr int kShrinkAccSlots = 4;
 
 struct alignas(64) ShrinkMod {
   CUtensorMap tm_x;                     // x [T][d_in], box {64, 1}, 128B swizzle (per call)
+  const __nv_bfloat16* x;               // x base and row stride (elements), for the cp.async path
+  int64_t ld_x;
   const CUtensorMap* tm_in;             // in_basis [C*rp][d_in], box {64, rp} (bank, global mem)
   const int4* tiles;                    // [slot][2]: (cluster, start, len, -) per 64-row half
   const int32_t* n_tiles;               // real slot count of this module's map
@@ -75,6 +77,7 @@ struct ShrinkParams {
   int prefix[kMaxGroup + 1];            // item prefix over modules (tile bound * ks each)
   int n_mod;
   int meta_ready;                       // 1: segment outputs are complete before griddep_wait
+  int x_cpasync;                        // 1: x rows by per-thread cp.async, 0: TMA tile::gather4
 };
 
 template <int RP>
@@ -126,9 +129,9 @@ __device__ __forceinline__ ShrinkRing shrink_ring(uint8_t* arena, uint64_t* bars
 }
 
 template <int RP>
-__device__ __forceinline__ void shrink_init_barriers(const ShrinkRing& R) {   // one thread
+__device__ __forceinline__ void shrink_init_barriers(const ShrinkRing& R, int x_cpasync) {   // one thread
   for (int s = 0; s < ShrinkCfg<RP>::kStages; ++s) {
-    mbar_init(&R.full[s], 1);
+    mbar_init(&R.full[s], x_cpasync ? 33 : 1);  // cp.async path: the 32 lanes + the B-slab expect_tx
     mbar_init(&R.empty[s], 1);
   }
   for (int s = 0; s < kShrinkAccSlots; ++s) {
@@ -138,8 +141,34 @@ __device__ __forceinline__ void shrink_init_barriers(const ShrinkRing& R) {   //
 }
 
 // ------------------------------------------------------------------ TMA producers (warps 0-3)
+// Tile metadata of a CTA's first non-empty item, loaded before griddep_wait when the segment
+// outputs are already complete (meta_ready), so the first gathers issue right after the wait
+// instead of after two dependent global loads.
+struct ShrinkFirst {
+  int item = -1;
+  int4 t0, t1, r4;
+};
+
+__device__ __forceinline__ ShrinkFirst shrink_first_meta(const ShrinkParams& p, int nt_lane, int lane) {
+  ShrinkFirst f;
+  const int total = p.prefix[p.n_mod];
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int g = find_module(p.prefix, p.n_mod, item);
+    const ShrinkMod& m = p.mod[g];
+    const int tile = (item - p.prefix[g]) / m.ks;
+    if (tile >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;
+    f.item = item;
+    f.t0 = m.tiles[2 * tile];
+    f.t1 = m.tiles[2 * tile + 1];
+    f.r4 = *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
+    break;
+  }
+  return f;
+}
+
 template <int RP>
-__device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int warp, int lane) {
+__device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int warp, int lane,
+                                const ShrinkFirst& first = ShrinkFirst()) {
   using L = ShrinkCfg<RP>;
   const int total = p.prefix[p.n_mod];
   int li = 0;                                     // K-block sequence index over this CTA's items
@@ -148,14 +177,33 @@ __device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, int 
     const ShrinkMod& m = p.mod[g];
     const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
     if (tile >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;   // empty tile slot
-    const int4 t0 = m.tiles[2 * tile], t1 = m.tiles[2 * tile + 1];
-    const int4 r4 = *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
+    const bool pre = item == first.item;
+    const int4 t0 = pre ? first.t0 : m.tiles[2 * tile], t1 = pre ? first.t1 : m.tiles[2 * tile + 1];
+    const int4 r4 = pre ? first.r4 : *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
     const bool shared = t1.z > 0;                 // two <=64-token tiles, one per half
     const int l0 = (t0.z + 3) & ~3, l1 = (t1.z + 3) & ~3;
     const bool gvalid = shared ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
     const int ngroups = (l0 + l1) >> 2;
     const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
-    const uint32_t bytes = static_cast<uint32_t>(ngroups * 512 + (shared ? 2 : 1) * L::kB1);
+    const uint32_t bbytes = static_cast<uint32_t>((shared ? 2 : 1) * L::kB1);
+    const uint32_t bytes = p.x_cpasync ? bbytes : static_cast<uint32_t>(ngroups * 512) + bbytes;
+    // cp.async path: lane copies 16-byte chunk (lane & 7) of rows (lane >> 3) + 4j, j < 32, into its
+    // 128B-swizzled place (chunk ^ row % 8); the row tokens come from the 4-row groups r4 of lane
+    // (row >> 2) by shuffle, once per item
+    int tok[32];
+    uint32_t vmask = 0;
+    if (p.x_cpasync) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int r = (lane >> 3) + 4 * j;                  // slot row; its 4-row group is r >> 2 = j
+        const int4 g4 = make_int4(__shfl_sync(0xffffffffu, r4.x, j), __shfl_sync(0xffffffffu, r4.y, j),
+                                  __shfl_sync(0xffffffffu, r4.z, j), __shfl_sync(0xffffffffu, r4.w, j));
+        const int q = r & 3;
+        tok[j] = q == 0 ? g4.x : q == 1 ? g4.y : q == 2 ? g4.z : g4.w;
+        const bool v = shared ? (r < kTileM / 2 ? r < l0 : r - kTileM / 2 < l1) : r < l0;
+        vmask |= static_cast<uint32_t>(v) << j;
+      }
+    }
     for (int kb = kb0; kb < kb1; ++kb, ++li) {
       if (li % kProducerWarps != warp) continue;
       const int stage = li % L::kStages;
@@ -164,7 +212,19 @@ __device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, int 
       if (lane == 0) mbar_arrive_expect_tx(&R.full[stage], bytes);
       __syncwarp();
       uint8_t* dA = R.sA + stage * L::kA;
-      if (gvalid) tma_gather4(dA + lane * 512, &m.tm_x, &R.full[stage], kb * kBK, r4.x, r4.y, r4.z, r4.w);
+      if (p.x_cpasync) {
+        const int c = lane & 7;
+        const __nv_bfloat16* src = m.x + kb * kBK + c * 8;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int r = (lane >> 3) + 4 * j;
+          if (vmask & (1u << j))
+            cp_async16(dA + r * 128 + ((c ^ (r & 7)) << 4), src + static_cast<int64_t>(tok[j]) * m.ld_x);
+        }
+        cp_async_mbar_arrive(&R.full[stage]);
+      } else if (gvalid) {
+        tma_gather4(dA + lane * 512, &m.tm_x, &R.full[stage], kb * kBK, r4.x, r4.y, r4.z, r4.w);
+      }
       if (lane == 0) {
         tma_load_2d(R.sB + stage * L::kB, m.tm_in, &R.full[stage], kb * kBK, t0.x * RP);
         if (shared) tma_load_2d(R.sB + stage * L::kB + L::kB1, m.tm_in, &R.full[stage], kb * kBK, t1.x * RP);
@@ -175,8 +235,11 @@ __device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, int 
 }
 
 // ------------------------------------------------------------------ MMA issuer (warp 4)
+// Returns once every MMA is issued; on return the accumulator ring position is (*acc_slot, *acc_phase)
+// so the fused kernel can wait for the epilogue to drain it (shrink_drain_tmem).
 template <int RP>
-__device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int lane) {
+__device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int lane,
+                           int* acc_slot = nullptr, uint32_t* acc_phase = nullptr) {
   using L = ShrinkCfg<RP>;
   // N = 2 r_pad: the two halves' basis slabs are contiguous in the B stage, so ONE MMA per K step
   // yields D0 = A B0^T (cols [0, rp)) and D1 = A B1^T (cols [rp, 2rp)); for an unshared slot the
@@ -214,6 +277,17 @@ __device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, int nt_la
     __syncwarp();
     if (++slot == kShrinkAccSlots) { slot = 0; aphase ^= 1; }
   }
+  if (acc_slot) { *acc_slot = slot; *acc_phase = aphase; }
+}
+
+// MMA warp: wait until the epilogue has read every accumulator slot the shrink used (the next
+// kShrinkAccSlots acquisitions of the ring), so the TMEM columns can be reused.
+__device__ __forceinline__ void shrink_drain_tmem(const ShrinkRing& R, int slot, uint32_t aphase) {
+  for (int k = 0; k < kShrinkAccSlots; ++k) {
+    mbar_wait(&R.acc_empty[slot], aphase ^ 1);
+    if (++slot == kShrinkAccSlots) { slot = 0; aphase ^= 1; }
+  }
+  tc_fence_after();
 }
 
 // ------------------------------------------------------------------ epilogue (warps 5-12)
@@ -271,6 +345,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int 
       if (set_tid == 0) R.s_last[set] = (atom_add_acq_rel_gpu(&m.counters[tile], 1) == m.ks - 1);
       named_bar_sync(1 + set, 128);
       finisher = R.s_last[set] != 0;
+      if (set_tid == 0 && finisher) CTS_STAMP(12);         // last arrival known
       if (finisher) {
         if (rvalid) {
           // sum the partials in kc order (deterministic); this CTA's own chunk comes from registers
@@ -293,6 +368,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int 
           }
         }
         if (set_tid == 0) m.counters[tile] = 0;       // ready for the next launch
+        if (set_tid == 0) CTS_STAMP(13);                // partials summed
       }
     }
     if (finisher && rvalid) {
@@ -335,9 +411,11 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int 
     }
     if (finisher && m.ready != nullptr) {
       // fused kernel: make the slot's t visible to other CTAs' TMA (async proxy), then publish
+      if (set_tid == 0) CTS_STAMP(14);                  // t stored
       fence_proxy_async_global();
       named_bar_sync(1 + set, 128);
       if (set_tid == 0) st_release_gpu(&m.ready[tile], 1);
+      if (set_tid == 0) CTS_STAMP(15);                  // flag published
     }
   }
 }
@@ -362,7 +440,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) shrink_sigma_kernel(const __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     CTS_STAMP(0);
-    shrink_init_barriers<RP>(R);
+    shrink_init_barriers<RP>(R, p.x_cpasync);
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<ShrinkCfg<RP>::kTmemCols>(tmem_slot);
@@ -374,13 +452,17 @@ __global__ void __launch_bounds__(kApplyThreads, 1) shrink_sigma_kernel(const __
   // before griddep_wait once another kernel separates this one from cts_segment (meta_ready): the
   // predecessor only triggers its dependents after its own griddep_wait.
   int nt_lane = 0;
-  if (p.meta_ready) nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
+  ShrinkFirst first;
+  if (p.meta_ready) {
+    nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
+    if (warp < kProducerWarps) first = shrink_first_meta(p, nt_lane, lane);
+  }
   griddep_wait();
   if (threadIdx.x == 0) griddep_launch_dependents();
   if (!p.meta_ready) nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
   if (threadIdx.x == 0) CTS_STAMP(1);
 
-  if (warp < kProducerWarps) shrink_producer<RP>(p, R, nt_lane, warp, lane);
+  if (warp < kProducerWarps) shrink_producer<RP>(p, R, nt_lane, warp, lane, first);
   else if (warp == kMmaWarp) shrink_mma<RP>(p, R, nt_lane, lane);
   else shrink_epilogue<RP>(p, R, nt_lane, warp, lane);
 

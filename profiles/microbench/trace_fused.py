@@ -25,8 +25,10 @@ big = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 L = cts.lib()
 L.cts_debug_trace.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 names = {0: "start", 1: "prologue+wait", 2: "shrink first TMA", 3: "shrink producers done", 4: "shrink MMA done",
-         5: "shrink epi set0 done", 6: "shrink epi set1 done", 7: "phase barrier", 8: "expand first t ready",
-         9: "expand producers done", 10: "expand epi done", 11: "end"}
+         5: "shrink epi set0 done", 6: "shrink epi set1 done", 7: "expand producers start", 8: "expand first t ready",
+         9: "expand producers done", 10: "expand epi done", 11: "end",
+         12: "finisher: last arrival", 13: "finisher: partials summed", 14: "finisher: t stored",
+         15: "finisher: flag published"}
 for grp in ([0, 1, 2], [3, 4]):
     for rep in range(3):
         big.zero_()

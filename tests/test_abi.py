@@ -19,7 +19,7 @@ def lib():
 
 def header_functions():
     src = open(os.path.join(ROOT, "include", "cts.h")).read()
-    return set(re.findall(r"^\s*(?:cts_status_t|int32_t|const char\*)\s+(cts_\w+)\s*\(", src, re.M))
+    return set(re.findall(r"^\s*(?:cts_status_t|int32_t|uint64_t|const char\*)\s+(cts_\w+)\s*\(", src, re.M))
 
 
 def test_header_and_binding_agree(lib):

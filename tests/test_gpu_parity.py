@@ -314,3 +314,30 @@ def test_grouped_qkv_shared_x_and_mlp(cts):
         plan.apply_group([0, 0], [x_attn] * 2, ys[:2], 1.0)
     with pytest.raises(cts.CtsError):                                      # y aliases another y
         plan.apply_group([1, 2], [x_attn] * 2, [ys[1], ys[1]], 1.0)
+
+
+def test_launch_count_and_split_path_agree(cts):
+    """cts_launch_count: segment = 1 launch, apply_group = 1 (fused), shrink/expand = 1 each; the
+    split path (shrink_group + expand_group) gives the same bits as the fused apply_group."""
+    N, C, r, T = 64, 5, 16, 300
+    shapes = [(512, 256), (512, 128)]
+    banks = [quantized_bank(di, do, N, C, r, seed=700 + m, cluster_of=cluster_map(N, C, 710 + m))[0]
+             for m, (di, do) in enumerate(shapes)]
+    bank = make_bank(cts, banks)
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, N, 41, frac_none=0.05)
+    x = dev_bf16(bf16_round(activations(T, 512, 42)))
+    ya = [torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes]
+    yb = [torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes]
+    n0 = cts.cts_launch_count()
+    plan.segment(torch.from_numpy(ta).cuda())
+    n1 = cts.cts_launch_count()
+    plan.apply_group([0, 1], [x, x], ya, 2.0)
+    n2 = cts.cts_launch_count()
+    plan.shrink_group([0, 1], [x, x], 2.0)
+    plan.expand_group([0, 1], yb)
+    n3 = cts.cts_launch_count()
+    torch.cuda.synchronize()
+    assert (n1 - n0, n2 - n1, n3 - n2) == (1, 1, 2)
+    for a, b in zip(ya, yb):
+        assert torch.equal(a, b)
