@@ -5,7 +5,7 @@ One step = one pass of the whole hot path over one synthetic batch: cts_segment 
 maps in one launch) + cts_apply for the 224 Mistral-7B projections (32 layers x q,k,v,o,gate,up,
 down), each apply = shrink+Sigma kernel + expand+residual kernel, replayed as one CUDA graph.
 
-  python bench.py [--config decode|prefill|q_proj|multi] [--gpus N --steps K --warmup W]
+  python bench.py [--config decode|prefill|q_proj|multi|tp_decode] [--gpus N --steps K --warmup W]
   python bench.py --impl reference ...     # the fp64 CPU oracle as the reference arm
 Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N: data-parallel request sharding, each rank
 holds a replicated bank and its own token stream (seed 1+rank); weak scaling; no collective on the
@@ -37,6 +37,10 @@ CONFIGS = {
     "q_proj": dict(workload="cfg2_q_proj", N=64, C=1, r=64, T=256, prefill=False, layers=1,
                    modules=(("q", 4096, 4096),), steps=2000, warmup=20),
     # configs[4], per GPU: 8192 adapters in 128 clusters, replicated bank
+    # configs[4] TP variant: the same bank split along d_model over the ranks (TP=N), every rank
+    # processes the same T tokens, one all-reduce of the rank-r partial per module (strong scaling)
+    "tp_decode": dict(workload="cfg5_tp_decode", N=8192, C=128, r=16, T=1024, prefill=False, tp=True,
+                      layers=MISTRAL_LAYERS, modules=MISTRAL_MODULES, steps=50, warmup=5),
     "multi": dict(workload="cfg5_multi_decode", N=8192, C=128, r=16, T=1024, prefill=False,
                   layers=MISTRAL_LAYERS, modules=MISTRAL_MODULES, steps=200, warmup=10),
 }
@@ -254,6 +258,115 @@ def config_dict(cfg, world):
             "cluster_maps": "per module", "parallelism": f"dp{world} (replicated bank, request sharding)",
             "l2": "inputs larger than L2: every module reads its own x/y/bases (>= 10 GB per step vs 126 MB L2)",
             "timing": "one CUDA graph per step (segment + all applies), CUDA events, max over ranks"}
+
+
+# ----------------------------------------------------------------------------- GPU leg, TP d-split
+def run_tp(args, cfg):
+    """TP=world d-split: rank g holds d_in/d_out slice g of every basis, all ranks
+    process the same batch; per module one NCCL all-reduce of the fp32 rank-r partial (T x r_pad).
+    One step = segment + 224 x (shrink partial, all-reduce, split + expand), replayed as a CUDA graph
+    when capture succeeds (eager otherwise).  value = T / max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_00066_b200 as cts
+    from paper_2407_00066_b200.tp import TensorParallelApply, shard_bank, shard_cols
+    from workloads.gen_torch import direct_bank_torch, tokens_torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    T, N, C, r = cfg["T"], cfg["N"], cfg["C"], cfg["r"]
+    mods = module_list(cfg)
+    ins, outs, sigs, maps = [], [], [], []
+    for m, (_, _, di, do) in enumerate(mods):
+        b = direct_bank_torch(di, do, N, C, r, seed=m % len(cfg["modules"]) + 1000 * (m // len(cfg["modules"])),
+                              device=dev, cluster_seed=50 + m)
+        si, so = shard_bank([b["in_basis"]], [b["out_basis"]], rank, world)
+        ins += si
+        outs += so
+        sigs.append(b["sigma"])
+        maps.append(b["cluster_of"])
+        del b
+    bank = cts.Bank(ins, outs, sigs, maps)
+    del ins, outs, sigs
+    torch.cuda.empty_cache()
+    tokens = tokens_torch(T, N, 1, cfg["prefill"], dev)          # the same batch on every rank
+    g = torch.Generator(device=dev).manual_seed(2)
+    xbuf, xs, ys = {}, [], []
+    for (layer, name, di, do) in mods:
+        key = (layer, x_slot(name))
+        if key not in xbuf:
+            xbuf[key] = torch.randn(T, di, generator=g, device=dev).to(torch.bfloat16)
+        xs.append(shard_cols(xbuf[key], rank, world))
+        ys.append(shard_cols(torch.randn(T, do, generator=g, device=dev).to(torch.bfloat16), rank, world))
+    plan = cts.Plan(bank, T)
+    tp = TensorParallelApply(plan)
+    groups = []
+    for layer in range(cfg["layers"]):
+        by_slot = {}
+        for m, (l, name, di, do) in enumerate(mods):
+            if l == layer:
+                by_slot.setdefault(x_slot(name), []).append(m)
+        groups += [by_slot[s] for s in ("attn", "o", "mlp", "down") if s in by_slot]
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        plan.segment(tokens)
+        for gm in groups:
+            tp.apply_group(gm, [xs[m] for m in gm], [ys[m] for m in gm], SCALE)
+
+    with torch.cuda.stream(stream):
+        step()
+        torch.cuda.synchronize()
+        graph, n0 = None, cts.cts_launch_count()
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                step()
+        except Exception as e:                                     # NCCL capture unsupported: eager
+            print(f"graph capture failed ({e}); timing eager steps", file=sys.stderr)
+            graph = None
+        launches = cts.cts_launch_count() - n0
+        run = graph.replay if graph is not None else step
+        for _ in range(args.warmup):
+            run()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clocks:
+            e0.record(stream)
+            for _ in range(args.steps):
+                run()
+            e1.record(stream)
+            e1.synchronize()
+        torch.cuda.synchronize()
+        dist.barrier()
+    per_step = e0.elapsed_time(e1) / args.steps
+    per_step = reduce_max([per_step], dist, dev)[0]
+    rp = plan.partial_elems() // T
+    line = {
+        "metric": METRIC, "value": T / (per_step / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded direct banks + Gaussian activations)",
+        "config": dict(config_dict(cfg, world), parallelism=f"tp{world} (d_model split, NCCL all-reduce of the "
+                       f"rank-{r} partial, {T * rp * 4} B per module)"),
+        "gpu_launches": args.steps * launches, "launches_per_step": launches, "graph": graph is not None,
+        "clocks": clocks.result(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
+    plan.close()
+    bank.close()
+    return 0
 
 
 # ----------------------------------------------------------------------------- GPU leg
@@ -504,6 +617,8 @@ def main():
     args.warmup = max(args.warmup, 3) if args.impl == "cts" else args.warmup
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if cfg.get("tp"):
+        return run_tp(args, cfg)
     return run_gpu(args, cfg)
 
 

@@ -156,6 +156,33 @@ cts_status_t cts_shrink_group(cts_plan_t plan, int32_t n, const int32_t* modules
 cts_status_t cts_expand_group(cts_plan_t plan, int32_t n, const int32_t* modules, void* const* ys,
                               const int64_t* ld_y, cudaStream_t stream);
 
+/*
+ * Tensor-parallel d-split (north_star: "an optional tensor-parallel split along
+ * d_model whose rank-r intermediate is all-reduced with NCCL over NVLink").  With G ranks, rank g
+ * loads a bank whose in_basis holds columns [g*d_in/G, (g+1)*d_in/G) of every V_c and whose
+ * out_basis holds rows [g*d_out/G, (g+1)*d_out/G) of every U_c; Sigma and the maps are replicated
+ * and every rank segments the SAME token batch.  Because Sigma_i is linear,
+ *     t = scale * Sigma_i V_c^T x = sum_g scale * Sigma_i V_c[g]^T x[g]          (Eq. 1)
+ * so each rank computes its partial t_g, the caller sums the partials over ranks (all-reduce), and
+ * each rank adds U_c[g] t to its d_out slice of y.
+ *
+ * cts_plan_partial_elems: *elems = fp32 elements of one module's partial buffer, T_max * r_pad:
+ *   row t (r_pad floats, zero-padded rank) is token t's partial; rows of unbound tokens and rows
+ *   t >= T are neither written nor read, so only the first T * r_pad floats need the all-reduce.
+ * cts_shrink_partial_group: like cts_shrink_group (x = this rank's d_in slice, ld_x its row stride)
+ *   but writes t_g as fp32 into parts[i] (device, caller-owned, 16-byte aligned, >= elems floats).
+ * cts_expand_reduced_group: parts[i] = the summed partials (same layout); splits them into the
+ *   bf16 hi+lo pair of R12 (one launch for the group) and runs the expand + residual add on this
+ *   rank's d_out slice of y (one launch).
+ * Errors as cts_shrink_group / cts_expand_group; CTS_ERR_INVALID_ARGUMENT for a null or misaligned
+ * part.  Every rank must pass the same modules in the same order.
+ */
+cts_status_t cts_plan_partial_elems(cts_plan_t plan, int64_t* elems);
+cts_status_t cts_shrink_partial_group(cts_plan_t plan, int32_t n, const int32_t* modules, const void* const* xs,
+                                      const int64_t* ld_x, float scale, float* const* parts, cudaStream_t stream);
+cts_status_t cts_expand_reduced_group(cts_plan_t plan, int32_t n, const int32_t* modules, const float* const* parts,
+                                      void* const* ys, const int64_t* ld_y, cudaStream_t stream);
+
 /* Read the plan's device error word (call after synchronizing the stream that ran cts_segment).
  * *code = CTS_OK or CTS_ERR_INDEX_OUT_OF_RANGE; *first_bad_token = smallest offending t or -1. */
 cts_status_t cts_plan_error(cts_plan_t plan, int32_t* code, int32_t* first_bad_token);
@@ -167,6 +194,7 @@ const char* cts_status_string(cts_status_t status);
  * plans; launches recorded into a CUDA graph under stream capture count once, at capture).  The
  * difference across a call sequence is that sequence's kernel count: cts_segment = 1,
  * cts_apply / cts_apply_group = 1 (fused kernel; 2 with CTS_FUSED=0), cts_shrink* = cts_expand* = 1,
+ * cts_expand_reduced_group = 2,
  * cts_bank_load = 3 per module.  Never fails. */
 uint64_t cts_launch_count(void);
 

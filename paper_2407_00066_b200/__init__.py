@@ -18,6 +18,9 @@ from .api import (  # noqa: F401
     cts_plan_create,
     cts_plan_error,
     cts_plan_free,
+    cts_plan_partial_elems,
+    cts_shrink_partial_group,
+    cts_expand_reduced_group,
     cts_plan_max_tiles,
     cts_segment,
     cts_segment_readback,

@@ -25,7 +25,7 @@ EXPORTS = (
     "cts_plan_create", "cts_plan_free", "cts_plan_max_tiles",
     "cts_segment", "cts_segment_readback", "cts_apply", "cts_shrink", "cts_expand",
     "cts_apply_group", "cts_shrink_group", "cts_expand_group", "cts_plan_error", "cts_status_string",
-    "cts_launch_count",
+    "cts_launch_count", "cts_plan_partial_elems", "cts_shrink_partial_group", "cts_expand_reduced_group",
 )
 
 
@@ -89,6 +89,9 @@ def lib():
         "cts_plan_error": ([P, ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
         "cts_status_string": ([I32], ctypes.c_char_p),
         "cts_launch_count": ([], ctypes.c_uint64),
+        "cts_plan_partial_elems": ([P, ctypes.POINTER(I64)], I32),
+        "cts_shrink_partial_group": ([P, I32, VP, VP, VP, F, VP, P], I32),
+        "cts_expand_reduced_group": ([P, I32, VP, VP, VP, VP, P], I32),
     }
     for name, (argt, rest) in sig.items():
         f = getattr(L, name)

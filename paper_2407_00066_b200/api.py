@@ -174,6 +174,37 @@ def cts_plan_error(plan):
     return code.value, bad.value
 
 
+def _part_args(parts, n):
+    if len(parts) != n:
+        raise ValueError("need one partial buffer per module")
+    for t in parts:
+        if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+            raise TypeError("partials must be contiguous fp32 CUDA tensors")
+    return (ctypes.c_void_p * n)(*[t.data_ptr() for t in parts])
+
+
+def cts_plan_partial_elems(plan):
+    e = ctypes.c_int64()
+    check("cts_plan_partial_elems", lib().cts_plan_partial_elems(plan, ctypes.byref(e)))
+    return e.value
+
+
+def cts_shrink_partial_group(plan, modules, xs, parts, scale=1.0, stream=None):
+    """TP rank-local shrink: parts[i] <- this rank's fp32 partial t of module i (sum over ranks next)."""
+    n, mods, xp, xl = _group_args(modules, xs, "x")
+    pp = _part_args(parts, n)
+    check("cts_shrink_partial_group", lib().cts_shrink_partial_group(plan, n, mods, xp, xl, ctypes.c_float(scale), pp,
+                                                                     _stream_handle(stream)))
+
+
+def cts_expand_reduced_group(plan, modules, parts, ys, stream=None):
+    """TP rank-local expand of the all-reduced partials into this rank's d_out slice of y."""
+    n, mods, yp, yl = _group_args(modules, ys, "y")
+    pp = _part_args(parts, n)
+    check("cts_expand_reduced_group", lib().cts_expand_reduced_group(plan, n, mods, pp, yp, yl,
+                                                                     _stream_handle(stream)))
+
+
 def cts_launch_count():
     """Kernels libcts has enqueued since load (graph captures count once, at capture)."""
     return int(lib().cts_launch_count())
@@ -243,6 +274,21 @@ class Plan:
 
     def expand_group(self, modules, ys, stream=None):
         cts_expand_group(self.handle, modules, ys, stream)
+
+    def partial_elems(self):
+        return cts_plan_partial_elems(self.handle)
+
+    def new_partials(self, n):
+        """n zeroed fp32 partial buffers for the TP entry points (one per module of a group)."""
+        e = self.partial_elems()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        return [torch.zeros(e, dtype=torch.float32, device=dev) for _ in range(n)]
+
+    def shrink_partial_group(self, modules, xs, parts, scale=1.0, stream=None):
+        cts_shrink_partial_group(self.handle, modules, xs, parts, scale, stream)
+
+    def expand_reduced_group(self, modules, parts, ys, stream=None):
+        cts_expand_reduced_group(self.handle, modules, parts, ys, stream)
 
     def error(self):
         return cts_plan_error(self.handle)

@@ -264,7 +264,7 @@ int choose_ks(int tiles_total, int min_kblocks) {
 int next_meta_ready(cts_plan_t p) { return p->launches_since_segment++ > 0 ? 1 : 0; }
 
 cts_status_t fill_shrink(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
-                         float scale, bool fused, ShrinkParams& prm, int& items) {
+                         float scale, bool fused, ShrinkParams& prm, int& items, float* const* parts = nullptr) {
   const cts_bank_t b = p->bank;
   const int T = p->T;
   const int tiles_bound = cts_plan_max_tiles(p, T);
@@ -289,6 +289,7 @@ cts_status_t fill_shrink(cts_plan_t p, int n, const int32_t* modules, const void
     sm.tile_adapters = p->tile_adapters + mid * p->max_tiles * kTileM;
     sm.sigma = m.sigma;
     sm.tbuf = module_tbuf(p, modules[i]);
+    sm.tpart = parts ? parts[i] : nullptr;
     sm.ws = p->ws + size_t(i) * p->ws_cap_rows * b->rp;
     sm.counters = p->counters + size_t(i) * p->max_tiles;
     sm.ready = fused ? p->ready + size_t(i) * p->max_tiles : nullptr;
@@ -334,12 +335,12 @@ cts_status_t fill_expand(cts_plan_t p, int n, const int32_t* modules, void* cons
 
 template <int RP>
 cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
-                           float scale, cudaStream_t stream) {
+                           float scale, cudaStream_t stream, float* const* parts = nullptr) {
   static const cudaError_t attr = set_smem(shrink_sigma_kernel<RP>, ShrinkKernelSmem<RP>::kBytes);
   CTS_CUDA(attr);
   ShrinkParams prm;
   int items = 0;
-  cts_status_t st = fill_shrink(p, n, modules, xs, ld_x, scale, false, prm, items);
+  cts_status_t st = fill_shrink(p, n, modules, xs, ld_x, scale, false, prm, items, parts);
   if (st != CTS_OK) return st;
   prm.meta_ready = next_meta_ready(p);
   CTS_CUDA(launch_pdl(shrink_sigma_kernel<RP>, std::min(sm_count(), items), kApplyThreads,
@@ -397,12 +398,37 @@ cts_status_t check_group(cts_plan_t p, int32_t n, const int32_t* modules, const 
 }
 
 cts_status_t do_shrink(cts_plan_t p, int n, const int32_t* mods, const void* const* xs, const int64_t* ld, float scale,
-                       cudaStream_t s) {
+                       cudaStream_t s, float* const* parts = nullptr) {
   switch (p->bank->rp) {
-    case 16: return launch_shrink<16>(p, n, mods, xs, ld, scale, s);
-    case 32: return launch_shrink<32>(p, n, mods, xs, ld, scale, s);
-    default: return launch_shrink<64>(p, n, mods, xs, ld, scale, s);
+    case 16: return launch_shrink<16>(p, n, mods, xs, ld, scale, s, parts);
+    case 32: return launch_shrink<32>(p, n, mods, xs, ld, scale, s, parts);
+    default: return launch_shrink<64>(p, n, mods, xs, ld, scale, s, parts);
   }
+}
+
+cts_status_t do_split(cts_plan_t p, int n, const int32_t* mods, const float* const* parts, cudaStream_t s) {
+  SplitArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n_mod = n;
+  a.rp = p->bank->rp;
+  for (int i = 0; i < n; ++i) {
+    a.part[i] = parts[i];
+    a.tbuf[i] = module_tbuf(p, mods[i]);
+    const size_t mid = p->bank->mods[mods[i]].map_id;
+    a.n_tiles[i] = p->n_tiles + mid;
+    a.tile_rows[i] = p->tile_rows + mid * p->max_tiles * kTileM;
+  }
+  (void)next_meta_ready(p);   // one more launch separating the plan's segment from later kernels
+  CTS_CUDA(launch_pdl(t_split_kernel, sm_count(), 256, 0, s, a));
+  return CTS_OK;
+}
+
+bool check_parts(cts_plan_t p, int n, const void* const* parts) {
+  if (!parts) return false;
+  for (int i = 0; i < n; ++i)
+    if (!parts[i] || !aligned16(parts[i])) return false;
+  (void)p;
+  return true;
 }
 
 cts_status_t do_expand(cts_plan_t p, int n, const int32_t* mods, void* const* ys, const int64_t* ld, cudaStream_t s) {
@@ -759,6 +785,31 @@ cts_status_t cts_apply_group(cts_plan_t p, int32_t n, const int32_t* modules, co
   }
   if (use_fused()) return do_fused(p, n, modules, xs, ld_x, ys, ld_y, scale, stream);
   if ((st = do_shrink(p, n, modules, xs, ld_x, scale, stream)) != CTS_OK) return st;
+  return do_expand(p, n, modules, ys, ld_y, stream);
+}
+
+cts_status_t cts_plan_partial_elems(cts_plan_t p, int64_t* elems) {
+  if (!p || !elems) return CTS_ERR_INVALID_ARGUMENT;
+  *elems = int64_t(p->T_max) * p->bank->rp;
+  return CTS_OK;
+}
+
+cts_status_t cts_shrink_partial_group(cts_plan_t p, int32_t n, const int32_t* modules, const void* const* xs,
+                                      const int64_t* ld_x, float scale, float* const* parts, cudaStream_t stream) {
+  cts_status_t st = check_group(p, n, modules, xs, ld_x, true);
+  if (st != CTS_OK) return st;
+  if (!check_parts(p, n, reinterpret_cast<const void* const*>(parts))) return CTS_ERR_INVALID_ARGUMENT;
+  if (p->T == 0) return CTS_OK;
+  return do_shrink(p, n, modules, xs, ld_x, scale, stream, parts);
+}
+
+cts_status_t cts_expand_reduced_group(cts_plan_t p, int32_t n, const int32_t* modules, const float* const* parts,
+                                      void* const* ys, const int64_t* ld_y, cudaStream_t stream) {
+  cts_status_t st = check_group(p, n, modules, ys, ld_y, false);
+  if (st != CTS_OK) return st;
+  if (!check_parts(p, n, reinterpret_cast<const void* const*>(parts))) return CTS_ERR_INVALID_ARGUMENT;
+  if (p->T == 0) return CTS_OK;
+  if ((st = do_split(p, n, modules, parts, stream)) != CTS_OK) return st;
   return do_expand(p, n, modules, ys, ld_y, stream);
 }
 

@@ -318,6 +318,34 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
   if (!DIRECT) bulk_wait0();                    // this warp's global writes complete before exit
 }
 
+// ------------------------------------------------------------------ TP: reduced fp32 t -> hi | lo
+// After the caller's all-reduce of the per-rank partials (cts_expand_reduced_group): gather each
+// slot row's token from the token-ordered fp32 t and split it into the bf16 hi + lo pair the
+// expand MMA consumes (same split as the shrink epilogue).
+struct SplitArgs {
+  const float* part[kMaxGroup];          // [T][rp] token order
+  __nv_bfloat16* tbuf[kMaxGroup];        // [slot*128 + row][2*rp]
+  const int32_t* n_tiles[kMaxGroup];
+  const int32_t* tile_rows[kMaxGroup];
+  int n_mod, rp;
+};
+
+__global__ void __launch_bounds__(256) t_split_kernel(const __grid_constant__ SplitArgs a) {
+  griddep_wait();
+  if (threadIdx.x == 0) griddep_launch_dependents();
+  for (int g = 0; g < a.n_mod; ++g) {
+    const size_t n = static_cast<size_t>(*a.n_tiles[g]) * kTileM * a.rp;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+      const size_t row = i / a.rp;
+      const int c = static_cast<int>(i % a.rp);
+      const float v = a.part[g][static_cast<size_t>(a.tile_rows[g][row]) * a.rp + c];
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      a.tbuf[g][row * 2 * a.rp + c] = hi;
+      a.tbuf[g][row * 2 * a.rp + a.rp + c] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    }
+  }
+}
+
 // ------------------------------------------------------------------ standalone kernel
 template <int RP>
 struct ExpandKernelSmem {

@@ -63,6 +63,7 @@ struct alignas(64) ShrinkMod {
   const int32_t* tile_adapters;         // [slot*128 + row] adapter id
   const __nv_bfloat16* sigma;           // [N][rp][rp], row = out index
   __nv_bfloat16* tbuf;                  // [max_tiles*128][2*rp]  (hi | lo)
+  float* tpart;                         // TP partial mode: fp32 t in TOKEN order [T][rp] instead of tbuf
   float* ws;                            // [ks][ws_rows][rp] split-K partials
   int32_t* counters;                    // [max_tiles] arrivals per slot (self-resetting)
   int32_t* ready;                       // [max_tiles] "t ready" flags (fused kernel only; else null)
@@ -374,6 +375,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int 
     if (finisher && rvalid) {
       // t = scale * Sigma_i s ; thread = token row
       const uint4* srow = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
+      const int tok = m.tpart != nullptr ? m.tile_rows[tile * kTileM + row] : 0;
       __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP);
 #pragma unroll 1
       for (int o0 = 0; o0 < RP; o0 += 8) {
@@ -394,6 +396,13 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int 
             }
           }
           t8[oo] = acc * m.scale;
+        }
+        if (m.tpart != nullptr) {                   // TP: this rank's fp32 partial, summed over ranks later
+          // rows past a tile's length repeat its last token with identical values: benign rewrites
+          float4* dp = reinterpret_cast<float4*>(m.tpart + static_cast<size_t>(tok) * RP + o0);
+          dp[0] = make_float4(t8[0], t8[1], t8[2], t8[3]);
+          dp[1] = make_float4(t8[4], t8[5], t8[6], t8[7]);
+          continue;
         }
         uint4 hi, lo;
         __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&hi);

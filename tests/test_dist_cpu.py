@@ -48,3 +48,78 @@ def test_two_rank_sharding_and_timing():
     assert g0[0] != g0[1]                                                # ranks draw different requests
     assert m0 == m1 == [3.0, 20.0]                                       # max over ranks on every rank
     assert v0 == v1 == pytest.approx(1024 * 2 / 3e-3)                    # all units / slowest rank time
+
+
+# ---------------------------------------------------------------- TP d-split orchestration (gloo)
+def _tp_worker(rank, world, port, q):
+    """Each rank runs paper_2407_00066_b200.tp's sharding + call order with the oracle standing in
+    for the two kernels (shrink partial = apply_ref with an identity out_basis; expand = apply_ref
+    with identity in_basis and Sigma) and gloo for the all-reduce; rank 0 checks the gathered
+    y slices against the unsharded oracle apply."""
+    import numpy as np
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import apply_ref
+    from paper_2407_00066_b200.tp import shard_bank, shard_bounds, shard_cols, tp_apply_group
+    from workloads import cluster_map, decode_tokens
+
+    rng = np.random.default_rng(5)
+    T, N, C, r, d_in, d_out = 40, 12, 3, 4, 256, 128
+    in_b = torch.from_numpy(rng.standard_normal((C, d_in, r)))
+    out_b = torch.from_numpy(rng.standard_normal((C, d_out, r)))
+    sig = rng.standard_normal((N, r, r))
+    cmap = cluster_map(N, C, 7)
+    ta = decode_tokens(T, N, 8, frac_none=0.1)
+    x = torch.from_numpy(rng.standard_normal((T, d_in)))
+    y0 = torch.from_numpy(rng.standard_normal((T, d_out)))
+    ins, outs = shard_bank([in_b], [out_b], rank, world)
+    eye_out = np.broadcast_to(np.eye(r), (C, r, r))
+    eye_sig = np.broadcast_to(np.eye(r), (N, r, r))
+
+    def shrink_partial(mods, xs, parts, scale):
+        for p, xg, ig in zip(parts, xs, ins):
+            t, _ = apply_ref(xg.numpy(), ta, cmap, ig.numpy(), eye_out, sig, scale)
+            p.copy_(torch.from_numpy(t).reshape(-1))
+
+    def expand_reduced(mods, parts, ys):
+        for p, yg, og in zip(parts, ys, outs):
+            dy, _ = apply_ref(p.reshape(T, r).numpy(), ta, cmap, eye_out, og.numpy(), eye_sig, 1.0)
+            yg += torch.from_numpy(dy)
+
+    parts = [torch.zeros(T * r, dtype=torch.float64)]
+    y_shard = shard_cols(y0, rank, world).clone()
+    tp_apply_group([0], [shard_cols(x, rank, world)], [y_shard], parts, T * r, 2.0,
+                   shrink_partial, dist.all_reduce, expand_reduced)
+    gathered = [torch.zeros_like(y_shard) for _ in range(world)]
+    dist.all_gather(gathered, y_shard)
+    if rank == 0:
+        dy, _ = apply_ref(x.numpy(), ta, cmap, in_b.numpy(), out_b.numpy(), sig, 2.0)
+        y_tp = torch.cat(gathered, dim=1).numpy()
+        q.put(("err", float(np.max(np.abs(y_tp - (y0.numpy() + dy)))), shard_bounds(d_out, 1, world)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_tensor_parallel_dsplit():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    tag, err, b1 = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert tag == "err" and err < 1e-10
+    assert b1 == (64, 128)
+
+
+def test_shard_bounds_validation():
+    from paper_2407_00066_b200.tp import shard_bounds
+    assert shard_bounds(4096, 7, 8) == (3584, 4096)
+    assert shard_bounds(14336, 0, 8) == (0, 1792)
+    with pytest.raises(ValueError):
+        shard_bounds(1024, 0, 32)           # 32-column slices: not a multiple of 64
+    with pytest.raises(ValueError):
+        shard_bounds(4096, 8, 8)

@@ -341,3 +341,46 @@ def test_launch_count_and_split_path_agree(cts):
     assert (n1 - n0, n2 - n1, n3 - n2) == (1, 1, 2)
     for a, b in zip(ya, yb):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_tensor_parallel_dsplit(cts, G):
+    """TP d-split through the ABI, G shards simulated in one process: each shard's bank holds its
+    d_in / d_out slices, cts_shrink_partial_group writes its fp32 partial, the partials are summed
+    (the all-reduce), cts_expand_reduced_group adds each shard's slice of y.  The assembled y must
+    meet the per-row 5e-3 bound against the unsharded fp64 oracle."""
+    from paper_2407_00066_b200.tp import shard_bank, shard_cols
+    N, C, r, T = 120, 5, 16, 333
+    shapes = [(512, 256), (512, 1024)]
+    banks, f64s = [], []
+    for m, (di, do) in enumerate(shapes):
+        b, f = quantized_bank(di, do, N, C, r, seed=900 + m, cluster_of=cluster_map(N, C, 910 + m))
+        banks.append(b)
+        f64s.append(f)
+    ins = [dev_bf16(b["in_basis"]) for b in banks]
+    outs = [dev_bf16(b["out_basis"]) for b in banks]
+    sig = [dev_bf16(b["sigma"]) for b in banks]
+    cmaps = [torch.from_numpy(b["cluster_of"]).cuda() for b in banks]
+    ta = decode_tokens(T, N, 51, frac_none=0.05)
+    tok = torch.from_numpy(ta).cuda()
+    xb = bf16_round(activations(T, 512, 52))
+    x = dev_bf16(xb)
+    ys = [torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes]
+    shards = []
+    for g in range(G):
+        si, so = shard_bank(ins, outs, g, G)
+        bank = cts.Bank(si, so, sig, cmaps)
+        plan = cts.Plan(bank, T)
+        plan.segment(tok)
+        shards.append((bank, plan, plan.new_partials(2)))
+    for g, (_, plan, parts) in enumerate(shards):
+        xg = shard_cols(x, g, G)
+        plan.shrink_partial_group([0, 1], [xg, xg], parts, 2.0)
+    total = [sum(s[2][i] for s in shards) for i in range(2)]     # stands in for the all-reduce
+    for g, (_, plan, _) in enumerate(shards):
+        n0 = cts.cts_launch_count()
+        plan.expand_reduced_group([0, 1], total, [shard_cols(y, g, G) for y in ys])
+        assert cts.cts_launch_count() - n0 == 2
+    torch.cuda.synchronize()
+    for m in range(2):
+        check_delta(ta, host_bits(ys[m]), f64s[m], xb, 2.0)
