@@ -41,7 +41,7 @@ struct FusedSmem {
   static_assert(ShrinkCfg<RP>::kTmemCols <= kTmemCols && ExpandCfg<RP>::kTmemCols <= kTmemCols, "TMEM");
 };
 
-template <int RP, bool DIRECT>
+template <int RP, int STORE>
 __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __grid_constant__ FusedParams p) {
   using S = FusedSmem<RP>;
   extern __shared__ uint8_t smem_raw[];
@@ -55,12 +55,19 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     CTS_STAMP(0);
-    shrink_init_barriers<RP>(RS, p.s.x_cpasync);
+    shrink_init_barriers<RP>(RS);
     expand_init_barriers<RP>(RE);
     mbar_init(arena_free, 1);
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<S::kTmemCols>(tmem_slot);
+  if (warp == 0 && lane < p.s.n_mod) {   // descriptors never depend on the previous kernel
+    tma_prefetch_desc(&p.s.mod[lane].tm_x);
+    tma_prefetch_desc(p.s.mod[lane].tm_in);
+    tma_prefetch_desc(&p.e.mod[lane].tm_y);
+    tma_prefetch_desc(p.e.mod[lane].tm_t);
+    tma_prefetch_desc(p.e.mod[lane].tm_out);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
     shrink_epilogue<RP>(p.s, RS, nt_lane, warp, lane);
     if (threadIdx.x == 32 * kEpiWarp0) CTS_STAMP(5);        // epilogue set 0 done
     if (threadIdx.x == 32 * (kEpiWarp0 + 4)) CTS_STAMP(6);  // epilogue set 1 done
-    expand_epilogue<RP, DIRECT>(p.e, RE, nt_lane, warp, lane);
+    expand_epilogue<RP, STORE>(p.e, RE, nt_lane, warp, lane);
   }
 
   // ---------------------------------------------------------------- exit: last CTA clears flags
@@ -113,11 +120,8 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   if (threadIdx.x == 0) *s_last_exit = atomicAdd(p.exit_count, 1) == static_cast<int>(gridDim.x) - 1;
   __syncthreads();
   if (*s_last_exit) {
-    for (int g = 0; g < p.s.n_mod; ++g) {
-      const ShrinkMod& m = p.s.mod[g];
-      const int slots = (p.s.prefix[g + 1] - p.s.prefix[g]) / m.ks;
-      for (int i = threadIdx.x; i < slots; i += blockDim.x) m.ready[i] = 0;
-    }
+    for (int g = 0; g < p.s.n_mod; ++g)
+      for (int i = threadIdx.x; i < p.s.tiles_bound; i += blockDim.x) p.s.mod[g].ready[i] = 0;
     if (threadIdx.x == 0) *p.exit_count = 0;
   }
   if (warp == kMmaWarp) tmem_dealloc<S::kTmemCols>(RS.tmem);

@@ -170,7 +170,7 @@ constexpr int kTargetItemsPerSMMax = 4;   // sizes the split-K workspace
 int target_items_per_sm() {
   static int v = [] {
     const char* e = std::getenv("CTS_ITEMS_PER_SM");
-    return e ? std::max(1, std::min(kTargetItemsPerSMMax, std::atoi(e))) : 2;
+    return e ? std::max(1, std::min(kTargetItemsPerSMMax, std::atoi(e))) : 1;
   }();
   return v;
 }
@@ -180,18 +180,19 @@ cudaError_t set_smem(Kern kernel, int bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-// expand store path: register-direct st.global when tiles are small (latency-bound, decode: the
-// stage is freed without waiting for a TMA scatter to read it), TMA scatter when tiles are full
-// (bandwidth-bound, prefill: st.global from a thread-per-row layout tops out lower).  Measured on
-// B200: decode expand 21.5 -> 19.5 us per launch direct; prefill 150 us scatter vs 183 us direct.
-// CTS_EXPAND_STORE = 0 / 1 forces scatter / direct (tuning aid).
-bool expand_direct_store(int T, int C) {
+// expand store path (expand.cuh STORE modes): register-direct stores when tiles are small
+// (latency-bound decode: the stage is freed right after the y_base reads), TMA scatter when tiles
+// are full (bandwidth-bound prefill).  Measured on B200 (expand us per launch, decode / prefill):
+// scatter 21.4 / 150.7, direct 19.4 / 179.1, coalesced row copies out of the stage 23.7 / 160.9
+// (the extra shared-memory round trip costs more than the 8x fewer store wavefronts save).
+// CTS_EXPAND_STORE = 0 / 1 / 2 forces scatter / direct / coalesced (tuning aid).
+int expand_store_mode(int T, int C) {
   static int v = [] {
     const char* e = std::getenv("CTS_EXPAND_STORE");
     return e ? std::atoi(e) : -1;
   }();
-  if (v >= 0) return v != 0;
-  return T < 96 * C;   // mean tokens per cluster < 96
+  if (v >= 0 && v <= 2) return v;
+  return T < 96 * C ? kStoreDirect : kStoreScatter;   // mean tokens per cluster < 96
 }
 
 // fused kernel, expand producer: poll the slot's t-ready flag before (1) or after (0) issuing the
@@ -203,17 +204,6 @@ int poll_first_default(int T, int C) {
   }();
   if (v >= 0) return v != 0;
   return T < 96 * C ? 0 : 1;
-}
-
-// shrink x rows: per-thread cp.async (1) or TMA tile::gather4 (0).  Measured on B200 (fused step):
-// gather4 235k / 584k tok/s (decode / prefill) vs cp.async 197k / 554k, so gather4 is the default;
-// CTS_X_CPASYNC=1 selects cp.async (tuning aid; both paths pass the parity suite).
-int x_cpasync_default() {
-  static int v = [] {
-    const char* e = std::getenv("CTS_X_CPASYNC");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v != 0;
 }
 
 // cts_apply[_group] runs the fused single-launch kernel unless CTS_FUSED=0 (tuning aid).
@@ -250,13 +240,11 @@ __nv_bfloat16* module_tbuf(cts_plan_t p, int module) {
   return p->tbuf + size_t(module) * p->max_tiles * kTileM * 2 * p->bank->rp;
 }
 
-// K chunks per tile for a group: aim for ~target_items_per_sm() items per SM over the tile BOUND,
-// each >= 4 K blocks.  (Sizing by the expected packed slot count instead -- more, shorter items --
-// measured slower at decode: 219k -> 189k tok/s, the extra split-K finisher chains end later.)
-int choose_ks(int tiles_total, int min_kblocks) {
-  const int want = (target_items_per_sm() * sm_count() + tiles_total - 1) / std::max(tiles_total, 1);
-  return std::max(1, std::min({want, 16, std::max(1, min_kblocks / 4)}));
-}
+// K chunks per slot: the DEVICE sizes them from the real slot count (shrink_ks: ~target items per
+// SM over the slots the segment kernel produced); the host only caps them: each chunk >= 4 K
+// blocks, <= 16 chunks.  The workspace holds (target * SMs + slots) * 128 rows per module, which
+// bounds slots * ks for any slot count.
+int ks_cap(int min_kblocks) { return std::max(1, std::min(16, min_kblocks / 4)); }
 
 // Segment outputs may be read before griddep_wait by every kernel but the first after cts_segment:
 // each kernel triggers its dependents only after its own griddep_wait, so when launch k starts,
@@ -270,17 +258,16 @@ cts_status_t fill_shrink(cts_plan_t p, int n, const int32_t* modules, const void
   const int tiles_bound = cts_plan_max_tiles(p, T);
   int min_kb = 1 << 30;
   for (int i = 0; i < n; ++i) min_kb = std::min(min_kb, b->mods[modules[i]].d_in / kBK);
-  const int ks = choose_ks(tiles_bound * n, min_kb);
-  if (size_t(ks) * tiles_bound * kTileM > p->ws_cap_rows) return CTS_ERR_SHAPE;
+  const int ks_max = ks_cap(min_kb);
   std::memset(&prm, 0, sizeof(prm));
   prm.n_mod = n;
-  prm.prefix[0] = 0;
+  prm.tiles_bound = tiles_bound;
+  prm.ks_max = ks_max;
+  prm.target_items = target_items_per_sm();
   for (int i = 0; i < n; ++i) {
     const Module& m = b->mods[modules[i]];
     ShrinkMod& sm = prm.mod[i];
     if (!make_tmap(&sm.tm_x, xs[i], m.d_in, T, ld_x[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
-    sm.x = static_cast<const __nv_bfloat16*>(xs[i]);
-    sm.ld_x = ld_x[i];
     sm.tm_in = b->d_tm_in + modules[i];
     const size_t mid = m.map_id;
     sm.tiles = p->tiles + mid * p->max_tiles * 2;
@@ -294,13 +281,9 @@ cts_status_t fill_shrink(cts_plan_t p, int n, const int32_t* modules, const void
     sm.counters = p->counters + size_t(i) * p->max_tiles;
     sm.ready = fused ? p->ready + size_t(i) * p->max_tiles : nullptr;
     sm.kblocks = m.d_in / kBK;
-    sm.ks = ks;
-    sm.ws_rows = tiles_bound * kTileM;
     sm.scale = scale;
-    prm.prefix[i + 1] = prm.prefix[i] + tiles_bound * ks;
   }
-  prm.x_cpasync = x_cpasync_default();
-  items = prm.prefix[n];
+  items = tiles_bound * n * ks_max;                // upper bound (grid sizing)
   return CTS_OK;
 }
 
@@ -311,7 +294,7 @@ cts_status_t fill_expand(cts_plan_t p, int n, const int32_t* modules, void* cons
   const int tiles_bound = cts_plan_max_tiles(p, T);
   std::memset(&prm, 0, sizeof(prm));
   prm.n_mod = n;
-  prm.prefix[0] = 0;
+  items = 0;
   for (int i = 0; i < n; ++i) {
     const Module& m = b->mods[modules[i]];
     ExpandMod& em = prm.mod[i];
@@ -327,9 +310,8 @@ cts_status_t fill_expand(cts_plan_t p, int n, const int32_t* modules, void* cons
     em.ld_y = ld_y[i];
     em.nblk = (m.d_out + kBN - 1) / kBN;
     em.d_out = m.d_out;
-    prm.prefix[i + 1] = prm.prefix[i] + tiles_bound * em.nblk;
+    items += tiles_bound * em.nblk;               // upper bound (grid sizing)
   }
-  items = prm.prefix[n];
   return CTS_OK;
 }
 
@@ -348,25 +330,25 @@ cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const vo
   return CTS_OK;
 }
 
-template <int RP, bool DIRECT>
+template <int RP, int STORE>
 cts_status_t launch_expand(cts_plan_t p, int n, const int32_t* modules, void* const* ys, const int64_t* ld_y,
                            cudaStream_t stream) {
-  static const cudaError_t attr = set_smem(expand_kernel<RP, DIRECT>, ExpandKernelSmem<RP>::kBytes);
+  static const cudaError_t attr = set_smem(expand_kernel<RP, STORE>, ExpandKernelSmem<RP>::kBytes);
   CTS_CUDA(attr);
   ExpandParams prm;
   int items = 0;
   cts_status_t st = fill_expand(p, n, modules, ys, ld_y, false, prm, items);
   if (st != CTS_OK) return st;
   prm.meta_ready = next_meta_ready(p);
-  CTS_CUDA(launch_pdl(expand_kernel<RP, DIRECT>, std::min(sm_count(), items), kApplyThreads,
+  CTS_CUDA(launch_pdl(expand_kernel<RP, STORE>, std::min(sm_count(), items), kApplyThreads,
                       ExpandKernelSmem<RP>::kBytes, stream, prm));
   return CTS_OK;
 }
 
-template <int RP, bool DIRECT>
+template <int RP, int STORE>
 cts_status_t launch_fused(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
                           void* const* ys, const int64_t* ld_y, float scale, cudaStream_t stream) {
-  static const cudaError_t attr = set_smem(apply_fused_kernel<RP, DIRECT>, FusedSmem<RP>::kBytes);
+  static const cudaError_t attr = set_smem(apply_fused_kernel<RP, STORE>, FusedSmem<RP>::kBytes);
   CTS_CUDA(attr);
   FusedParams prm;
   int items_s = 0, items_e = 0;
@@ -376,7 +358,7 @@ cts_status_t launch_fused(cts_plan_t p, int n, const int32_t* modules, const voi
   prm.s.meta_ready = prm.e.meta_ready = next_meta_ready(p);
   prm.e.poll_first = poll_first_default(p->T, p->bank->C);
   prm.exit_count = p->exit_count;
-  CTS_CUDA(launch_pdl(apply_fused_kernel<RP, DIRECT>, std::min(sm_count(), std::max(items_s, items_e)), kApplyThreads,
+  CTS_CUDA(launch_pdl(apply_fused_kernel<RP, STORE>, std::min(sm_count(), std::max(items_s, items_e)), kApplyThreads,
                       FusedSmem<RP>::kBytes, stream, prm));
   return CTS_OK;
 }
@@ -431,29 +413,43 @@ bool check_parts(cts_plan_t p, int n, const void* const* parts) {
   return true;
 }
 
-cts_status_t do_expand(cts_plan_t p, int n, const int32_t* mods, void* const* ys, const int64_t* ld, cudaStream_t s) {
-  const bool direct = expand_direct_store(p->T, p->bank->C);
-  switch (p->bank->rp) {
-    case 16: return direct ? launch_expand<16, true>(p, n, mods, ys, ld, s)
-                           : launch_expand<16, false>(p, n, mods, ys, ld, s);
-    case 32: return direct ? launch_expand<32, true>(p, n, mods, ys, ld, s)
-                           : launch_expand<32, false>(p, n, mods, ys, ld, s);
-    default: return direct ? launch_expand<64, true>(p, n, mods, ys, ld, s)
-                           : launch_expand<64, false>(p, n, mods, ys, ld, s);
+// template dispatch over (r_pad, store mode)
+template <template <int, int> class F, typename... A>
+cts_status_t dispatch_rp_store(int rp, int store, A... a) {
+  switch (rp * 4 + store) {
+    case 16 * 4 + kStoreScatter: return F<16, kStoreScatter>::run(a...);
+    case 16 * 4 + kStoreDirect: return F<16, kStoreDirect>::run(a...);
+    case 16 * 4 + kStoreCoalesced: return F<16, kStoreCoalesced>::run(a...);
+    case 32 * 4 + kStoreScatter: return F<32, kStoreScatter>::run(a...);
+    case 32 * 4 + kStoreDirect: return F<32, kStoreDirect>::run(a...);
+    case 32 * 4 + kStoreCoalesced: return F<32, kStoreCoalesced>::run(a...);
+    case 64 * 4 + kStoreScatter: return F<64, kStoreScatter>::run(a...);
+    case 64 * 4 + kStoreDirect: return F<64, kStoreDirect>::run(a...);
+    default: return F<64, kStoreCoalesced>::run(a...);
   }
+}
+template <int RP, int STORE>
+struct ExpandLaunch {
+  static cts_status_t run(cts_plan_t p, int n, const int32_t* mods, void* const* ys, const int64_t* ld, cudaStream_t s) {
+    return launch_expand<RP, STORE>(p, n, mods, ys, ld, s);
+  }
+};
+template <int RP, int STORE>
+struct FusedLaunch {
+  static cts_status_t run(cts_plan_t p, int n, const int32_t* mods, const void* const* xs, const int64_t* ldx,
+                          void* const* ys, const int64_t* ldy, float scale, cudaStream_t s) {
+    return launch_fused<RP, STORE>(p, n, mods, xs, ldx, ys, ldy, scale, s);
+  }
+};
+
+cts_status_t do_expand(cts_plan_t p, int n, const int32_t* mods, void* const* ys, const int64_t* ld, cudaStream_t s) {
+  return dispatch_rp_store<ExpandLaunch>(p->bank->rp, expand_store_mode(p->T, p->bank->C), p, n, mods, ys, ld, s);
 }
 
 cts_status_t do_fused(cts_plan_t p, int n, const int32_t* mods, const void* const* xs, const int64_t* ldx,
                       void* const* ys, const int64_t* ldy, float scale, cudaStream_t s) {
-  const bool direct = expand_direct_store(p->T, p->bank->C);
-  switch (p->bank->rp) {
-    case 16: return direct ? launch_fused<16, true>(p, n, mods, xs, ldx, ys, ldy, scale, s)
-                           : launch_fused<16, false>(p, n, mods, xs, ldx, ys, ldy, scale, s);
-    case 32: return direct ? launch_fused<32, true>(p, n, mods, xs, ldx, ys, ldy, scale, s)
-                           : launch_fused<32, false>(p, n, mods, xs, ldx, ys, ldy, scale, s);
-    default: return direct ? launch_fused<64, true>(p, n, mods, xs, ldx, ys, ldy, scale, s)
-                           : launch_fused<64, false>(p, n, mods, xs, ldx, ys, ldy, scale, s);
-  }
+  return dispatch_rp_store<FusedLaunch>(p->bank->rp, expand_store_mode(p->T, p->bank->C), p, n, mods, xs, ldx, ys,
+                                        ldy, scale, s);
 }
 
 bool overlaps(const void* a, size_t na, const void* b, size_t nb) {

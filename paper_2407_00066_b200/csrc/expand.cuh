@@ -18,12 +18,16 @@
 //               one of kAccSlots TMEM accumulators.
 //   warps 5-12  epilogue: two sets of 4 warps take alternate items; in a set each warp owns one
 //               32-row quarter (its TMEM lanes).  Thread = token row: tcgen05.ld 64 fp32 columns at
-//               a time, add y_base from smem, round to bf16 (RNE), then either
-//                 DIRECT=false: write back into the stage; the warp TMA-scatters its 8 four-row
-//                               groups and releases the stage once the scatter has read it;
-//                 DIRECT=true:  store the row's 16-byte chunks straight from registers and release
-//                               the stage right after the y_base reads.
-//               (host picks DIRECT for small tiles / latency-bound batches, scatter for full tiles)
+//               a time, add y_base from smem, round to bf16 (RNE), then (STORE mode)
+//                 kStoreScatter:   write back into the stage; the warp TMA-scatters its 8 four-row
+//                                  groups and releases the stage once the scatter has read it;
+//                 kStoreDirect:    store the row's 16-byte chunks straight from registers (one
+//                                  16-byte piece of 32 different rows per warp store) and release
+//                                  the stage right after the y_base reads;
+//                 kStoreCoalesced: write back into the stage, then the warp copies its rows out
+//                                  with row-contiguous stores (8 lanes per 128-byte line, 4 lines
+//                                  per instruction, 8x fewer L1 store wavefronts than direct) and
+//                                  releases the stage as soon as those shared-memory reads are done.
 #pragma once
 #include "sm100.cuh"
 #include "segment.cuh"
@@ -34,6 +38,15 @@ namespace cts {
 constexpr int kExpandThreads = kApplyThreads;
 constexpr int kBN = 128;                 // d_out columns per work item
 constexpr int kExpandAccSlots = 2;       // 2 x (D0 | D1) x 128 fp32 columns = all of TMEM
+constexpr int kStoreScatter = 0, kStoreDirect = 1, kStoreCoalesced = 2;   // expand epilogue store paths
+// Epilogue work split.  kEpiSplit: BOTH epilogue sets work on every item, set s on 64-column
+// segment s (the two warps of a TMEM lane quarter split the columns), so an item's accumulator
+// and stage are released after half the epilogue latency.  Otherwise the sets alternate items.
+#ifndef CTS_EPI_SPLIT
+#define CTS_EPI_SPLIT 1
+#endif
+constexpr bool kEpiSplit = CTS_EPI_SPLIT != 0;
+constexpr int kEpiArrivals = kEpiSplit ? 4 * kEpiSets : 4;   // arrivals per item on acc_empty / empty
 
 struct alignas(64) ExpandMod {
   CUtensorMap tm_y;                      // y [T][d_out], box {64, 1}, 128B swizzle (per call)
@@ -51,7 +64,6 @@ struct alignas(64) ExpandMod {
 
 struct ExpandParams {
   ExpandMod mod[kMaxGroup];
-  int prefix[kMaxGroup + 1];             // item prefix over modules (tile bound * nblk each)
   int n_mod;
   int meta_ready;                        // 1: segment outputs are complete before griddep_wait
   int poll_first;                        // fused: 1 = wait for t before issuing the item's loads
@@ -100,12 +112,16 @@ template <int RP>
 __device__ __forceinline__ void expand_init_barriers(const ExpandRing& R) {   // one thread
   for (int s = 0; s < ExpandCfg<RP>::kStages; ++s) {
     mbar_init(&R.full[s], 1);
-    mbar_init(&R.empty[s], 4);          // one arrival per epilogue warp of the owning set
+    mbar_init(&R.empty[s], kEpiArrivals);   // one arrival per epilogue warp working on the item
   }
   for (int s = 0; s < kExpandAccSlots; ++s) {
     mbar_init(&R.acc_full[s], 1);
-    mbar_init(&R.acc_empty[s], 4);
+    mbar_init(&R.acc_empty[s], kEpiArrivals);
   }
+}
+
+__device__ __forceinline__ ItemMap expand_map(const ExpandParams& p, int nt_lane, int lane) {
+  return make_item_map(p.n_mod, nt_lane, lane < p.n_mod ? p.mod[lane].nblk : 0, lane);
 }
 
 template <int RP> __device__ __forceinline__ uint8_t* stage_y(const ExpandRing& R, int s) {
@@ -128,13 +144,13 @@ template <int RP> __device__ __forceinline__ int4* stage_info(const ExpandRing& 
 template <int RP>
 __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane) {
   using L = ExpandCfg<RP>;
-  const int total = p.prefix[p.n_mod];
-  int li = 0;                                     // index over this CTA's non-empty items
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const int g = find_module(p.prefix, p.n_mod, item);
+  const ItemMap M = expand_map(p, nt_lane, lane);
+  int li = 0;                                     // index over this CTA's items
+  for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
+    int local;
+    const int g = map_item(M, p.n_mod, item, lane, &local);
     const ExpandMod& m = p.mod[g];
-    const int tile = (item - p.prefix[g]) / m.nblk, nb = (item - p.prefix[g]) % m.nblk;
-    if (tile >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;
+    const int tile = local / m.nblk, nb = local % m.nblk;
     const int my = li++;
     if (my % kProducerWarps != warp) continue;
     const int4 t0 = m.tiles[2 * tile], t1 = m.tiles[2 * tile + 1];
@@ -203,13 +219,10 @@ __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_la
   // MMA per K step gives D0 = t U_c0^T (cols [0,128)) and D1 = t U_c1^T (cols [128,256)); for an
   // unshared slot the second block is stale and D1 is never read.
   constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * kBN);
-  const int total = p.prefix[p.n_mod];
+  const ItemMap M = expand_map(p, nt_lane, lane);
   int stage = 0, slot = 0;
   uint32_t phase = 0, aphase = 0;
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const int g = find_module(p.prefix, p.n_mod, item);
-    const ExpandMod& m = p.mod[g];
-    if ((item - p.prefix[g]) / m.nblk >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;
+  for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
     mbar_wait(&R.acc_empty[slot], aphase ^ 1);
     mbar_wait(&R.full[stage], phase);
     tc_fence_after();
@@ -231,21 +244,20 @@ __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_la
 }
 
 // ------------------------------------------------------------------ epilogue (warps 5-12)
-template <int RP, bool DIRECT>
+template <int RP, int STORE>
 __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane) {
   using L = ExpandCfg<RP>;
-  const int total = p.prefix[p.n_mod];
+  const ItemMap M = expand_map(p, nt_lane, lane);
   const int ew = warp - kEpiWarp0;               // 0..7
   const int set = ew >> 2;
   const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
   const int row = quarter * 32 + lane;
   int li = 0;
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const int g = find_module(p.prefix, p.n_mod, item);
-    const ExpandMod& m = p.mod[g];
-    if ((item - p.prefix[g]) / m.nblk >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;
+  for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
     const int my = li++;
-    if (my % kEpiSets != set) continue;
+    if (!kEpiSplit && my % kEpiSets != set) continue;
+    static_assert(!kEpiSplit || kEpiSets == kBN / 64, "split epilogue: one 64-column segment per set");
+    const int seg0 = kEpiSplit ? set : 0, seg1 = kEpiSplit ? set + 1 : kBN / 64;   // this warp's segments
     const int stage = my % L::kStages, slot = my % kExpandAccSlots;
     const uint32_t phase = (my / L::kStages) & 1, aphase = (my / kExpandAccSlots) & 1;
     mbar_wait(&R.acc_full[slot], aphase);
@@ -261,7 +273,7 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
     const bool active = quarter * 32 < len4;     // warp-uniform: this quarter holds live rows
     if (active) {
 #pragma unroll 1
-      for (int j2 = 0; j2 < kBN / 64; ++j2) {
+      for (int j2 = seg0; j2 < seg1; ++j2) {
         float v[64];
         const uint32_t taddr =
             R.tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * L::kSlotCols + sub * kBN + j2 * 64;
@@ -270,6 +282,7 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
         tmem_ld_wait();
         // rows len..len4 duplicate the last token (identical bytes for the 4-row scatter); the
         // direct variant stores real rows only
+        constexpr bool DIRECT = STORE == kStoreDirect;
         const bool live = DIRECT ? (row - sbase < slen) : (row < len4);
         if (live) {
           uint8_t* base = ys + j2 * L::kY + row * 128;   // 64 columns = one segment
@@ -299,12 +312,30 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&R.acc_empty[slot]);
-    if (!DIRECT && active) {
+    if (STORE == kStoreCoalesced && active) {
+      // lane -> (row, 64-column segment, 16-byte chunk): 8 lanes cover one 128-byte line, the two
+      // segments of a row are adjacent in y, so one instruction writes 2 rows x 256 contiguous bytes
+      const ExpandMod& mo = p.mod[info.x];
+      const int* rows = stage_rows<RP>(R, stage);
+      constexpr int nseg = kEpiSplit ? 1 : L::kSeg;
+#pragma unroll 4
+      for (int it = 0; it < nseg * 8; ++it) {
+        const int idx = it * 32 + lane;
+        const int rr = quarter * 32 + idx / (8 * nseg);
+        const int seg = seg0 + (idx >> 3) % nseg, ch = idx & 7;
+        const int col = info.z * kBN + seg * 64 + ch * 8;
+        if (rr - sbase < slen && col < mo.d_out) {
+          const uint4 w = *reinterpret_cast<const uint4*>(ys + seg * L::kY + rr * 128 + ((ch ^ (rr & 7)) << 4));
+          *reinterpret_cast<uint4*>(mo.y + static_cast<size_t>(rows[rr]) * mo.ld_y + col) = w;
+        }
+      }
+    }
+    if (STORE == kStoreScatter && active) {
       // this warp's 8 four-row groups: lane -> (group, segment); TMA scatter of the rows
       fence_proxy_async_smem();
       __syncwarp();
-      const int grp = quarter * 8 + (lane & 7), seg = lane >> 3;
-      if (grp * 4 < len4 && seg < L::kSeg) {
+      const int grp = quarter * 8 + (lane & 7), seg = seg0 + (lane >> 3);
+      if (grp * 4 < len4 && seg < seg1) {
         const int4 r4 = *reinterpret_cast<const int4*>(stage_rows<RP>(R, stage) + 4 * grp);
         tma_scatter4(&p.mod[info.x].tm_y, ys + seg * L::kY + grp * 512, info.z * kBN + seg * 64, r4.x, r4.y, r4.z,
                      r4.w);
@@ -315,7 +346,7 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
     __syncwarp();
     if (lane == 0) mbar_arrive(&R.empty[stage]);
   }
-  if (!DIRECT) bulk_wait0();                    // this warp's global writes complete before exit
+  if (STORE == kStoreScatter) bulk_wait0();     // this warp's global writes complete before exit
 }
 
 // ------------------------------------------------------------------ TP: reduced fp32 t -> hi | lo
@@ -355,7 +386,7 @@ struct ExpandKernelSmem {
   static constexpr int kBytes = kOffMisc + 64 + 1024;
 };
 
-template <int RP, bool DIRECT>
+template <int RP, int STORE>
 __global__ void __launch_bounds__(kApplyThreads, 1) expand_kernel(const __grid_constant__ ExpandParams p) {
   using S = ExpandKernelSmem<RP>;
   extern __shared__ uint8_t smem_raw[];
@@ -380,7 +411,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) expand_kernel(const __grid_c
 
   if (warp < kProducerWarps) expand_producer<RP>(p, R, nt_lane, warp, lane);
   else if (warp == kMmaWarp) expand_mma<RP>(p, R, nt_lane, lane);
-  else expand_epilogue<RP, DIRECT>(p, R, nt_lane, warp, lane);
+  else expand_epilogue<RP, STORE>(p, R, nt_lane, warp, lane);
 
   __syncthreads();
   if (warp == kMmaWarp) tmem_dealloc<ExpandCfg<RP>::kTmemCols>(R.tmem);

@@ -51,11 +51,12 @@ constexpr int kEpiSets = 2;             // epilogue warp-sets working on alterna
 constexpr int kApplyThreads = 32 * (kProducerWarps + 1 + 4 * kEpiSets);   // producers, MMA, epilogue
 constexpr int kShrinkThreads = kApplyThreads;
 constexpr int kShrinkAccSlots = 4;
+#ifndef CTS_KCHUNK_NUM
+#define CTS_KCHUNK_NUM 32   // finisher: partials fetched per L2 round trip = CTS_KCHUNK_NUM / r_pad
+#endif
 
 struct alignas(64) ShrinkMod {
   CUtensorMap tm_x;                     // x [T][d_in], box {64, 1}, 128B swizzle (per call)
-  const __nv_bfloat16* x;               // x base and row stride (elements), for the cp.async path
-  int64_t ld_x;
   const CUtensorMap* tm_in;             // in_basis [C*rp][d_in], box {64, rp} (bank, global mem)
   const int4* tiles;                    // [slot][2]: (cluster, start, len, -) per 64-row half
   const int32_t* n_tiles;               // real slot count of this module's map
@@ -64,21 +65,20 @@ struct alignas(64) ShrinkMod {
   const __nv_bfloat16* sigma;           // [N][rp][rp], row = out index
   __nv_bfloat16* tbuf;                  // [max_tiles*128][2*rp]  (hi | lo)
   float* tpart;                         // TP partial mode: fp32 t in TOKEN order [T][rp] instead of tbuf
-  float* ws;                            // [ks][ws_rows][rp] split-K partials
+  float* ws;                            // [(slot*ks + kc)*128 + row][rp] split-K partials
   int32_t* counters;                    // [max_tiles] arrivals per slot (self-resetting)
   int32_t* ready;                       // [max_tiles] "t ready" flags (fused kernel only; else null)
   int kblocks;                          // d_in / 64
-  int ks;                               // K chunks per tile
-  int ws_rows;                          // tile bound * 128
   float scale;
 };
 
 struct ShrinkParams {
   ShrinkMod mod[kMaxGroup];
-  int prefix[kMaxGroup + 1];            // item prefix over modules (tile bound * ks each)
   int n_mod;
+  int tiles_bound;                      // host-known slot bound per module (flag clearing)
+  int ks_max;                           // K chunks per slot: cap (>= 4 K blocks each, workspace fit)
+  int target_items;                     // wanted items per SM (K chunks sized on the device)
   int meta_ready;                       // 1: segment outputs are complete before griddep_wait
-  int x_cpasync;                        // 1: x rows by per-thread cp.async, 0: TMA tile::gather4
 };
 
 template <int RP>
@@ -95,10 +95,51 @@ struct ShrinkCfg {
   static constexpr uint32_t kTmemCols = kSlotCols * kShrinkAccSlots;  // 128 / 256 / 512
 };
 
-// item -> module g through the per-module item prefix sums
-__device__ __forceinline__ int find_module(const int* prefix, int n_mod, int item) {
-  int g = 0;
-  while (g + 1 < n_mod && item >= prefix[g + 1]) ++g;
+// ------------------------------------------------------------------ device-side work map
+// Work items are laid over the REAL slot counts the segment kernel produced (lane g of every warp
+// holds module g's count, nt_lane), so no item is empty and the K split is sized from the real
+// slot total: ks = ceil(target_items * grid / slots), capped by the host.  Every role of every CTA
+// derives the identical map from the same counts.
+struct ItemMap {
+  int pre;                              // lane g < n_mod: first item of module g
+  int total;                            // items in the launch
+  int per;                              // items per slot of this lane's module (ks or nblk)
+};
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ ItemMap make_item_map(int n_mod, int nt_lane, int per_lane, int lane) {
+  ItemMap M;
+  const int cnt = lane < n_mod ? nt_lane * per_lane : 0;
+  int inc = cnt;                                           // inclusive scan over lanes
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  M.pre = inc - cnt;
+  M.total = __shfl_sync(0xffffffffu, inc, 31);
+  M.per = per_lane;
+  return M;
+}
+
+// K chunks per slot for the shrink, from the real slot total of the group
+__device__ __forceinline__ int shrink_ks(const ShrinkParams& p, int nt_lane, int lane) {
+  const int slots = warp_sum(lane < p.n_mod ? nt_lane : 0);
+  if (slots == 0) return 1;
+  const int want = (p.target_items * static_cast<int>(gridDim.x) + slots - 1) / slots;
+  return max(1, min(want, p.ks_max));
+}
+
+// item -> (module g, index within the module); warp-uniform item, all lanes participate
+__device__ __forceinline__ int map_item(const ItemMap& M, int n_mod, int item, int lane, int* local) {
+  const unsigned b = __ballot_sync(0xffffffffu, lane < n_mod && M.pre <= item);
+  const int g = 31 - __clz(b);
+  *local = item - __shfl_sync(0xffffffffu, M.pre, g);
   return g;
 }
 
@@ -130,9 +171,9 @@ __device__ __forceinline__ ShrinkRing shrink_ring(uint8_t* arena, uint64_t* bars
 }
 
 template <int RP>
-__device__ __forceinline__ void shrink_init_barriers(const ShrinkRing& R, int x_cpasync) {   // one thread
+__device__ __forceinline__ void shrink_init_barriers(const ShrinkRing& R) {   // one thread
   for (int s = 0; s < ShrinkCfg<RP>::kStages; ++s) {
-    mbar_init(&R.full[s], x_cpasync ? 33 : 1);  // cp.async path: the 32 lanes + the B-slab expect_tx
+    mbar_init(&R.full[s], 1);
     mbar_init(&R.empty[s], 1);
   }
   for (int s = 0; s < kShrinkAccSlots; ++s) {
@@ -152,17 +193,18 @@ struct ShrinkFirst {
 
 __device__ __forceinline__ ShrinkFirst shrink_first_meta(const ShrinkParams& p, int nt_lane, int lane) {
   ShrinkFirst f;
-  const int total = p.prefix[p.n_mod];
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const int g = find_module(p.prefix, p.n_mod, item);
+  const int ks = shrink_ks(p, nt_lane, lane);
+  const ItemMap M = make_item_map(p.n_mod, nt_lane, ks, lane);
+  const int item = blockIdx.x;
+  if (item < M.total) {
+    int local;
+    const int g = map_item(M, p.n_mod, item, lane, &local);
     const ShrinkMod& m = p.mod[g];
-    const int tile = (item - p.prefix[g]) / m.ks;
-    if (tile >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;
+    const int tile = local / ks;
     f.item = item;
     f.t0 = m.tiles[2 * tile];
     f.t1 = m.tiles[2 * tile + 1];
     f.r4 = *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
-    break;
   }
   return f;
 }
@@ -171,13 +213,14 @@ template <int RP>
 __device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int warp, int lane,
                                 const ShrinkFirst& first = ShrinkFirst()) {
   using L = ShrinkCfg<RP>;
-  const int total = p.prefix[p.n_mod];
+  const int ks = shrink_ks(p, nt_lane, lane);
+  const ItemMap M = make_item_map(p.n_mod, nt_lane, ks, lane);
   int li = 0;                                     // K-block sequence index over this CTA's items
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const int g = find_module(p.prefix, p.n_mod, item);
+  for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
+    int local;
+    const int g = map_item(M, p.n_mod, item, lane, &local);
     const ShrinkMod& m = p.mod[g];
-    const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
-    if (tile >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;   // empty tile slot
+    const int tile = local / ks, kc = local % ks;
     const bool pre = item == first.item;
     const int4 t0 = pre ? first.t0 : m.tiles[2 * tile], t1 = pre ? first.t1 : m.tiles[2 * tile + 1];
     const int4 r4 = pre ? first.r4 : *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
@@ -185,47 +228,23 @@ __device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, int 
     const int l0 = (t0.z + 3) & ~3, l1 = (t1.z + 3) & ~3;
     const bool gvalid = shared ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
     const int ngroups = (l0 + l1) >> 2;
-    const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
+    const int kb0 = kc * m.kblocks / ks, kb1 = (kc + 1) * m.kblocks / ks;
     const uint32_t bbytes = static_cast<uint32_t>((shared ? 2 : 1) * L::kB1);
-    const uint32_t bytes = p.x_cpasync ? bbytes : static_cast<uint32_t>(ngroups * 512) + bbytes;
-    // cp.async path: lane copies 16-byte chunk (lane & 7) of rows (lane >> 3) + 4j, j < 32, into its
-    // 128B-swizzled place (chunk ^ row % 8); the row tokens come from the 4-row groups r4 of lane
-    // (row >> 2) by shuffle, once per item
-    int tok[32];
-    uint32_t vmask = 0;
-    if (p.x_cpasync) {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int r = (lane >> 3) + 4 * j;                  // slot row; its 4-row group is r >> 2 = j
-        const int4 g4 = make_int4(__shfl_sync(0xffffffffu, r4.x, j), __shfl_sync(0xffffffffu, r4.y, j),
-                                  __shfl_sync(0xffffffffu, r4.z, j), __shfl_sync(0xffffffffu, r4.w, j));
-        const int q = r & 3;
-        tok[j] = q == 0 ? g4.x : q == 1 ? g4.y : q == 2 ? g4.z : g4.w;
-        const bool v = shared ? (r < kTileM / 2 ? r < l0 : r - kTileM / 2 < l1) : r < l0;
-        vmask |= static_cast<uint32_t>(v) << j;
-      }
-    }
+    const uint32_t bytes = static_cast<uint32_t>(ngroups * 512) + bbytes;
     for (int kb = kb0; kb < kb1; ++kb, ++li) {
       if (li % kProducerWarps != warp) continue;
       const int stage = li % L::kStages;
       const uint32_t phase = (li / L::kStages) & 1;
+      if (li == 0 && lane == 0) CTS_STAMP(16);          // first item mapped
       mbar_wait(&R.empty[stage], phase ^ 1);
       if (lane == 0) mbar_arrive_expect_tx(&R.full[stage], bytes);
+      if (li == 0 && lane == 0) CTS_STAMP(17);          // expect_tx armed
       __syncwarp();
       uint8_t* dA = R.sA + stage * L::kA;
-      if (p.x_cpasync) {
-        const int c = lane & 7;
-        const __nv_bfloat16* src = m.x + kb * kBK + c * 8;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int r = (lane >> 3) + 4 * j;
-          if (vmask & (1u << j))
-            cp_async16(dA + r * 128 + ((c ^ (r & 7)) << 4), src + static_cast<int64_t>(tok[j]) * m.ld_x);
-        }
-        cp_async_mbar_arrive(&R.full[stage]);
-      } else if (gvalid) {
+      if (gvalid) {
         tma_gather4(dA + lane * 512, &m.tm_x, &R.full[stage], kb * kBK, r4.x, r4.y, r4.z, r4.w);
       }
+      if (li == 0 && lane == 0) CTS_STAMP(18);          // first x gathers issued
       if (lane == 0) {
         tma_load_2d(R.sB + stage * L::kB, m.tm_in, &R.full[stage], kb * kBK, t0.x * RP);
         if (shared) tma_load_2d(R.sB + stage * L::kB + L::kB1, m.tm_in, &R.full[stage], kb * kBK, t1.x * RP);
@@ -247,15 +266,16 @@ __device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, int nt_la
   // second slab is stale and D1 is never read.  (A second MMA per K step measurably slowed the
   // single issuing thread.)
   constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * RP);
-  const int total = p.prefix[p.n_mod];
+  const int ks = shrink_ks(p, nt_lane, lane);
+  const ItemMap M = make_item_map(p.n_mod, nt_lane, ks, lane);
   int stage = 0, slot = 0;
   uint32_t phase = 0, aphase = 0;
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const int g = find_module(p.prefix, p.n_mod, item);
+  for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
+    int local;
+    const int g = map_item(M, p.n_mod, item, lane, &local);
     const ShrinkMod& m = p.mod[g];
-    const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
-    if (tile >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;
-    const int kb0 = kc * m.kblocks / m.ks, kb1 = (kc + 1) * m.kblocks / m.ks;
+    const int kc = local % ks;
+    const int kb0 = kc * m.kblocks / ks, kb1 = (kc + 1) * m.kblocks / ks;
     mbar_wait(&R.acc_empty[slot], aphase ^ 1);
     tc_fence_after();
     const uint32_t acc = R.tmem + slot * L::kSlotCols;
@@ -295,18 +315,19 @@ __device__ __forceinline__ void shrink_drain_tmem(const ShrinkRing& R, int slot,
 template <int RP>
 __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int warp, int lane) {
   using L = ShrinkCfg<RP>;
-  const int total = p.prefix[p.n_mod];
+  const int ks = shrink_ks(p, nt_lane, lane);
+  const ItemMap M = make_item_map(p.n_mod, nt_lane, ks, lane);
   const int ew = warp - kEpiWarp0;              // 0..7
   const int set = ew >> 2;
   const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
   const int row = quarter * 32 + lane;
   const int set_tid = (ew & 3) * 32 + lane;      // 0..127 within the set
-  int li = 0;                                    // index over this CTA's non-empty items
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const int g = find_module(p.prefix, p.n_mod, item);
+  int li = 0;                                    // index over this CTA's items
+  for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
+    int local;
+    const int g = map_item(M, p.n_mod, item, lane, &local);
     const ShrinkMod& m = p.mod[g];
-    const int tile = (item - p.prefix[g]) / m.ks, kc = (item - p.prefix[g]) % m.ks;
-    if (tile >= __shfl_sync(0xffffffffu, nt_lane, g)) continue;
+    const int tile = local / ks, kc = local % ks;
     const bool mine = (li % kEpiSets) == set;
     const int slot = li % kShrinkAccSlots;
     const uint32_t aphase = (li / kShrinkAccSlots) & 1;
@@ -324,6 +345,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int 
     }
     mbar_wait(&R.acc_full[slot], aphase);
     tc_fence_after();
+    if (li <= 2 && set_tid == 0) CTS_STAMP(19);        // first accumulator ready
     float s[RP];
 #pragma unroll
     for (int c = 0; c < RP; c += 16)
@@ -334,37 +356,47 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int 
     if (lane == 0) mbar_arrive(&R.acc_empty[slot]);
 
     bool finisher = true;
-    if (m.ks > 1) {
+    if (ks > 1) {
       // split-K: publish this chunk's partial; the LAST arriving CTA (acq_rel counter) sums the
-      // ks partials in kc order, so the result does not depend on scheduling
+      // ks partials in kc order, so the result does not depend on scheduling.
+      // Workspace row = (slot*ks + kc)*128 + row.
+      float* const wbase = m.ws + (static_cast<size_t>(tile) * ks * kTileM + row) * RP;   // + kc*128*RP
       if (rvalid) {
-        float4* dst = reinterpret_cast<float4*>(m.ws + (static_cast<size_t>(kc) * m.ws_rows + tile * kTileM + row) * RP);
+        float4* dst = reinterpret_cast<float4*>(wbase + static_cast<size_t>(kc) * kTileM * RP);
 #pragma unroll
         for (int c = 0; c < RP / 4; ++c) dst[c] = make_float4(s[4 * c], s[4 * c + 1], s[4 * c + 2], s[4 * c + 3]);
       }
       named_bar_sync(1 + set, 128);
-      if (set_tid == 0) R.s_last[set] = (atom_add_acq_rel_gpu(&m.counters[tile], 1) == m.ks - 1);
+      if (set_tid == 0) R.s_last[set] = (atom_add_acq_rel_gpu(&m.counters[tile], 1) == ks - 1);
       named_bar_sync(1 + set, 128);
       finisher = R.s_last[set] != 0;
       if (set_tid == 0 && finisher) CTS_STAMP(12);         // last arrival known
       if (finisher) {
         if (rvalid) {
-          // sum the partials in kc order (deterministic); this CTA's own chunk comes from registers
-          float own[RP];
+          // sum in kc order (deterministic), this CTA's own chunk included (it is in L2 from the
+          // store above); kChunk partials are fetched at a time, all their loads in flight
+          // together: ceil(ks/kChunk) L2 round trips instead of ks
+          constexpr int kChunk = CTS_KCHUNK_NUM / RP > 1 ? CTS_KCHUNK_NUM / RP : 1;
 #pragma unroll
-          for (int c = 0; c < RP; ++c) { own[c] = s[c]; s[c] = 0.f; }
-          for (int q = 0; q < m.ks; ++q) {
-            if (q == kc) {
+          for (int c = 0; c < RP; ++c) s[c] = 0.f;
+          for (int q0 = 0; q0 < ks; q0 += kChunk) {
+            float4 buf[kChunk][RP / 4];
 #pragma unroll
-              for (int c = 0; c < RP; ++c) s[c] += own[c];
-              continue;
+            for (int j = 0; j < kChunk; ++j) {
+              if (q0 + j < ks) {
+                const float4* src = reinterpret_cast<const float4*>(wbase + static_cast<size_t>(q0 + j) * kTileM * RP);
+#pragma unroll
+                for (int c = 0; c < RP / 4; ++c) buf[j][c] = __ldcg(src + c);
+              }
             }
-            const float4* src = reinterpret_cast<const float4*>(
-                m.ws + (static_cast<size_t>(q) * m.ws_rows + tile * kTileM + row) * RP);
 #pragma unroll
-            for (int c = 0; c < RP / 4; ++c) {
-              const float4 v = __ldcg(src + c);
-              s[4 * c] += v.x; s[4 * c + 1] += v.y; s[4 * c + 2] += v.z; s[4 * c + 3] += v.w;
+            for (int j = 0; j < kChunk; ++j) {
+              if (q0 + j >= ks) break;
+#pragma unroll
+              for (int c = 0; c < RP / 4; ++c) {
+                s[4 * c] += buf[j][c].x; s[4 * c + 1] += buf[j][c].y;
+                s[4 * c + 2] += buf[j][c].z; s[4 * c + 3] += buf[j][c].w;
+              }
             }
           }
         }
@@ -449,7 +481,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) shrink_sigma_kernel(const __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     CTS_STAMP(0);
-    shrink_init_barriers<RP>(R, p.x_cpasync);
+    shrink_init_barriers<RP>(R);
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<ShrinkCfg<RP>::kTmemCols>(tmem_slot);

@@ -230,6 +230,9 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* addr, int v) {
 __device__ __forceinline__ void st_release_gpu(int* addr, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
 }
+__device__ __forceinline__ void red_release_add_gpu(int* addr, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ int ld_acquire_gpu(const int* addr) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
@@ -246,7 +249,7 @@ __device__ __forceinline__ void nanosleep_ns(uint32_t ns) { asm volatile("nanosl
 
 // ------------------------------------------------------------------ debug timeline (off unless traced)
 // A kernel built with CTS_TRACE records %globaltimer stamps per CTA into g_cts_trace[cta][slot].
-constexpr int kTraceSlots = 16;
+constexpr int kTraceSlots = 24;
 constexpr int kTraceCtas = 160;
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;

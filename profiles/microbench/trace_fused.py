@@ -28,15 +28,16 @@ names = {0: "start", 1: "prologue+wait", 2: "shrink first TMA", 3: "shrink produ
          5: "shrink epi set0 done", 6: "shrink epi set1 done", 7: "expand producers start", 8: "expand first t ready",
          9: "expand producers done", 10: "expand epi done", 11: "end",
          12: "finisher: last arrival", 13: "finisher: partials summed", 14: "finisher: t stored",
-         15: "finisher: flag published"}
+         15: "finisher: flag published", 16: "shrink: first item mapped", 17: "shrink: expect_tx armed",
+         18: "shrink: first gathers issued", 19: "shrink: first acc ready"}
 for grp in ([0, 1, 2], [3, 4]):
     for rep in range(3):
         big.zero_()
         plan.apply_group(grp, [x] * len(grp), [ys[m] for m in grp], 2.0)
         torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (160 * 16))()
-    L.cts_debug_trace(buf, 160 * 16)
-    a = np.array(buf, dtype=np.int64).reshape(160, 16)[:148].astype(np.float64)
+    buf = (ctypes.c_ulonglong * (160 * 24))()
+    L.cts_debug_trace(buf, 160 * 24)
+    a = np.array(buf, dtype=np.int64).reshape(160, 24)[:148].astype(np.float64)
     t0 = a[:, 0].min()
     rel = (a - t0) / 1e3
     print(f"fused group {grp} (T={T}): us after first CTA start: min / median / max over CTAs")
