@@ -35,7 +35,8 @@ struct FusedSmem {
   static constexpr int kOffBarS = kArena;
   static constexpr int kOffBarE = kOffBarS + ShrinkCfg<RP>::kNumBars * 8;
   static constexpr int kOffBarF = kOffBarE + ExpandCfg<RP>::kNumBars * 8;   // "shrink operands consumed"
-  static constexpr int kOffMisc = kOffBarF + 8;
+  static constexpr int kOffBarT = kOffBarF + 8;                                // "shrink TMEM released"
+  static constexpr int kOffMisc = kOffBarT + 8;
   static constexpr int kBytes = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;
   static_assert(ShrinkCfg<RP>::kTmemCols <= kTmemCols && ExpandCfg<RP>::kTmemCols <= kTmemCols, "TMEM");
@@ -52,12 +53,14 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
                                   reinterpret_cast<int*>(smem + S::kOffMisc + 16));
   ExpandRing RE = expand_ring<RP>(smem, reinterpret_cast<uint64_t*>(smem + S::kOffBarE));
   uint64_t* arena_free = reinterpret_cast<uint64_t*>(smem + S::kOffBarF);
+  uint64_t* tmem_free = reinterpret_cast<uint64_t*>(smem + S::kOffBarT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     CTS_STAMP(0);
     shrink_init_barriers<RP>(RS);
     expand_init_barriers<RP>(RE);
     mbar_init(arena_free, 1);
+    mbar_init(tmem_free, 4 * kEpiSets);       // every epilogue warp, after its last shrink TMEM access
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<S::kTmemCols>(tmem_slot);
@@ -88,7 +91,8 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   // No CTA-wide barrier between the phases: each role moves on as soon as what it reuses is free.
   //   producers: the operand arena, once the shrink MMAs have consumed every stage (arena_free,
   //              committed by the MMA warp after its last MMA);
-  //   MMA warp:  the TMEM columns, once the epilogue has read every shrink accumulator;
+  //   MMA warp:  the TMEM columns, once every epilogue warp is done with its shrink TMEM (the
+//              accumulators and the staged Sigma_i, tmem_free);
   //   epilogue:  nothing -- it takes expand items after its own split-K / Sigma work, so expand
   //              loads and MMAs of this CTA overlap its shrink finisher chain.
   if (warp < kProducerWarps) {
@@ -103,10 +107,15 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
     shrink_mma<RP>(p.s, RS, nt_lane, lane, &slot, &aphase);
     if (lane == 0) { umma_commit(arena_free); CTS_STAMP(4); }
     __syncwarp();
-    shrink_drain_tmem(RS, slot, aphase);
+    (void)slot; (void)aphase;
+    mbar_wait(tmem_free, 0);                  // shrink accumulators and staged Sigma all read
+    tc_fence_after();
     expand_mma<RP>(p.e, RE, nt_lane, lane);
   } else {
     shrink_epilogue<RP>(p.s, RS, nt_lane, warp, lane);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tmem_free);
     if (threadIdx.x == 32 * kEpiWarp0) CTS_STAMP(5);        // epilogue set 0 done
     if (threadIdx.x == 32 * (kEpiWarp0 + 4)) CTS_STAMP(6);  // epilogue set 1 done
     expand_epilogue<RP, STORE>(p.e, RE, nt_lane, warp, lane);

@@ -52,7 +52,7 @@ constexpr int kApplyThreads = 32 * (kProducerWarps + 1 + 4 * kEpiSets);   // pro
 constexpr int kShrinkThreads = kApplyThreads;
 constexpr int kShrinkAccSlots = 4;
 #ifndef CTS_KCHUNK_NUM
-#define CTS_KCHUNK_NUM 32   // finisher: partials fetched per L2 round trip = CTS_KCHUNK_NUM / r_pad
+#define CTS_KCHUNK_NUM 48   // finisher: partials fetched per L2 round trip = CTS_KCHUNK_NUM / r_pad
 #endif
 
 struct alignas(64) ShrinkMod {
@@ -92,13 +92,20 @@ struct ShrinkCfg {
   static constexpr int kArena = kOffB + kStages * kB;          // bytes of staged operands
   static constexpr int kNumBars = 2 * kStages + 2 * kShrinkAccSlots;
   static constexpr uint32_t kSlotCols = 2 * RP < 32 ? 32 : 2 * RP;   // D0 | D1 (one per slot half)
-  static constexpr uint32_t kTmemCols = kSlotCols * kShrinkAccSlots;  // 128 / 256 / 512
+  // r_pad = 16: each epilogue set stages its row's Sigma_i (16 x 16 bf16 = 128 TMEM columns) in
+  // TMEM while the MMA runs, so the finisher's Sigma matvec reads TMEM instead of doing two
+  // dependent global round trips on the split-K critical path
+  static constexpr bool kSigmaTmem = RP == 16;
+  static constexpr uint32_t kSigmaCol0 = kSlotCols * kShrinkAccSlots;
+  static constexpr uint32_t kSigmaCols = kSigmaTmem ? RP * RP / 2 : 0;  // per set
+  static constexpr uint32_t kUsedCols = kSigmaCol0 + kEpiSets * kSigmaCols;
+  static constexpr uint32_t kTmemCols = kUsedCols <= 128 ? 128 : (kUsedCols <= 256 ? 256 : 512);
 };
 
 // ------------------------------------------------------------------ device-side work map
 // Work items are laid over the REAL slot counts the segment kernel produced (lane g of every warp
 // holds module g's count, nt_lane), so no item is empty and the K split is sized from the real
-// slot total: ks = ceil(target_items * grid / slots), capped by the host.  Every role of every CTA
+// slot total: ks = floor(target_items * grid / slots), capped by the host.  Every role of every CTA
 // derives the identical map from the same counts.
 struct ItemMap {
   int pre;                              // lane g < n_mod: first item of module g
@@ -131,7 +138,9 @@ __device__ __forceinline__ ItemMap make_item_map(int n_mod, int nt_lane, int per
 __device__ __forceinline__ int shrink_ks(const ShrinkParams& p, int nt_lane, int lane) {
   const int slots = warp_sum(lane < p.n_mod ? nt_lane : 0);
   if (slots == 0) return 1;
-  const int want = (p.target_items * static_cast<int>(gridDim.x) + slots - 1) / slots;
+  // floor, not ceil: items <= target * grid, so no CTA takes a second shrink item whose slot's
+  // split-K exchange (and every expand item waiting on it) would then finish a whole item later
+  const int want = (p.target_items * static_cast<int>(gridDim.x)) / slots;
   return max(1, min(want, p.ks_max));
 }
 
@@ -338,7 +347,23 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int 
     const int slen4 = ((sub ? t1.z : t0.z) + 3) & ~3;
     const bool rvalid = row - sub * (kTileM / 2) < slen4;
     const int adapter = rvalid ? m.tile_adapters[tile * kTileM + row] : 0;
-    if (rvalid) {                                 // warm L2 with this row's Sigma_i while the MMA runs
+    const uint32_t tsig = R.tmem + (static_cast<uint32_t>(quarter * 32) << 16) + L::kSigmaCol0 + set * L::kSigmaCols;
+    if constexpr (L::kSigmaTmem) {
+      // this row's Sigma_i -> TMEM lane `row`, 64 columns (8 rows of Sigma_i) per global round trip
+      const uint4* sg = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        uint32_t w[64];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const uint4 q = rvalid ? __ldg(sg + 16 * h + v) : make_uint4(0, 0, 0, 0);
+          w[4 * v] = q.x; w[4 * v + 1] = q.y; w[4 * v + 2] = q.z; w[4 * v + 3] = q.w;
+        }
+        tmem_st32(tsig + 64 * h, w);
+        tmem_st32(tsig + 64 * h + 32, w + 32);
+      }
+      tmem_st_wait();
+    } else if (rvalid) {                          // warm L2 with this row's Sigma_i while the MMA runs
       const uint8_t* sp = reinterpret_cast<const uint8_t*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
 #pragma unroll
       for (int off = 0; off < RP * RP * 2; off += 128) prefetch_l2(sp + off);
@@ -404,7 +429,54 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int 
         if (set_tid == 0) CTS_STAMP(13);                // partials summed
       }
     }
-    if (finisher && rvalid) {
+    if (L::kSigmaTmem && finisher) {
+      // t = scale * Sigma_i s from the TMEM-staged Sigma_i (warp-collective loads: whole warps)
+      float t[RP];
+#pragma unroll 1
+      for (int h = 0; h < 4; ++h) {             // (t is indexed by h: a 64-byte local array)
+        float w[32];
+        tmem_ld32(tsig + 32 * h, w);
+        tmem_ld_wait();
+#pragma unroll
+        for (int oo = 0; oo < 4; ++oo) {               // Sigma rows 4h .. 4h+3, 16 bf16 each
+          float acc = 0.f;
+#pragma unroll
+          for (int e = 0; e < RP / 2; ++e) {
+            const uint32_t u = __float_as_uint(w[oo * (RP / 2) + e]);
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+            acc = fmaf(f.x, s[2 * e], acc);
+            acc = fmaf(f.y, s[2 * e + 1], acc);
+          }
+          t[4 * h + oo] = acc * m.scale;
+        }
+      }
+      if (rvalid) {
+        if (m.tpart != nullptr) {
+          const int tok = m.tile_rows[tile * kTileM + row];
+          float4* dp = reinterpret_cast<float4*>(m.tpart + static_cast<size_t>(tok) * RP);
+#pragma unroll
+          for (int c = 0; c < RP / 4; ++c) dp[c] = make_float4(t[4 * c], t[4 * c + 1], t[4 * c + 2], t[4 * c + 3]);
+        } else {
+          __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP);
+#pragma unroll
+          for (int o0 = 0; o0 < RP; o0 += 8) {
+            uint4 hi, lo;
+            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&hi);
+            __nv_bfloat162* ll = reinterpret_cast<__nv_bfloat162*>(&lo);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const __nv_bfloat162 h2 = __floats2bfloat162_rn(t[o0 + 2 * e], t[o0 + 2 * e + 1]);
+              const float2 hf = __bfloat1622float2(h2);
+              hh[e] = h2;
+              ll[e] = __floats2bfloat162_rn(t[o0 + 2 * e] - hf.x, t[o0 + 2 * e + 1] - hf.y);
+            }
+            *reinterpret_cast<uint4*>(dst + o0) = hi;
+            *reinterpret_cast<uint4*>(dst + RP + o0) = lo;
+          }
+        }
+      }
+    }
+    if (!L::kSigmaTmem && finisher && rvalid) {
       // t = scale * Sigma_i s ; thread = token row
       const uint4* srow = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
       const int tok = m.tpart != nullptr ? m.tile_rows[tile * kTileM + row] : 0;
