@@ -77,14 +77,19 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   RS.tmem = RE.tmem = *tmem_slot;
   // shrink and expand items cover the same modules, so one per-module slot count serves both
   int nt_lane = 0;
+  ShrinkWork W;
   ShrinkFirst first;
   if (p.s.meta_ready) {
     nt_lane = lane < p.s.n_mod ? *p.s.mod[lane].n_tiles : 0;
-    if (warp < kProducerWarps) first = shrink_first_meta(p.s, nt_lane, lane);
+    W = shrink_work(p.s, nt_lane, lane);
+    if (warp < kProducerWarps) first = shrink_first_meta(p.s, W, lane);
   }
   griddep_wait();
   if (threadIdx.x == 0) griddep_launch_dependents();
-  if (!p.s.meta_ready) nt_lane = lane < p.s.n_mod ? *p.s.mod[lane].n_tiles : 0;
+  if (!p.s.meta_ready) {
+    nt_lane = lane < p.s.n_mod ? *p.s.mod[lane].n_tiles : 0;
+    W = shrink_work(p.s, nt_lane, lane);
+  }
   if (threadIdx.x == 0) CTS_STAMP(1);
 
   // ---------------------------------------------------------------- phase 1 -> phase 2, per role
@@ -96,7 +101,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   //   epilogue:  nothing -- it takes expand items after its own split-K / Sigma work, so expand
   //              loads and MMAs of this CTA overlap its shrink finisher chain.
   if (warp < kProducerWarps) {
-    shrink_producer<RP>(p.s, RS, nt_lane, warp, lane, first);
+    shrink_producer<RP>(p.s, RS, W, warp, lane, first);
     if (threadIdx.x == 0) CTS_STAMP(3);               // producers done issuing
     mbar_wait(arena_free, 0);
     if (threadIdx.x == 0) CTS_STAMP(7);
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   } else if (warp == kMmaWarp) {
     int slot = 0;
     uint32_t aphase = 0;
-    shrink_mma<RP>(p.s, RS, nt_lane, lane, &slot, &aphase);
+    shrink_mma<RP>(p.s, RS, W, lane, &slot, &aphase);
     if (lane == 0) { umma_commit(arena_free); CTS_STAMP(4); }
     __syncwarp();
     (void)slot; (void)aphase;
@@ -112,7 +117,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
     tc_fence_after();
     expand_mma<RP>(p.e, RE, nt_lane, lane);
   } else {
-    shrink_epilogue<RP>(p.s, RS, nt_lane, warp, lane);
+    shrink_epilogue<RP>(p.s, RS, W, warp, lane);
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(tmem_free);

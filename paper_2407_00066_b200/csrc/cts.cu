@@ -206,6 +206,17 @@ int poll_first_default(int T, int C) {
   return T < 96 * C ? 0 : 1;
 }
 
+// fused kernel, expand producer: how many of a CTA's expand items may load y / out_basis before
+// their t is ready (the rest poll first, so their loads do not queue ahead of the split-K
+// exchange's round trips).  CTS_EARLY_ITEMS overrides (tuning aid).
+int early_items_default() {
+  static int v = [] {
+    const char* e = std::getenv("CTS_EARLY_ITEMS");
+    return e ? std::atoi(e) : 4;
+  }();
+  return v;
+}
+
 // cts_apply[_group] runs the fused single-launch kernel unless CTS_FUSED=0 (tuning aid).
 bool use_fused() {
   static bool v = [] {
@@ -357,6 +368,7 @@ cts_status_t launch_fused(cts_plan_t p, int n, const int32_t* modules, const voi
   if ((st = fill_expand(p, n, modules, ys, ld_y, true, prm.e, items_e)) != CTS_OK) return st;
   prm.s.meta_ready = prm.e.meta_ready = next_meta_ready(p);
   prm.e.poll_first = poll_first_default(p->T, p->bank->C);
+  prm.e.early_items = early_items_default();
   prm.exit_count = p->exit_count;
   CTS_CUDA(launch_pdl(apply_fused_kernel<RP, STORE>, std::min(sm_count(), std::max(items_s, items_e)), kApplyThreads,
                       FusedSmem<RP>::kBytes, stream, prm));

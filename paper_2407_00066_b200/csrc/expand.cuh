@@ -67,6 +67,8 @@ struct ExpandParams {
   int n_mod;
   int meta_ready;                        // 1: segment outputs are complete before griddep_wait
   int poll_first;                        // fused: 1 = wait for t before issuing the item's loads
+  int early_items;                       // fused, poll_first = 0: only this CTA's first early_items items
+                                         // issue their y / out_basis loads before their t is ready
 };
 
 template <int RP>
@@ -161,8 +163,9 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
     const int l0 = (t0.z + 3) & ~3, l1 = (t1.z + 3) & ~3;
     const bool gvalid = shared ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
     const int ngroups = (l0 + l1) >> 2;
-    const bool poll_late = m.ready != nullptr && !p.poll_first;
-    if (m.ready != nullptr && p.poll_first) {
+    const bool early = !p.poll_first && my < p.early_items;
+    const bool poll_late = m.ready != nullptr && early;
+    if (m.ready != nullptr && !early) {
       if (lane == 0) {
         while (ld_acquire_gpu(m.ready + tile) == 0) nanosleep_ns(64);
         fence_proxy_async_global();

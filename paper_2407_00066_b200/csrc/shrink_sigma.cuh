@@ -144,6 +144,14 @@ __device__ __forceinline__ int shrink_ks(const ShrinkParams& p, int nt_lane, int
   return max(1, min(want, p.ks_max));
 }
 
+// The shrink's work map of a launch: K chunks per slot and the item map (per warp, lane g holding
+// module g's values).  Computed once per warp -- before griddep_wait when the segment outputs are
+// already complete -- so the parameter and shuffle latency stays off the critical path.
+struct ShrinkWork {
+  int ks;
+  ItemMap M;
+};
+
 // item -> (module g, index within the module); warp-uniform item, all lanes participate
 __device__ __forceinline__ int map_item(const ItemMap& M, int n_mod, int item, int lane, int* local) {
   const unsigned b = __ballot_sync(0xffffffffu, lane < n_mod && M.pre <= item);
@@ -200,10 +208,17 @@ struct ShrinkFirst {
   int4 t0, t1, r4;
 };
 
-__device__ __forceinline__ ShrinkFirst shrink_first_meta(const ShrinkParams& p, int nt_lane, int lane) {
+__device__ __forceinline__ ShrinkWork shrink_work(const ShrinkParams& p, int nt_lane, int lane) {
+  ShrinkWork w;
+  w.ks = shrink_ks(p, nt_lane, lane);
+  w.M = make_item_map(p.n_mod, nt_lane, w.ks, lane);
+  return w;
+}
+
+__device__ __forceinline__ ShrinkFirst shrink_first_meta(const ShrinkParams& p, const ShrinkWork& W, int lane) {
   ShrinkFirst f;
-  const int ks = shrink_ks(p, nt_lane, lane);
-  const ItemMap M = make_item_map(p.n_mod, nt_lane, ks, lane);
+  const int ks = W.ks;
+  const ItemMap& M = W.M;
   const int item = blockIdx.x;
   if (item < M.total) {
     int local;
@@ -219,11 +234,11 @@ __device__ __forceinline__ ShrinkFirst shrink_first_meta(const ShrinkParams& p, 
 }
 
 template <int RP>
-__device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int warp, int lane,
+__device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, const ShrinkWork& W, int warp, int lane,
                                 const ShrinkFirst& first = ShrinkFirst()) {
   using L = ShrinkCfg<RP>;
-  const int ks = shrink_ks(p, nt_lane, lane);
-  const ItemMap M = make_item_map(p.n_mod, nt_lane, ks, lane);
+  const int ks = W.ks;
+  const ItemMap& M = W.M;
   int li = 0;                                     // K-block sequence index over this CTA's items
   for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
     int local;
@@ -267,7 +282,7 @@ __device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, int 
 // Returns once every MMA is issued; on return the accumulator ring position is (*acc_slot, *acc_phase)
 // so the fused kernel can wait for the epilogue to drain it (shrink_drain_tmem).
 template <int RP>
-__device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int lane,
+__device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, const ShrinkWork& W, int lane,
                            int* acc_slot = nullptr, uint32_t* acc_phase = nullptr) {
   using L = ShrinkCfg<RP>;
   // N = 2 r_pad: the two halves' basis slabs are contiguous in the B stage, so ONE MMA per K step
@@ -275,8 +290,8 @@ __device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, int nt_la
   // second slab is stale and D1 is never read.  (A second MMA per K step measurably slowed the
   // single issuing thread.)
   constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * RP);
-  const int ks = shrink_ks(p, nt_lane, lane);
-  const ItemMap M = make_item_map(p.n_mod, nt_lane, ks, lane);
+  const int ks = W.ks;
+  const ItemMap& M = W.M;
   int stage = 0, slot = 0;
   uint32_t phase = 0, aphase = 0;
   for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
@@ -322,10 +337,10 @@ __device__ __forceinline__ void shrink_drain_tmem(const ShrinkRing& R, int slot,
 
 // ------------------------------------------------------------------ epilogue (warps 5-12)
 template <int RP>
-__device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, int nt_lane, int warp, int lane) {
+__device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, const ShrinkWork& W, int warp, int lane) {
   using L = ShrinkCfg<RP>;
-  const int ks = shrink_ks(p, nt_lane, lane);
-  const ItemMap M = make_item_map(p.n_mod, nt_lane, ks, lane);
+  const int ks = W.ks;
+  const ItemMap& M = W.M;
   const int ew = warp - kEpiWarp0;              // 0..7
   const int set = ew >> 2;
   const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
@@ -565,19 +580,24 @@ __global__ void __launch_bounds__(kApplyThreads, 1) shrink_sigma_kernel(const __
   // before griddep_wait once another kernel separates this one from cts_segment (meta_ready): the
   // predecessor only triggers its dependents after its own griddep_wait.
   int nt_lane = 0;
+  ShrinkWork W;
   ShrinkFirst first;
   if (p.meta_ready) {
     nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
-    if (warp < kProducerWarps) first = shrink_first_meta(p, nt_lane, lane);
+    W = shrink_work(p, nt_lane, lane);
+    if (warp < kProducerWarps) first = shrink_first_meta(p, W, lane);
   }
   griddep_wait();
   if (threadIdx.x == 0) griddep_launch_dependents();
-  if (!p.meta_ready) nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
+  if (!p.meta_ready) {
+    nt_lane = lane < p.n_mod ? *p.mod[lane].n_tiles : 0;
+    W = shrink_work(p, nt_lane, lane);
+  }
   if (threadIdx.x == 0) CTS_STAMP(1);
 
-  if (warp < kProducerWarps) shrink_producer<RP>(p, R, nt_lane, warp, lane, first);
-  else if (warp == kMmaWarp) shrink_mma<RP>(p, R, nt_lane, lane);
-  else shrink_epilogue<RP>(p, R, nt_lane, warp, lane);
+  if (warp < kProducerWarps) shrink_producer<RP>(p, R, W, warp, lane, first);
+  else if (warp == kMmaWarp) shrink_mma<RP>(p, R, W, lane);
+  else shrink_epilogue<RP>(p, R, W, warp, lane);
 
   __syncthreads();
   if (warp == kMmaWarp) tmem_dealloc<ShrinkCfg<RP>::kTmemCols>(R.tmem);

@@ -29,8 +29,8 @@ names = {0: "start", 1: "prologue+wait", 2: "shrink first TMA", 3: "shrink produ
          9: "expand producers done", 10: "expand epi done", 11: "end",
          12: "finisher: last arrival", 13: "finisher: partials summed", 14: "finisher: t stored",
          15: "finisher: flag published", 16: "shrink: first item mapped", 17: "shrink: expect_tx armed",
-         18: "shrink: first gathers issued", 19: "shrink: first acc ready", 20: "finisher: t[0:8] done",
-         21: "finisher: Sigma starts"}
+         18: "shrink: first gathers issued", 19: "shrink: first acc ready", 20: "-",
+         21: "-", 22: "-"}
 for grp in ([0, 1, 2], [3, 4]):
     for rep in range(3):
         big.zero_()
