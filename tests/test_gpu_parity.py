@@ -384,3 +384,52 @@ def test_tensor_parallel_dsplit(cts, G):
     torch.cuda.synchronize()
     for m in range(2):
         check_delta(ta, host_bits(ys[m]), f64s[m], xb, 2.0)
+
+
+# ---------------------------------------------------------------- uncompressed multi-LoRA bank
+@pytest.mark.parametrize("T,prefill", [(300, False), (700, True)])
+def test_uncompressed_multi_lora_bank(cts, T, prefill):
+    """the paper's baseline (N separate rank-16 LoRAs) through
+    the same kernels -- every adapter its own cluster, in_basis = A_i^T, out_basis = B_i,
+    Sigma_i = I -- must equal the plain LoRA update B_i (A_i x) (Sec. 3) of the oracle on
+    the same bf16 factors."""
+    from oracle import apply_lora_ref
+    N, d_in, d_out, r = 150, 256, 384, 16
+    Bs, As, _ = gen_loras("random", d_in, d_out, N, r, seed=5)
+    Ab = [bf16_round(A / np.sqrt(d_in)) for A in As]
+    Bb = [bf16_round(B / np.sqrt(r)) for B in Bs]
+    bits = {"in_basis": np.stack([A.T for A in Ab]), "out_basis": np.stack(Bb),
+            "sigma": bf16_round(np.broadcast_to(np.eye(r), (N, r, r)).copy()),
+            "cluster_of": np.arange(N, dtype=np.int32)}
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    ta = prefill_tokens(T, N, 21) if prefill else decode_tokens(T, N, 21, frac_none=0.05)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(T, d_in, 22))
+    got = bf16_to_f64(run_apply(cts, plan, 0, x, np.zeros((T, d_out), np.uint16), 2.0))
+    ref = apply_lora_ref(bf16_to_f64(x), ta, [bf16_to_f64(b) for b in Bb], [bf16_to_f64(a) for a in Ab], 2.0)
+    bound = ta >= 0
+    err = row_rel_err(got[bound], ref[bound])
+    assert err.max() <= PARITY_TOL, f"max per-row rel err {err.max():.3e}"
+    assert np.all(got[~bound] == 0)
+    plan.close()
+    bank.close()
+
+
+def test_diagonal_sigma_jd_diag(cts):
+    """JD-Diag (Sigma_i diagonal) runs the same apply: the r x r matvec of App D
+    reduces to an r-vector scale; checked against the oracle on a diagonal bank."""
+    bits, f64 = quantized_bank(512, 256, 40, 4, 16, seed=77)
+    d = bf16_round(np.stack([np.diag(np.diag(bf16_to_f64(s))) for s in bits["sigma"]]))
+    bits["sigma"] = d
+    f64["sigma"] = bf16_to_f64(d)
+    bank = make_bank(cts, [bits])
+    T = 257
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, 40, 31)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(T, 512, 32))
+    got = run_apply(cts, plan, 0, x, np.zeros((T, 256), np.uint16), 1.5)
+    check_delta(ta, got, f64, x, 1.5)
+    plan.close()
+    bank.close()

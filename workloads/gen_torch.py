@@ -43,3 +43,18 @@ def tokens_torch(T: int, N: int, seed: int, prefill: bool, device):
         out[pos:pos + L] = int(torch.randint(0, N, (1,), generator=g))
         pos += L
     return out.to(device)
+
+
+def lora_bank_torch(d_in: int, d_out: int, N: int, r: int, seed: int, device):
+    """The UNCOMPRESSED multi-LoRA collection in the same bank layout (the paper's baseline:
+    serving N separate rank-r LoRAs; Punica/vLLM multi-LoRA, App F):
+    every adapter is its own cluster, in_basis[i] = A_i^T [d_in][r], out_basis[i] = B_i [d_out][r],
+    sigma_i = I_r, cluster_of = identity, so the apply computes y += scale * B_i (A_i x).
+    A_i ~ N(0, 1/d_in), B_i ~ N(0, 1/r) (trained-LoRA-like magnitudes); bf16."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    A_t = (torch.randn(N, d_in, r, generator=g, device=device) / d_in ** 0.5).to(torch.bfloat16)
+    B = (torch.randn(N, d_out, r, generator=g, device=device) / r ** 0.5).to(torch.bfloat16)
+    sigma = torch.eye(r, device=device, dtype=torch.bfloat16).expand(N, r, r).contiguous()
+    cluster_of = torch.arange(N, dtype=torch.int32, device=device)
+    return {"in_basis": A_t, "out_basis": B, "sigma": sigma, "cluster_of": cluster_of}
