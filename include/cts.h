@@ -183,6 +183,24 @@ cts_status_t cts_shrink_partial_group(cts_plan_t plan, int32_t n, const int32_t*
 cts_status_t cts_expand_reduced_group(cts_plan_t plan, int32_t n, const int32_t* modules, const float* const* parts,
                                       void* const* ys, const int64_t* ld_y, cudaStream_t stream);
 
+/*
+ * Fused base + compressed-LoRA projection: for every token t of the batch
+ * segmented into `plan` (all T tokens, bound or not),
+ *     y[t] = bf16( W0 x[t] + scale * U_c Sigma_i V_c^T x[t] )        (Sec. 3 P:L107-109 with
+ *                                                                       Eq. 1)
+ * with the LoRA term omitted for tokens whose id is -1.  W0 = w0: device, bf16, [d_out][ld_w] row
+ * major (the nn.Linear weight layout: row o is output feature o), ld_w >= d_in.  x: [T][ld_x] bf16.
+ * y: [T][ld_y] bf16, OUTPUT ONLY (overwritten; unlike cts_apply it is not read).  Two launches:
+ * the shrink + Sigma kernel (t into the plan), then one persistent tcgen05 GEMM whose 128-row
+ * tiles are the cluster-sorted slots (and base-only tiles of the unbound tokens) and whose last
+ * pipeline stage adds t U_c^T into the same TMEM accumulator.  Requires r_pad == 16 (rank <= 16),
+ * d_out % 256 == 0 and d_in % 64 == 0 (else CTS_ERR_UNSUPPORTED); ld/alignment as cts_apply;
+ * CTS_ERR_INVALID_ARGUMENT if y overlaps x or w0.  A poisoned plan leaves y untouched.
+ * Stream-ordered; x, w0 and y must stay valid until the stream reaches the call.
+ */
+cts_status_t cts_project(cts_plan_t plan, int32_t module, const void* x, int64_t ld_x, const void* w0, int64_t ld_w,
+                         void* y, int64_t ld_y, float scale, cudaStream_t stream);
+
 /* Read the plan's device error word (call after synchronizing the stream that ran cts_segment).
  * *code = CTS_OK or CTS_ERR_INDEX_OUT_OF_RANGE; *first_bad_token = smallest offending t or -1. */
 cts_status_t cts_plan_error(cts_plan_t plan, int32_t* code, int32_t* first_bad_token);
@@ -194,7 +212,7 @@ const char* cts_status_string(cts_status_t status);
  * plans; launches recorded into a CUDA graph under stream capture count once, at capture).  The
  * difference across a call sequence is that sequence's kernel count: cts_segment = 1,
  * cts_apply / cts_apply_group = 1 (fused kernel; 2 with CTS_FUSED=0), cts_shrink* = cts_expand* = 1,
- * cts_expand_reduced_group = 2,
+ * cts_expand_reduced_group = 2, cts_project = 2,
  * cts_bank_load = 3 per module.  Never fails. */
 uint64_t cts_launch_count(void);
 

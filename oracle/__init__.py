@@ -10,11 +10,12 @@ something other than itself live in tests/test_oracle_*.py (see DESIGN.md "Oracl
 
 Parity status
   segment_ref, apply_ref, apply_dense_ref, apply_lora_ref  pinned (brute force, Prop. 1, invariants)
+  project_ref                                               pinned (brute-force loops; W0 = 0 / Sigma = 0 cases)
   jd_full, sigma_star, jd_objective                         pinned (closed forms, Thm 1, Eckart-Young)
   bank_params, usage_ratio, para_saved                      pinned (App F / Table H printed values)
   random-LoRA reconstruction values (App H)   parity unpinned (distribution unknown)
 """
-from .apply import segment_ref, apply_ref, apply_dense_ref, apply_lora_ref  # noqa: F401
+from .apply import segment_ref, apply_ref, apply_dense_ref, apply_lora_ref, project_ref  # noqa: F401
 from .jd import (  # noqa: F401
     lora_product,
     sigma_star,

@@ -86,3 +86,14 @@ def apply_lora_ref(x, token_adapter, Bs, As, scale=1.0):
         if i >= 0:
             dy[t] = scale * (Bs[i] @ (As[i] @ x[t]))
     return dy
+
+
+def project_ref(x, W0, token_adapter, cluster_of, in_basis, out_basis, sigma, scale=1.0):
+    """The LoRA'd projection (W0 + B_i A_i) x_t of Sec. 3 with the adapter replaced by
+    its compressed form: y_t = W0 x_t + scale * U_c Sigma_i V_c^T x_t (Eq. 1; clusters
+    P:L162-166); tokens with id -1 get the base projection only.  W0 is [d_out][d_in] (row o =
+    output feature o).  fp64; returns y."""
+    x = np.asarray(x, dtype=np.float64)
+    base = x @ np.asarray(W0, dtype=np.float64).T
+    dy, _ = apply_ref(x, token_adapter, cluster_of, in_basis, out_basis, sigma, scale)
+    return base + dy

@@ -6,6 +6,7 @@ from .api import (  # noqa: F401
     Plan,
     cts_apply,
     cts_apply_group,
+    cts_project,
     cts_expand_group,
     cts_shrink_group,
     cts_expand,

@@ -26,6 +26,7 @@ EXPORTS = (
     "cts_segment", "cts_segment_readback", "cts_apply", "cts_shrink", "cts_expand",
     "cts_apply_group", "cts_shrink_group", "cts_expand_group", "cts_plan_error", "cts_status_string",
     "cts_launch_count", "cts_plan_partial_elems", "cts_shrink_partial_group", "cts_expand_reduced_group",
+    "cts_project",
 )
 
 
@@ -92,6 +93,7 @@ def lib():
         "cts_plan_partial_elems": ([P, ctypes.POINTER(I64)], I32),
         "cts_shrink_partial_group": ([P, I32, VP, VP, VP, F, VP, P], I32),
         "cts_expand_reduced_group": ([P, I32, VP, VP, VP, VP, P], I32),
+        "cts_project": ([P, I32, VP, I64, VP, I64, VP, I64, F, P], I32),
     }
     for name, (argt, rest) in sig.items():
         f = getattr(L, name)

@@ -120,6 +120,18 @@ def cts_apply(plan, module, x, y, scale=1.0, stream=None):
                                        _stream_handle(stream)))
 
 
+def cts_project(plan, module, x, w0, y, scale=1.0, stream=None):
+    """Fused projection y[t] = W0 x[t] + scale * U_c Sigma_i V_c^T x[t] (y is overwritten; w0 is the
+    [d_out][d_in] nn.Linear weight).  bf16 CUDA tensors, 2-D, unit inner stride."""
+    for t, nm in ((x, "x"), (w0, "w0"), (y, "y")):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or t.dim() != 2 or t.stride(1) != 1:
+            raise TypeError(f"{nm} must be a 2-D bf16 CUDA tensor with unit inner stride")
+    check("cts_project", lib().cts_project(plan, int(module), ctypes.c_void_p(x.data_ptr()), x.stride(0),
+                                           ctypes.c_void_p(w0.data_ptr()), w0.stride(0),
+                                           ctypes.c_void_p(y.data_ptr()), y.stride(0), ctypes.c_float(scale),
+                                           _stream_handle(stream)))
+
+
 def cts_shrink(plan, module, x, scale=1.0, stream=None):
     """Kernel 1 only: t = scale * Sigma_i V_c^T x_t into the plan's scratch for `module`."""
     if x.dtype != torch.bfloat16 or not x.is_cuda or x.dim() != 2 or x.stride(1) != 1:
@@ -259,6 +271,9 @@ class Plan:
 
     def apply(self, module, x, y, scale=1.0, stream=None):
         cts_apply(self.handle, module, x, y, scale, stream)
+
+    def project(self, module, x, w0, y, scale=1.0, stream=None):
+        cts_project(self.handle, module, x, w0, y, scale, stream)
 
     def shrink(self, module, x, scale=1.0, stream=None):
         cts_shrink(self.handle, module, x, scale, stream)

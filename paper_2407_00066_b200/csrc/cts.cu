@@ -15,6 +15,7 @@
 #include "../../include/cts.h"
 #include "apply_fused.cuh"
 #include "expand.cuh"
+#include "proj_fused.cuh"
 #include "segment.cuh"
 #include "shrink_sigma.cuh"
 
@@ -58,6 +59,20 @@ bool make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, 
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 3-D tiled map (used for the fused projection's masked t halves: out-of-bounds boxes fill zeros)
+bool make_tmap3(CUtensorMap* m, const void* ptr, const uint64_t dims_in[3], const uint64_t strides_in[2],
+                const uint32_t box_in[3], CUtensorMapSwizzle sw) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {dims_in[0], dims_in[1], dims_in[2]};
+  cuuint64_t strides[2] = {strides_in[0], strides_in[1]};
+  cuuint32_t box[3] = {box_in[0], box_in[1], box_in[2]};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -139,6 +154,8 @@ struct cts_plan_s {
   int32_t* tile_rows;     // [n_maps][max_tiles*128]
   int32_t* tile_adapters; // [n_maps][max_tiles*128]
   int32_t* err;           // [2]
+  int32_t* unbound_rows;  // [T_max + 128] tokens with id -1 (fused projection)
+  int32_t* n_unbound;     // [1]
   __nv_bfloat16* tbuf;    // [n_modules][max_tiles*128][2*rp]  rank-r intermediate (t hi | t lo)
   CUtensorMap* d_tm_t;    // [n_modules] device copies
   float* ws;              // [kMaxGroup][ws_cap rows][rp]  split-K partials
@@ -464,6 +481,47 @@ cts_status_t do_fused(cts_plan_t p, int n, const int32_t* mods, const void* cons
                                         ldy, scale, s);
 }
 
+// fused base + LoRA projection (proj_fused.cuh): shrink + Sigma into the plan's t, then one GEMM
+cts_status_t launch_project(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, const void* w0, int64_t ld_w,
+                            void* y, int64_t ld_y, float scale, cudaStream_t stream) {
+  const cts_bank_t b = p->bank;
+  const Module& m = b->mods[module];
+  cts_status_t st = launch_shrink<16>(p, 1, &module, &x, &ld_x, scale, stream);
+  if (st != CTS_OK) return st;
+  static const cudaError_t attr = set_smem(proj_fused_kernel, ProjCfg::kBytes);
+  CTS_CUDA(attr);
+  ProjParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  if (!make_tmap(&prm.tm_x4, x, m.d_in, p->T, ld_x * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_tmap(&prm.tm_x8, x, m.d_in, p->T, ld_x * 2, 64, 8, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_tmap(&prm.tm_w, w0, m.d_in, m.d_out, ld_w * 2, 64, kProjBN, CU_TENSOR_MAP_SWIZZLE_128B))
+    return CTS_ERR_CUDA;
+  {
+    const uint64_t dims[3] = {uint64_t(2 * b->rp), 64, uint64_t(2 * p->max_tiles)};
+    const uint64_t strides[2] = {uint64_t(4 * b->rp), uint64_t(64 * 4 * b->rp)};
+    const uint32_t box[3] = {uint32_t(b->rp), 64, 1};
+    if (!make_tmap3(&prm.tm_t3, module_tbuf(p, module), dims, strides, box, CU_TENSOR_MAP_SWIZZLE_32B))
+      return CTS_ERR_CUDA;
+  }
+  prm.tm_out = b->d_tm_out + module;
+  const size_t mid = m.map_id;
+  prm.tiles = p->tiles + mid * p->max_tiles * 2;
+  prm.n_tiles = p->n_tiles + mid;
+  prm.tile_rows = p->tile_rows + mid * p->max_tiles * kTileM;
+  prm.unbound_rows = p->unbound_rows;
+  prm.n_unbound = p->n_unbound;
+  prm.y = static_cast<__nv_bfloat16*>(y);
+  prm.ld_y = ld_y;
+  prm.kblocks = m.d_in / kBK;
+  prm.nblk = m.d_out / kProjBN;
+  prm.d_out = m.d_out;
+  prm.meta_ready = next_meta_ready(p);
+  const int items = (p->max_tiles + (p->T + kTileM - 1) / kTileM) * prm.nblk;
+  CTS_CUDA(launch_pdl(proj_fused_kernel, std::min(sm_count(), std::max(items, 1)), kApplyThreads, ProjCfg::kBytes,
+                      stream, prm));
+  return CTS_OK;
+}
+
 bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   const uint8_t* x = static_cast<const uint8_t*>(a);
   const uint8_t* y = static_cast<const uint8_t*>(b);
@@ -640,6 +698,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   const size_t o_trows = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
   const size_t o_tads = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
   const size_t o_err = off; off = align_up(off + 16, 256);
+  const size_t o_unb = off; off = align_up(off + (size_t(T_max) + kTileM + 4) * 4, 256);
   const size_t o_cnt = off; off = align_up(off + size_t(kMaxGroup) * p->max_tiles * 4, 1024);
   const size_t o_rdy = off; off = align_up(off + size_t(kMaxGroup) * p->max_tiles * 4 + 16, 1024);
   const size_t o_tm = off; off = align_up(off + size_t(b->n_modules) * sizeof(CUtensorMap), 1024);
@@ -655,6 +714,8 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->tile_rows = reinterpret_cast<int32_t*>(base + o_trows);
   p->tile_adapters = reinterpret_cast<int32_t*>(base + o_tads);
   p->err = reinterpret_cast<int32_t*>(base + o_err);
+  p->n_unbound = reinterpret_cast<int32_t*>(base + o_unb);
+  p->unbound_rows = p->n_unbound + 4;
   p->counters = reinterpret_cast<int32_t*>(base + o_cnt);
   p->ready = reinterpret_cast<int32_t*>(base + o_rdy);
   p->exit_count = p->ready + size_t(kMaxGroup) * p->max_tiles;
@@ -662,7 +723,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->ws = reinterpret_cast<float*>(base + o_ws);
   p->tbuf = reinterpret_cast<__nv_bfloat16*>(base + o_t);
   const int32_t init_err[2] = {0, -1};
-  bool ok = cudaMemset(p->n_tiles, 0, nm * 4) == cudaSuccess &&
+  bool ok = cudaMemset(p->n_tiles, 0, nm * 4) == cudaSuccess && cudaMemset(p->n_unbound, 0, 16) == cudaSuccess &&
             cudaMemset(p->tiles, 0, nm * p->max_tiles * 32) == cudaSuccess &&
             cudaMemset(p->counters, 0, size_t(kMaxGroup) * p->max_tiles * 4) == cudaSuccess &&
             cudaMemset(p->ready, 0, size_t(kMaxGroup) * p->max_tiles * 4 + 16) == cudaSuccess &&
@@ -704,6 +765,9 @@ cts_status_t cts_segment(cts_plan_t p, const int32_t* token_adapter, int32_t T, 
   a.tile_rows = p->tile_rows;
   a.tile_adapters = p->tile_adapters;
   a.err = p->err;
+  a.unbound_rows = p->unbound_rows;
+  a.n_unbound = p->n_unbound;
+  a.n_maps = b->n_maps;
   a.T = T;
   a.T_max = p->T_max;
   a.N = b->N;
@@ -717,7 +781,7 @@ cts_status_t cts_segment(cts_plan_t p, const int32_t* token_adapter, int32_t T, 
   static const cudaError_t seg_attr = cudaFuncSetAttribute(
       segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (kSegWarps + 3) * 1024 * 4);
   CTS_CUDA(seg_attr);
-  CTS_CUDA(launch_pdl(segment_kernel, b->n_maps, kSegThreads, size_t(kSegWarps + 3) * b->C * 4, stream, a));
+  CTS_CUDA(launch_pdl(segment_kernel, b->n_maps + 1, kSegThreads, size_t(kSegWarps + 3) * b->C * 4, stream, a));
   p->T = T;
   p->launches_since_segment = 0;
   return CTS_OK;
@@ -832,6 +896,23 @@ cts_status_t cts_expand(cts_plan_t p, int32_t module, void* y, int64_t ld_y, cud
 cts_status_t cts_apply(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, void* y, int64_t ld_y, float scale,
                        cudaStream_t stream) {
   return cts_apply_group(p, 1, &module, &x, &ld_x, &y, &ld_y, scale, stream);
+}
+
+cts_status_t cts_project(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, const void* w0, int64_t ld_w,
+                         void* y, int64_t ld_y, float scale, cudaStream_t stream) {
+  if (!p || !x || !w0 || !y) return CTS_ERR_INVALID_ARGUMENT;
+  const cts_bank_t b = p->bank;
+  if (module < 0 || module >= b->n_modules) return CTS_ERR_SHAPE;
+  if (b->rp != 16) return CTS_ERR_UNSUPPORTED;
+  const Module& m = b->mods[module];
+  if (m.d_out % kProjBN || m.d_in % kBK) return CTS_ERR_UNSUPPORTED;
+  if (ld_x < m.d_in || ld_w < m.d_in || ld_y < m.d_out || (ld_x * 2) % 16 || (ld_w * 2) % 16 || (ld_y * 2) % 16 ||
+      !aligned16(x) || !aligned16(w0) || !aligned16(y))
+    return CTS_ERR_SHAPE;
+  const size_t nx = size_t(p->T) * ld_x * 2, nw = size_t(m.d_out) * ld_w * 2, ny = size_t(p->T) * ld_y * 2;
+  if (p->T > 0 && (overlaps(y, ny, x, nx) || overlaps(y, ny, w0, nw))) return CTS_ERR_INVALID_ARGUMENT;
+  if (p->T == 0) return CTS_OK;
+  return launch_project(p, module, x, ld_x, w0, ld_w, y, ld_y, scale, stream);
 }
 
 #ifdef CTS_TRACE

@@ -41,6 +41,9 @@ struct SegArgs {
   int32_t* tile_rows;            // [n_maps][max_tiles*128] token of each tile row (dup of last past len)
   int32_t* tile_adapters;        // [n_maps][max_tiles*128] adapter of that token
   int32_t* err;                  // [2] code, first bad token
+  int32_t* unbound_rows;         // [T_max + 128] tokens with id -1 in order, padded to a multiple of 128
+  int32_t* n_unbound;            // [1] (0 if the batch is invalid)
+  int n_maps;                    // CTAs 0..n_maps-1 segment one map each; CTA n_maps lists unbound tokens
   int T, T_max, N, C, max_tiles;
   int pack;                      // 1: pair <=64-token remainders into shared slots
 };
@@ -73,6 +76,31 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_sums, int& 
   return res;
 }
 
+// CTA n_maps: the stable list of UNBOUND tokens (id -1), for the fused projection (proj_fused.cuh),
+// which must still compute y = W0 x for them.  Chunks of 1024 tokens, block scan per chunk; the
+// list is padded with its last token to a multiple of 128 rows.
+__device__ void unbound_list(const SegArgs& a, int* warp_sums) {
+  __shared__ int s_bad_u;
+  if (threadIdx.x == 0) s_bad_u = 0;
+  __syncthreads();
+  int base = 0;
+  for (int t0 = 0; t0 < a.T; t0 += kSegThreads) {
+    const int t = t0 + threadIdx.x;
+    const int id = t < a.T ? a.token_adapter[t] : 0;
+    if (t < a.T && (id < -1 || id >= a.N)) s_bad_u = 1;
+    const int f = (t < a.T && id == -1) ? 1 : 0;
+    int total;
+    const int pos = block_exclusive_scan(f, warp_sums, total);
+    if (f) a.unbound_rows[base + pos] = t;
+    base += total;
+  }
+  __syncthreads();
+  const int n = s_bad_u ? 0 : base;
+  const int padded = (n + kTileM - 1) / kTileM * kTileM;
+  for (int i = n + threadIdx.x; i < padded; i += kSegThreads) a.unbound_rows[i] = a.unbound_rows[n - 1];
+  if (threadIdx.x == 0) *a.n_unbound = n;
+}
+
 __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
   extern __shared__ int seg_smem[];
   int* hist = seg_smem;                            // [kSegWarps][C]
@@ -91,6 +119,10 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
 
   griddep_wait();                                   // previous step's applies still read the plan
   griddep_launch_dependents();
+  if (map_id == a.n_maps) {
+    unbound_list(a, warp_sums);
+    return;
+  }
   if (threadIdx.x == 0) s_bad = 0x7fffffff;
   for (int i = threadIdx.x; i < kSegWarps * a.C; i += kSegThreads) hist[i] = 0;
   __syncthreads();

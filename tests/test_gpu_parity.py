@@ -433,3 +433,50 @@ def test_diagonal_sigma_jd_diag(cts):
     check_delta(ta, got, f64, x, 1.5)
     plan.close()
     bank.close()
+
+
+# ---------------------------------------------------------------- fused base + LoRA projection
+@pytest.mark.parametrize("d_in,d_out,T,prefill,frac_none", [(512, 512, 300, False, 0.1), (256, 768, 700, True, 0.0),
+                                                            (1024, 256, 130, False, 1.0), (256, 512, 5, False, 0.0)])
+def test_fused_projection(cts, d_in, d_out, T, prefill, frac_none):
+    """cts_project: y = W0 x + scale U_c Sigma_i V_c^T x for EVERY token
+    (unbound ones get W0 x) vs the fp64 oracle on the same bf16 bits; packed and whole slots,
+    several 256-column blocks, all-unbound and tiny batches."""
+    from oracle import project_ref
+    N, C = 40, 5
+    bits, f64 = quantized_bank(d_in, d_out, N, C, 16, seed=d_in + T)
+    g = np.random.default_rng(T)
+    w_bits = bf16_round(g.standard_normal((d_out, d_in)) / np.sqrt(d_in))
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    if frac_none >= 1.0:
+        ta = np.full(T, -1, np.int32)
+    else:
+        ta = prefill_tokens(T, N, 41) if prefill else decode_tokens(T, N, 41, frac_none=frac_none)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(T, d_in, 42))
+    y = torch.full((T, d_out), float("nan"), dtype=torch.bfloat16, device="cuda")
+    plan.project(0, dev_bf16(x), dev_bf16(w_bits), y, 2.0)
+    torch.cuda.synchronize()
+    got = bf16_to_f64(host_bits(y))
+    ref = project_ref(bf16_to_f64(x), bf16_to_f64(w_bits), ta, f64["cluster_of"], f64["in_basis"], f64["out_basis"],
+                      f64["sigma"], 2.0)
+    assert np.all(np.isfinite(got)), "some rows of y were not written"
+    err = row_rel_err(got, ref)
+    assert err.max() <= PARITY_TOL, f"max per-row rel err {err.max():.3e}"
+    plan.close()
+    bank.close()
+
+
+def test_fused_projection_unsupported_rank(cts):
+    bits, _ = quantized_bank(256, 256, 8, 2, 24, seed=1)          # r = 24 pads to 32: not supported
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, 16)
+    plan.segment(torch.zeros(16, dtype=torch.int32, device="cuda"))
+    x = torch.zeros(16, 256, dtype=torch.bfloat16, device="cuda")
+    w = torch.zeros(256, 256, dtype=torch.bfloat16, device="cuda")
+    y = torch.zeros(16, 256, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(cts.CtsError):
+        plan.project(0, x, w, y, 1.0)
+    plan.close()
+    bank.close()

@@ -134,3 +134,27 @@ def test_clustered_bank_from_jd_matches_per_cluster_loras():
     dy, _ = apply_ref(x, ta, bank["cluster_of"], bank["in_basis"], bank["out_basis"], bank["sigma"])
     ref = apply_lora_ref(x, ta, Bs, As)
     assert np.max(np.abs(dy - ref)) <= 1e-11 * np.max(np.abs(ref))
+
+
+def test_project_ref_brute_force_and_special_cases():
+    """project_ref = W0 x + Delta y (Sec. 3 P:L107-109 with Eq. 1): a scalar-loop W0 x plus the
+    brute-force apply on tiny inputs; W0 = 0 reduces it to apply_ref, Sigma = 0 to the plain
+    projection, and id -1 rows get the base projection only."""
+    from oracle import project_ref
+    T, d_in, d_out, N, C, r = 6, 5, 4, 3, 2, 2
+    b = _bank(d_in, d_out, N, C, r, seed=3)
+    g = np.random.default_rng(4)
+    x = g.standard_normal((T, d_in))
+    W0 = g.standard_normal((d_out, d_in))
+    ta = np.array([0, 2, -1, 1, 0, -1])
+    want = np.array([[sum(W0[o, j] * x[t, j] for j in range(d_in)) for o in range(d_out)] for t in range(T)])
+    want += brute_apply(x, ta, b["cluster_of"], b["in_basis"], b["out_basis"], b["sigma"], 1.5)
+    got = project_ref(x, W0, ta, b["cluster_of"], b["in_basis"], b["out_basis"], b["sigma"], 1.5)
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+    dy, _ = apply_ref(x, ta, b["cluster_of"], b["in_basis"], b["out_basis"], b["sigma"], 1.5)
+    assert np.allclose(project_ref(x, np.zeros_like(W0), ta, b["cluster_of"], b["in_basis"], b["out_basis"],
+                                   b["sigma"], 1.5), dy, rtol=0, atol=1e-14)
+    plain = project_ref(x, W0, ta, b["cluster_of"], b["in_basis"], b["out_basis"], np.zeros_like(b["sigma"]), 1.5)
+    assert np.allclose(plain, want - brute_apply(x, ta, b["cluster_of"], b["in_basis"], b["out_basis"],
+                                                 b["sigma"], 1.5), rtol=1e-12, atol=1e-12)
+    assert np.array_equal(got[ta < 0], plain[ta < 0])
