@@ -494,6 +494,8 @@ cts_status_t launch_project(cts_plan_t p, int32_t module, const void* x, int64_t
   std::memset(&prm, 0, sizeof(prm));
   if (!make_tmap(&prm.tm_x4, x, m.d_in, p->T, ld_x * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_tmap(&prm.tm_x8, x, m.d_in, p->T, ld_x * 2, 64, 8, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_tmap(&prm.tm_x32, x, m.d_in, p->T, ld_x * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_tmap(&prm.tm_x128, x, m.d_in, p->T, ld_x * 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_tmap(&prm.tm_w, w0, m.d_in, m.d_out, ld_w * 2, 64, kProjBN, CU_TENSOR_MAP_SWIZZLE_128B))
     return CTS_ERR_CUDA;
   {

@@ -15,12 +15,12 @@
 // applies the right basis to every row.  The epilogue rounds D to bf16 and stores the valid rows
 // to y in token order (register-direct, thread = token row).
 //
-// A operand: the slot's token rows of x.  Loading them with tile::gather4 (4 rows per instruction)
-// ran the GEMM ~25% below 2-D tile loads of the same bytes (profiles/microbench/proj_speed.py), so an
-// 8-row group whose tokens are consecutive (at prefill a request is a contiguous run of 128-256
-// tokens with one adapter, so nearly all groups are) is loaded as ONE {64 x 8} box; other groups fall
-// back to gather4.  (A slot-ordered copy of x, loaded as {64 x 128} tiles, measured the same overall:
-// the copy costs an extra pass over x.)
+// A operand: the slot's token rows of x.  The TMA unit takes one instruction at a time, and 32
+// tile::gather4 (4 rows each) per K block kept the MMA ~30% idle (ncu: tensor pipe 66% active,
+// L2 at 51%), so runs of consecutive tokens -- at prefill a request is a contiguous run of 128-256
+// tokens with one adapter -- are loaded as the largest aligned {64 x 128 | 32 | 8} box; only groups
+// at run boundaries fall back to gather4.  (A slot-ordered copy of x, loaded as {64 x 128} tiles,
+// measured no better: the copy costs an extra pass over x.)
 // Persistent, one CTA per SM, 13 warps: 4 TMA producer warps (x rows as above and W0 tiles
 // {64 x 256} by 2-D TMA, 4-stage ring of 48 KB), 1 MMA warp (one elected
 // lane, M=128 N=256 K=16), 8 epilogue warps (set s stores columns [128 s, 128 s + 128)).  Two TMEM
@@ -55,6 +55,8 @@ struct ProjParams {
   int meta_ready;
   CUtensorMap tm_x4;                     // x [T][d_in], box {64, 1}, 128B swizzle (gather4)
   CUtensorMap tm_x8;                     // x [T][d_in], box {64, 8}, 128B swizzle (runs of 8 tokens)
+  CUtensorMap tm_x32;                    // x [T][d_in], box {64, 32} (runs of 32 tokens)
+  CUtensorMap tm_x128;                   // x [T][d_in], box {64, 128} (a slot that is one run)
 };
 
 struct ProjCfg {
@@ -107,6 +109,8 @@ __global__ void __launch_bounds__(kApplyThreads, 1) proj_fused_kernel(const __gr
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&p.tm_x4);
     tma_prefetch_desc(&p.tm_x8);
+    tma_prefetch_desc(&p.tm_x32);
+    tma_prefetch_desc(&p.tm_x128);
     tma_prefetch_desc(&p.tm_w);
     tma_prefetch_desc(&p.tm_t3);
     tma_prefetch_desc(p.tm_out);
@@ -144,10 +148,26 @@ __global__ void __launch_bounds__(kApplyThreads, 1) proj_fused_kernel(const __gr
       const int4 r4 = *reinterpret_cast<const int4*>((lora ? p.tile_rows : p.unbound_rows) + slot * kTileM + 4 * lane);
       const int l0 = (t0.z + 3) & ~3, l1 = (t1.z + 3) & ~3;
       const bool gvalid = t1.z > 0 ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
+      // The fewest TMA instructions that load the slot's valid rows: the TMA unit issues them one at
+      // a time, so 32 gather4 per K block starve the MMA; contiguous token runs use the largest
+      // aligned box (128, 32 or 8 rows), the rest gather4.  Lane 4j's 4-row group starts row 4j.
+      // run[j]: the 4 rows of group j are consecutive tokens continuing group j-1 (j > 0).
       const bool run4 = gvalid && r4.y == r4.x + 1 && r4.z == r4.x + 2 && r4.w == r4.x + 3;
-      const int nx = __shfl_xor_sync(0xffffffffu, r4.x, 1);
-      const bool nrun = __shfl_xor_sync(0xffffffffu, run4, 1);
-      const bool box8 = run4 && nrun && ((lane & 1) ? nx + 4 == r4.x : r4.x + 4 == nx);   // pair agrees
+      const int prev_w = __shfl_up_sync(0xffffffffu, r4.w, 1);
+      const bool cont = run4 && (lane == 0 || prev_w + 1 == r4.x);     // continues the previous group
+      const uint32_t mrun = __ballot_sync(0xffffffffu, run4), mcont = __ballot_sync(0xffffffffu, cont);
+      // a box of 4b groups starting at group j is one run iff run4 for all and cont for j+1..j+b-1
+      auto is_box = [&](int j, int b) {
+        const uint32_t all = (b == 32 ? 0xffffffffu : ((1u << b) - 1u)) << j;
+        const uint32_t inner = all & ~(1u << j);
+        return (mrun & all) == all && (mcont & inner) == inner;
+      };
+      const bool box128 = is_box(0, 32);
+      const bool box32 = !box128 && (lane & 7) == 0 && is_box(lane, 8);       // quarter lane/8
+      const bool in32 = !box128 && is_box(lane & ~7, 8);                      // my quarter is one box
+      const bool box8 = !box128 && !in32 && (lane & 1) == 0 && is_box(lane, 2);
+      const bool in8 = box128 || in32 || is_box(lane & ~1, 2);
+      const bool g4 = gvalid && !in8;                                          // gather4 fallback
       const uint32_t abytes = static_cast<uint32_t>(__popc(__ballot_sync(0xffffffffu, gvalid)) * 512);
       const int steps = p.kblocks + (lora ? 1 : 0);    // K blocks (+ the LoRA stage)
       for (int k = 0; k < steps; ++k, ++li) {
@@ -163,11 +183,10 @@ __global__ void __launch_bounds__(kApplyThreads, 1) proj_fused_kernel(const __gr
             tma_load_2d(sB, &p.tm_w, &full[stage], k * kBK, nb * kProjBN);
           }
           __syncwarp();
-          if (box8) {
-            if ((lane & 1) == 0) tma_load_2d(sA + lane * 512, &p.tm_x8, &full[stage], k * kBK, r4.x);
-          } else if (gvalid) {
-            tma_gather4(sA + lane * 512, &p.tm_x4, &full[stage], k * kBK, r4.x, r4.y, r4.z, r4.w);
-          }
+          if (box128 && lane == 0) tma_load_2d(sA, &p.tm_x128, &full[stage], k * kBK, r4.x);
+          if (box32) tma_load_2d(sA + lane * 512, &p.tm_x32, &full[stage], k * kBK, r4.x);
+          if (box8) tma_load_2d(sA + lane * 512, &p.tm_x8, &full[stage], k * kBK, r4.x);
+          if (g4) tma_gather4(sA + lane * 512, &p.tm_x4, &full[stage], k * kBK, r4.x, r4.y, r4.z, r4.w);
         } else if (lane == 0) {
           // LoRA stage: A = [hi0 | lo0 | hi1 | lo1], each 128 rows with the other half's rows zero
           // (out-of-bounds boxes fill zeros); B = [U_c0 block | U_c1 block]
