@@ -295,7 +295,10 @@ cts_status_t fill_shrink(cts_plan_t p, int n, const int32_t* modules, const void
   for (int i = 0; i < n; ++i) {
     const Module& m = b->mods[modules[i]];
     ShrinkMod& sm = prm.mod[i];
-    if (!make_tmap(&sm.tm_x, xs[i], m.d_in, T, ld_x[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
+    if (!make_tmap(&sm.tm_x, xs[i], m.d_in, T, ld_x[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap(&sm.tm_x8, xs[i], m.d_in, T, ld_x[i] * 2, 64, 8, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap(&sm.tm_x32, xs[i], m.d_in, T, ld_x[i] * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+      return CTS_ERR_CUDA;
     sm.tm_in = b->d_tm_in + modules[i];
     const size_t mid = m.map_id;
     sm.tiles = p->tiles + mid * p->max_tiles * 2;
@@ -326,7 +329,10 @@ cts_status_t fill_expand(cts_plan_t p, int n, const int32_t* modules, void* cons
   for (int i = 0; i < n; ++i) {
     const Module& m = b->mods[modules[i]];
     ExpandMod& em = prm.mod[i];
-    if (!make_tmap(&em.tm_y, ys[i], m.d_out, T, ld_y[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B)) return CTS_ERR_CUDA;
+    if (!make_tmap(&em.tm_y, ys[i], m.d_out, T, ld_y[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap(&em.tm_y8, ys[i], m.d_out, T, ld_y[i] * 2, 64, 8, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap(&em.tm_y32, ys[i], m.d_out, T, ld_y[i] * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+      return CTS_ERR_CUDA;
     em.tm_t = p->d_tm_t + modules[i];
     em.tm_out = b->d_tm_out + modules[i];
     const size_t mid = m.map_id;

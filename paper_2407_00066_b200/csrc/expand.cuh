@@ -39,6 +39,9 @@ constexpr int kExpandThreads = kApplyThreads;
 constexpr int kBN = 128;                 // d_out columns per work item
 constexpr int kExpandAccSlots = 2;       // 2 x (D0 | D1) x 128 fp32 columns = all of TMEM
 constexpr int kStoreScatter = 0, kStoreDirect = 1, kStoreCoalesced = 2;   // expand epilogue store paths
+#ifndef CTS_EXPAND_BOXES
+#define CTS_EXPAND_BOXES 1   // runs of consecutive tokens as box loads / stores (row_boxes)
+#endif
 // Epilogue work split.  kEpiSplit: BOTH epilogue sets work on every item, set s on 64-column
 // segment s (the two warps of a TMEM lane quarter split the columns), so an item's accumulator
 // and stage are released after half the epilogue latency.  Otherwise the sets alternate items.
@@ -50,6 +53,8 @@ constexpr int kEpiArrivals = kEpiSplit ? 4 * kEpiSets : 4;   // arrivals per ite
 
 struct alignas(64) ExpandMod {
   CUtensorMap tm_y;                      // y [T][d_out], box {64, 1}, 128B swizzle (per call)
+  CUtensorMap tm_y8;                     // y, box {64, 8}  (runs of consecutive tokens, row_boxes)
+  CUtensorMap tm_y32;                    // y, box {64, 32}
   const CUtensorMap* tm_t;               // tbuf [max_tiles*128][2*rp], box {rp, 128} (plan, global mem)
   const CUtensorMap* tm_out;             // out_basis [C*d_out][rp], box {rp, 64} (bank, global mem)
   const int4* tiles;                     // [slot][2]: (cluster, start, len, -) per 64-row half
@@ -195,11 +200,17 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
       }
     }
     __syncwarp();
-    if (gvalid) {
+    {
+      RowBoxes rb = row_boxes(r4, gvalid, lane);
+      if (!CTS_EXPAND_BOXES) rb = RowBoxes{false, false, gvalid};
 #pragma unroll
-      for (int s = 0; s < L::kSeg; ++s)
-        tma_gather4(stage_y<RP>(R, stage) + s * L::kY + lane * 512, &m.tm_y, &R.full[stage], nb * kBN + s * 64, r4.x,
-                    r4.y, r4.z, r4.w);
+      for (int s = 0; s < L::kSeg; ++s) {
+        uint8_t* dst = stage_y<RP>(R, stage) + s * L::kY + lane * 512;
+        const int c0 = nb * kBN + s * 64;
+        if (rb.box32) tma_load_2d(dst, &m.tm_y32, &R.full[stage], c0, r4.x);
+        if (rb.box8) tma_load_2d(dst, &m.tm_y8, &R.full[stage], c0, r4.x);
+        if (rb.g4) tma_gather4(dst, &m.tm_y, &R.full[stage], c0, r4.x, r4.y, r4.z, r4.w);
+      }
     }
     if (lane == 0) {
       if (poll_late) {                            // fused kernel: t of this slot published?
@@ -337,11 +348,23 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
       // this warp's 8 four-row groups: lane -> (group, segment); TMA scatter of the rows
       fence_proxy_async_smem();
       __syncwarp();
+      // lane l plans 4-row group l of the slot (row_boxes), then this warp stores its quarter's
+      // 8 groups (lane -> (group, segment)) as 32-row / 8-row boxes or scatter4
+      const int4 rl = *reinterpret_cast<const int4*>(stage_rows<RP>(R, stage) + 4 * lane);
+      RowBoxes rb = row_boxes(rl, 4 * lane < len4 && (lane >> 3) == quarter, lane);
+      if (!CTS_EXPAND_BOXES) rb = RowBoxes{false, false, 4 * lane < len4 && (lane >> 3) == quarter};
+      const uint32_t m32 = __ballot_sync(0xffffffffu, rb.box32), m8 = __ballot_sync(0xffffffffu, rb.box8);
+      const uint32_t mg4 = __ballot_sync(0xffffffffu, rb.g4);
       const int grp = quarter * 8 + (lane & 7), seg = seg0 + (lane >> 3);
-      if (grp * 4 < len4 && seg < seg1) {
+      if (seg < seg1) {
         const int4 r4 = *reinterpret_cast<const int4*>(stage_rows<RP>(R, stage) + 4 * grp);
-        tma_scatter4(&p.mod[info.x].tm_y, ys + seg * L::kY + grp * 512, info.z * kBN + seg * 64, r4.x, r4.y, r4.z,
-                     r4.w);
+        const CUtensorMap* tm = nullptr;
+        if (m32 >> grp & 1) tm = &p.mod[info.x].tm_y32;
+        else if (m8 >> grp & 1) tm = &p.mod[info.x].tm_y8;
+        if (tm) tma_store_2d(tm, ys + seg * L::kY + grp * 512, info.z * kBN + seg * 64, r4.x);
+        else if (mg4 >> grp & 1)
+          tma_scatter4(&p.mod[info.x].tm_y, ys + seg * L::kY + grp * 512, info.z * kBN + seg * 64, r4.x, r4.y, r4.z,
+                       r4.w);
       }
       bulk_commit();
       bulk_wait_read<0>();                      // the scatter has read this warp's rows out of the stage

@@ -57,6 +57,8 @@ constexpr int kShrinkAccSlots = 4;
 
 struct alignas(64) ShrinkMod {
   CUtensorMap tm_x;                     // x [T][d_in], box {64, 1}, 128B swizzle (per call)
+  CUtensorMap tm_x8;                    // x, box {64, 8}  (runs of consecutive tokens, row_boxes)
+  CUtensorMap tm_x32;                   // x, box {64, 32}
   const CUtensorMap* tm_in;             // in_basis [C*rp][d_in], box {64, rp} (bank, global mem)
   const int4* tiles;                    // [slot][2]: (cluster, start, len, -) per 64-row half
   const int32_t* n_tiles;               // real slot count of this module's map
@@ -252,6 +254,7 @@ __device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, cons
     const int l0 = (t0.z + 3) & ~3, l1 = (t1.z + 3) & ~3;
     const bool gvalid = shared ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
     const int ngroups = (l0 + l1) >> 2;
+    const RowBoxes rb = row_boxes(r4, gvalid, lane);
     const int kb0 = kc * m.kblocks / ks, kb1 = (kc + 1) * m.kblocks / ks;
     const uint32_t bbytes = static_cast<uint32_t>((shared ? 2 : 1) * L::kB1);
     const uint32_t bytes = static_cast<uint32_t>(ngroups * 512) + bbytes;
@@ -265,9 +268,9 @@ __device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, cons
       if (li == 0 && lane == 0) CTS_STAMP(17);          // expect_tx armed
       __syncwarp();
       uint8_t* dA = R.sA + stage * L::kA;
-      if (gvalid) {
-        tma_gather4(dA + lane * 512, &m.tm_x, &R.full[stage], kb * kBK, r4.x, r4.y, r4.z, r4.w);
-      }
+      if (rb.box32) tma_load_2d(dA + lane * 512, &m.tm_x32, &R.full[stage], kb * kBK, r4.x);
+      if (rb.box8) tma_load_2d(dA + lane * 512, &m.tm_x8, &R.full[stage], kb * kBK, r4.x);
+      if (rb.g4) tma_gather4(dA + lane * 512, &m.tm_x, &R.full[stage], kb * kBK, r4.x, r4.y, r4.z, r4.w);
       if (li == 0 && lane == 0) CTS_STAMP(18);          // first x gathers issued
       if (lane == 0) {
         tma_load_2d(R.sB + stage * L::kB, m.tm_in, &R.full[stage], kb * kBK, t0.x * RP);

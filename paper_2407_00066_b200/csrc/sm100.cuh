@@ -74,6 +74,13 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uin
       "r"(r3)
       : "memory");
 }
+// 2-D tile store from shared memory; bulk-group completion.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
 // Scatter four rows from shared memory (inverse of gather4); bulk-group completion.
 __device__ __forceinline__ void tma_scatter4(const CUtensorMap* m, const void* src, int c0, int r0,
                                              int r1, int r2, int r3) {
@@ -95,6 +102,35 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 // Make generic-proxy shared-memory writes visible to the async (TMA) proxy.
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ row boxes
+// A 128-row slot is moved by 32 lanes, lane l owning rows 4l..4l+3 (tokens r4, valid = gvalid).
+// The TMA unit takes one instruction at a time, so runs of CONSECUTIVE tokens (at prefill a request
+// is a contiguous run of 128-256 tokens with one adapter) are moved as the largest aligned box --
+// 32 rows (issued by lane 8q for quarter q) or 8 rows (even lane 2g) -- and only the 4-row groups
+// at run boundaries as gather4 / scatter4.  Warp-collective; every lane gets its own role.
+struct RowBoxes {
+  bool box32, box8, g4;
+};
+
+__device__ __forceinline__ RowBoxes row_boxes(const int4& r4, bool gvalid, int lane) {
+  const bool run4 = gvalid && r4.y == r4.x + 1 && r4.z == r4.x + 2 && r4.w == r4.x + 3;
+  const int prev_w = __shfl_up_sync(0xffffffffu, r4.w, 1);
+  const bool cont = run4 && (lane == 0 || prev_w + 1 == r4.x);   // continues the previous group
+  const uint32_t mrun = __ballot_sync(0xffffffffu, run4), mcont = __ballot_sync(0xffffffffu, cont);
+  auto is_box = [&](int j, int b) {              // groups j .. j+b-1 form one run of tokens
+    const uint32_t all = ((1u << b) - 1u) << j;
+    const uint32_t inner = all & ~(1u << j);
+    return (mrun & all) == all && (mcont & inner) == inner;
+  };
+  RowBoxes rb;
+  const bool in32 = is_box(lane & ~7, 8);
+  rb.box32 = in32 && (lane & 7) == 0;
+  const bool in8 = in32 || is_box(lane & ~1, 2);
+  rb.box8 = !in32 && in8 && (lane & 1) == 0;
+  rb.g4 = gvalid && !in8;
+  return rb;
 }
 
 // ------------------------------------------------------------------ tcgen05
