@@ -36,8 +36,11 @@
 namespace cts {
 
 constexpr int kExpandThreads = kApplyThreads;
-constexpr int kBN = 128;                 // d_out columns per work item
-constexpr int kExpandAccSlots = 2;       // 2 x (D0 | D1) x 128 fp32 columns = all of TMEM
+#ifndef CTS_EXPAND_BN
+#define CTS_EXPAND_BN 128
+#endif
+constexpr int kBN = CTS_EXPAND_BN;       // d_out columns per work item
+constexpr int kExpandAccSlots = 512 / (2 * kBN);   // (D0 | D1) x kBN fp32 columns each: all of TMEM
 constexpr int kStoreScatter = 0, kStoreDirect = 1, kStoreCoalesced = 2;   // expand epilogue store paths
 #ifndef CTS_EXPAND_BOXES
 #define CTS_EXPAND_BOXES 1   // runs of consecutive tokens as box loads / stores (row_boxes)
@@ -46,7 +49,7 @@ constexpr int kStoreScatter = 0, kStoreDirect = 1, kStoreCoalesced = 2;   // exp
 // segment s (the two warps of a TMEM lane quarter split the columns), so an item's accumulator
 // and stage are released after half the epilogue latency.  Otherwise the sets alternate items.
 #ifndef CTS_EPI_SPLIT
-#define CTS_EPI_SPLIT 1
+#define CTS_EPI_SPLIT (CTS_EXPAND_BN == 128)
 #endif
 constexpr bool kEpiSplit = CTS_EPI_SPLIT != 0;
 constexpr int kEpiArrivals = kEpiSplit ? 4 * kEpiSets : 4;   // arrivals per item on acc_empty / empty
