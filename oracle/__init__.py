@@ -12,6 +12,8 @@ Parity status
   segment_ref, apply_ref, apply_dense_ref, apply_lora_ref  pinned (brute force, Prop. 1, invariants)
   project_ref                                               pinned (brute-force loops; W0 = 0 / Sigma = 0 cases)
   jd_full, sigma_star, jd_objective                         pinned (closed forms, Thm 1, Eckart-Young)
+  jd_eigen_iteration, orthogonalize (App A.2)               pinned (fixed point at the App A.1 optimum,
+                                                            n = 1 -> SVD subspaces, exact span, QR)
   bank_params, usage_ratio, para_saved                      pinned (App F / Table H printed values)
   random-LoRA reconstruction values (App H)   parity unpinned (distribution unknown)
 """
@@ -24,5 +26,7 @@ from .jd import (  # noqa: F401
     jd_objective,
     mean_relative_error,
     svd_truncate,
+    orthogonalize,
+    jd_eigen_iteration,
 )
 from .accounting import bank_params, baseline_params, usage_ratio, para_saved  # noqa: F401

@@ -199,3 +199,41 @@ def svd_truncate(B, A, r: int):
     """SVD_r(B_i A_i) = U_i Sigma_i V_i^T (Eq. 4): the k = n extreme of clustering."""
     u, s, vt = np.linalg.svd(np.asarray(B) @ np.asarray(A), full_matrices=False)
     return u[:, :r], np.diag(s[:r]), vt[:r].T
+
+
+def orthogonalize(X) -> np.ndarray:
+    """Q of the reduced QR of X with diag(R) > 0 (the unique orthonormal basis whose R has a positive
+    diagonal) -- the `orthogonalize` of App A.2 ("e.g. by using the Q part of the
+    reduced-size QR factorization")."""
+    Q, R = np.linalg.qr(np.asarray(X, dtype=np.float64))
+    s = np.sign(np.diag(R))
+    s[s == 0] = 1.0
+    return Q * s
+
+
+def jd_eigen_iteration(Bs, As, U0, V0, iters: int):
+    """App A.2 "Additional Eigenvalue Iteration Algorithm", the GPU-oriented
+    alternative to App A.1 Case 1, step by step and parenthesized as the paper writes it:
+        U0^(k+1) <- sum_i B_i (A_i V^(k)) ((V^(k))^T A_i^T) (B_i^T U^(k))
+        V0^(k+1) <- sum_i A_i^T (B_i^T U^(k)) ((U^(k))^T B_i) (A_i V^(k))
+        U^(k+1) <- orthogonalize(U0^(k+1)),  V^(k+1) <- orthogonalize(V0^(k+1))
+    (both updates use the k-th iterates).  U0, V0 (initial bases, d_out x r / d_in x r) are
+    INPUTS: the paper does not fix the initialization.  Sigma_i = U^T B_i A_i V (Eq. sigmastar,
+    P:L452) of the final iterate, as (B_i^T U)^T (A_i V).  No normalization (the caller's choice,
+    Sec. 6.1).  Returns dict(U, V, sigma, captured_trace = sum_i ||Sigma_i||_F^2 per iterate)."""
+    Bs = [np.asarray(B, dtype=np.float64) for B in Bs]
+    As = [np.asarray(A, dtype=np.float64) for A in As]
+    U = np.asarray(U0, dtype=np.float64)
+    V = np.asarray(V0, dtype=np.float64)
+
+    def captured(U, V):
+        return float(sum(np.sum(((B.T @ U).T @ (A @ V)) ** 2) for B, A in zip(Bs, As)))
+
+    trace = [captured(U, V)]
+    for _ in range(iters):
+        Un = sum(B @ ((A @ V) @ ((V.T @ A.T) @ (B.T @ U))) for B, A in zip(Bs, As))
+        Vn = sum(A.T @ ((B.T @ U) @ ((U.T @ B) @ (A @ V))) for B, A in zip(Bs, As))
+        U, V = orthogonalize(Un), orthogonalize(Vn)
+        trace.append(captured(U, V))
+    sigma = np.stack([(B.T @ U).T @ (A @ V) for B, A in zip(Bs, As)])
+    return {"U": U, "V": V, "sigma": sigma, "captured_trace": trace}

@@ -136,3 +136,56 @@ def test_convergence_criterion_stops_early():
     Bs, As, _ = gen_loras("trained_like", 30, 30, 6, 2, 3, n_families=1, noise=0.05)
     res = jd_full(Bs, As, 4, iters=50, tol=1e-3)
     assert 1 <= res["iters"] < 50
+
+
+# ---------------------------------------------------------------- App A.2 eigenvalue iteration
+def test_orthogonalize_is_qr_with_positive_diagonal():
+    from oracle import orthogonalize
+    X = np.random.default_rng(0).standard_normal((40, 6))
+    Q = orthogonalize(X)
+    assert np.allclose(Q.T @ Q, np.eye(6), atol=1e-12)
+    R = Q.T @ X                                        # upper triangular with positive diagonal
+    assert np.allclose(np.tril(R, -1), 0, atol=1e-12) and np.all(np.diag(R) > 0)
+    assert np.allclose(Q @ R, X, atol=1e-12)
+
+
+def test_eigen_iteration_fixed_point_at_alternating_optimum():
+    """At a converged App A.1 solution U spans the top-r eigenvectors of M (M U = U Lambda), so
+    U0^(k+1) = U Lambda and orthogonalize gives U back (up to column signs): the App A.2 iteration
+     must stay there."""
+    from oracle import jd_eigen_iteration
+    Bs, As, _ = gen_loras("trained_like", 40, 36, 6, 3, seed=5, n_families=2)
+    res = jd_full(Bs, As, 4, iters=200, normalize=False, method="direct")
+    out = jd_eigen_iteration(Bs, As, res["U"], res["V"], iters=3)
+    PU, PV = res["U"] @ res["U"].T, res["V"] @ res["V"].T
+    assert np.allclose(out["U"] @ out["U"].T, PU, atol=1e-8)
+    assert np.allclose(out["V"] @ out["V"].T, PV, atol=1e-8)
+    assert np.allclose(out["captured_trace"], out["captured_trace"][0], rtol=1e-10)
+
+
+def test_eigen_iteration_single_adapter_is_svd_subspace_iteration():
+    """n = 1: U0 <- B A V V^T A^T B^T U, i.e. (BA)(BA)^T-power steps coupled with V; the iteration
+    converges to the top-r left / right singular subspaces of B A (Eckart-Young, Eq. 4),
+    checked against numpy's SVD."""
+    from oracle import jd_eigen_iteration, orthogonalize
+    g = np.random.default_rng(3)
+    B, A = g.standard_normal((30, 8)), g.standard_normal((8, 25))
+    r = 3
+    out = jd_eigen_iteration([B], [A], orthogonalize(g.standard_normal((30, r))),
+                             orthogonalize(g.standard_normal((25, r))), iters=300)
+    u, s, vt = np.linalg.svd(B @ A)
+    assert np.allclose(out["U"] @ out["U"].T, u[:, :r] @ u[:, :r].T, atol=1e-8)
+    assert np.allclose(out["V"] @ out["V"].T, vt[:r].T @ vt[:r], atol=1e-8)
+    assert np.isclose(out["captured_trace"][-1], np.sum(s[:r] ** 2), rtol=1e-10)
+
+
+def test_eigen_iteration_exact_span_is_lossless():
+    """Adapters in a shared rank-r span (Prop. 1): from a generic start the iteration
+    captures all the energy, and U Sigma_i V^T reproduces every B_i A_i."""
+    from oracle import jd_eigen_iteration, orthogonalize
+    Bs, As, _ = gen_loras("exact_span", 48, 40, 5, 2, seed=9, r_span=4)
+    g = np.random.default_rng(1)
+    out = jd_eigen_iteration(Bs, As, orthogonalize(g.standard_normal((40, 4))),
+                             orthogonalize(g.standard_normal((48, 4))), iters=100)
+    for B, A, S in zip(Bs, As, out["sigma"]):
+        assert np.allclose(out["U"] @ S @ out["V"].T, B @ A, atol=1e-8 * np.abs(B @ A).max())
