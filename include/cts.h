@@ -201,6 +201,34 @@ cts_status_t cts_expand_reduced_group(cts_plan_t plan, int32_t n, const int32_t*
 cts_status_t cts_project(cts_plan_t plan, int32_t module, const void* x, int64_t ld_x, const void* w0, int64_t ld_w,
                          void* y, int64_t ld_y, float scale, cudaStream_t stream);
 
+/*
+ * GPU compression: the joint diagonalization of each cluster's LoRAs by the
+ * paper's "Additional Eigenvalue Iteration Algorithm" (App A.2), for a batch of
+ * independent problems (e.g. every cluster of a module), `iters` iterations of
+ *     U0 <- sum_i B_i (A_i V)(V^T A_i^T)(B_i^T U),   V0 <- sum_i A_i^T (B_i^T U)(U^T B_i)(A_i V),
+ *     U <- orthogonalize(U0),  V <- orthogonalize(V0)      (reduced QR with diag(R) > 0)
+ * then Sigma_i = U^T B_i A_i V (Eq. sigmastar).  All pointers device, fp32, row major:
+ *   a_stack  [n*r_i][d_in]   rows r_i*i .. r_i*i + r_i - 1 = A_i          (the LoRA "A" factors)
+ *   bt_stack [n*r_i][d_out]  rows r_i*i + j = column j of B_i (B_i^T)      (the LoRA "B" factors)
+ *   U [d_out][r], V [d_in][r]: IN the initial bases (orthonormal columns; the paper fixes no
+ *                 initialization), OUT the result (U = out_basis, V = in_basis of the bank)
+ *   sigma [n][r][r]: OUT, row = out index (the bank's Sigma layout before bf16 rounding)
+ * r in {8, 16, 32, 64} (else CTS_ERR_UNSUPPORTED); d_in, d_out >= r.  workspace: device, >=
+ * cts_jd_workspace_bytes(...), 16-byte aligned (CTS_ERR_SHAPE otherwise).  No normalization is
+ * applied (do it on the factors beforehand, Sec. 6.1, if wanted).  Stream-ordered, deterministic.
+ */
+typedef struct {
+  const float* a_stack;
+  const float* bt_stack;
+  int32_t n, r_i, d_in, d_out;
+  float* U;
+  float* V;
+  float* sigma;
+} cts_jd_problem_t;
+cts_status_t cts_jd_workspace_bytes(const cts_jd_problem_t* problems, int32_t count, int32_t r, size_t* bytes);
+cts_status_t cts_jd_eigen_iteration(const cts_jd_problem_t* problems, int32_t count, int32_t r, int32_t iters,
+                                    void* workspace, size_t ws_bytes, cudaStream_t stream);
+
 /* Read the plan's device error word (call after synchronizing the stream that ran cts_segment).
  * *code = CTS_OK or CTS_ERR_INDEX_OUT_OF_RANGE; *first_bad_token = smallest offending t or -1. */
 cts_status_t cts_plan_error(cts_plan_t plan, int32_t* code, int32_t* first_bad_token);
@@ -212,7 +240,8 @@ const char* cts_status_string(cts_status_t status);
  * plans; launches recorded into a CUDA graph under stream capture count once, at capture).  The
  * difference across a call sequence is that sequence's kernel count: cts_segment = 1,
  * cts_apply / cts_apply_group = 1 (fused kernel; 2 with CTS_FUSED=0), cts_shrink* = cts_expand* = 1,
- * cts_expand_reduced_group = 2, cts_project = 2,
+ * cts_expand_reduced_group = 2, cts_project = 2, cts_jd_eigen_iteration = 6 per iteration + 3 per
+ * batch of 32 problems,
  * cts_bank_load = 3 per module.  Never fails. */
 uint64_t cts_launch_count(void);
 

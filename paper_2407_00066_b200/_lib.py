@@ -26,7 +26,7 @@ EXPORTS = (
     "cts_segment", "cts_segment_readback", "cts_apply", "cts_shrink", "cts_expand",
     "cts_apply_group", "cts_shrink_group", "cts_expand_group", "cts_plan_error", "cts_status_string",
     "cts_launch_count", "cts_plan_partial_elems", "cts_shrink_partial_group", "cts_expand_reduced_group",
-    "cts_project",
+    "cts_project", "cts_jd_workspace_bytes", "cts_jd_eigen_iteration",
 )
 
 
@@ -38,6 +38,20 @@ class CtsError(RuntimeError):
     def __init__(self, fn, code):
         self.code = code
         super().__init__(f"{fn} failed: {STATUS.get(code, code)}")
+
+
+class JdProblem(ctypes.Structure):
+    _fields_ = [
+        ("a_stack", ctypes.c_void_p),
+        ("bt_stack", ctypes.c_void_p),
+        ("n", ctypes.c_int32),
+        ("r_i", ctypes.c_int32),
+        ("d_in", ctypes.c_int32),
+        ("d_out", ctypes.c_int32),
+        ("U", ctypes.c_void_p),
+        ("V", ctypes.c_void_p),
+        ("sigma", ctypes.c_void_p),
+    ]
 
 
 class BankDesc(ctypes.Structure):
@@ -94,6 +108,8 @@ def lib():
         "cts_shrink_partial_group": ([P, I32, VP, VP, VP, F, VP, P], I32),
         "cts_expand_reduced_group": ([P, I32, VP, VP, VP, VP, P], I32),
         "cts_project": ([P, I32, VP, I64, VP, I64, VP, I64, F, P], I32),
+        "cts_jd_workspace_bytes": ([ctypes.POINTER(JdProblem), I32, I32, ctypes.POINTER(ctypes.c_size_t)], I32),
+        "cts_jd_eigen_iteration": ([ctypes.POINTER(JdProblem), I32, I32, I32, VP, ctypes.c_size_t, P], I32),
     }
     for name, (argt, rest) in sig.items():
         f = getattr(L, name)

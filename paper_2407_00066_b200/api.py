@@ -132,6 +132,32 @@ def cts_project(plan, module, x, w0, y, scale=1.0, stream=None):
                                            _stream_handle(stream)))
 
 
+def cts_jd_eigen_iteration(problems, r, iters, stream=None):
+    """GPU compression (App A.2 eigenvalue iteration) for a batch of problems; each problem is a dict
+    of fp32 CUDA tensors: a_stack [n*r_i][d_in], bt_stack [n*r_i][d_out], U [d_out][r] and
+    V [d_in][r] (initial bases in, result out), sigma [n][r][r] (out).  Marshalling only."""
+    from ._lib import JdProblem
+    arr = (JdProblem * max(1, len(problems)))()
+    for k, q in enumerate(problems):
+        for nm in ("a_stack", "bt_stack", "U", "V", "sigma"):
+            t = q[nm]
+            if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+                raise TypeError(f"{nm} must be a contiguous fp32 CUDA tensor")
+        K, d_in = q["a_stack"].shape
+        d_out = q["bt_stack"].shape[1]
+        n = q["sigma"].shape[0]
+        arr[k] = JdProblem(q["a_stack"].data_ptr(), q["bt_stack"].data_ptr(), n, K // n, d_in, d_out,
+                           q["U"].data_ptr(), q["V"].data_ptr(), q["sigma"].data_ptr())
+    nbytes = ctypes.c_size_t()
+    check("cts_jd_workspace_bytes", lib().cts_jd_workspace_bytes(arr, len(problems), int(r), ctypes.byref(nbytes)))
+    dev = problems[0]["U"].device if problems else torch.device("cuda")
+    ws = torch.empty(max(16, nbytes.value), dtype=torch.uint8, device=dev)
+    check("cts_jd_eigen_iteration", lib().cts_jd_eigen_iteration(arr, len(problems), int(r), int(iters),
+                                                                 ctypes.c_void_p(ws.data_ptr()), nbytes.value,
+                                                                 _stream_handle(stream)))
+    return ws          # keep alive until the stream has consumed it
+
+
 def cts_shrink(plan, module, x, scale=1.0, stream=None):
     """Kernel 1 only: t = scale * Sigma_i V_c^T x_t into the plan's scratch for `module`."""
     if x.dtype != torch.bfloat16 or not x.is_cuda or x.dim() != 2 or x.stride(1) != 1:

@@ -16,6 +16,7 @@
 #include "apply_fused.cuh"
 #include "expand.cuh"
 #include "proj_fused.cuh"
+#include "jd_eigen.cuh"
 #include "segment.cuh"
 #include "shrink_sigma.cuh"
 
@@ -530,6 +531,64 @@ cts_status_t launch_project(cts_plan_t p, int32_t module, const void* x, int64_t
   return CTS_OK;
 }
 
+// ------------------------------------------------------------------ GPU compression (App A.2)
+size_t jd_problem_floats(const cts_jd_problem_t& q, int r) {
+  const size_t K = size_t(q.n) * q.r_i;
+  return 4 * K * r + size_t(q.d_in + q.d_out) * r + 64;   // P, Q, W, Z, U0, V0 (+ alignment slack)
+}
+
+template <int R>
+cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t iters, float* ws,
+                           cudaStream_t stream) {
+  static const cudaError_t attr = cudaFuncSetAttribute(jd_small<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       96 * 1024);
+  CTS_CUDA(attr);
+  for (int b0 = 0; b0 < count; b0 += kJdMaxBatch) {
+    JdBatch jb;
+    std::memset(&jb, 0, sizeof(jb));
+    jb.count = std::min(kJdMaxBatch, count - b0);
+    int kmax = 1, dmax = 1, nmax = 1, rimax = 1;
+    for (int i = 0; i < jb.count; ++i) {
+      const cts_jd_problem_t& q = problems[b0 + i];
+      JdProblem& p = jb.pr[i];
+      const size_t K = size_t(q.n) * q.r_i;
+      p.a = q.a_stack; p.bt = q.bt_stack; p.U = q.U; p.V = q.V; p.sigma = q.sigma;
+      p.n = q.n; p.ri = q.r_i; p.d_in = q.d_in; p.d_out = q.d_out;
+      float* w = ws;
+      p.P = w; w += K * R;
+      p.Q = w; w += K * R;
+      p.W = w; w += K * R;
+      p.Z = w; w += K * R;
+      p.U0 = w; w += size_t(q.d_out) * R;
+      p.V0 = w;
+      ws += jd_problem_floats(q, R);
+      kmax = std::max<int>(kmax, int(K));
+      dmax = std::max({dmax, q.d_in, q.d_out});
+      nmax = std::max(nmax, q.n);
+      rimax = std::max(rimax, q.r_i);
+    }
+    const dim3 g_rows((kmax + 31) / 32, 1, jb.count), g_cols((dmax + 63) / 64, 1, jb.count);
+    const dim3 g_small(nmax, jb.count), g_orth(2, jb.count);
+    const size_t small_smem = (2 * size_t(rimax) * R + R * R) * 4;
+    if (small_smem > 96 * 1024) return CTS_ERR_SHAPE;
+    for (int it = 0; it < iters; ++it) {
+      jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 0);
+      jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 1);
+      jd_small<R><<<g_small, 256, small_smem, stream>>>(jb);
+      jd_cols_times<R><<<g_cols, 256, 0, stream>>>(jb, 0);
+      jd_cols_times<R><<<g_cols, 256, 0, stream>>>(jb, 1);
+      jd_orth<R><<<g_orth, 256, 0, stream>>>(jb);
+      g_launches.fetch_add(6, std::memory_order_relaxed);
+    }
+    jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 0);
+    jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 1);
+    jd_sigma<R><<<g_small, 256, 0, stream>>>(jb);
+    g_launches.fetch_add(3, std::memory_order_relaxed);
+    CTS_CUDA(cudaGetLastError());
+  }
+  return CTS_OK;
+}
+
 bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   const uint8_t* x = static_cast<const uint8_t*>(a);
   const uint8_t* y = static_cast<const uint8_t*>(b);
@@ -921,6 +980,36 @@ cts_status_t cts_project(cts_plan_t p, int32_t module, const void* x, int64_t ld
   if (p->T > 0 && (overlaps(y, ny, x, nx) || overlaps(y, ny, w0, nw))) return CTS_ERR_INVALID_ARGUMENT;
   if (p->T == 0) return CTS_OK;
   return launch_project(p, module, x, ld_x, w0, ld_w, y, ld_y, scale, stream);
+}
+
+cts_status_t cts_jd_workspace_bytes(const cts_jd_problem_t* problems, int32_t count, int32_t r, size_t* bytes) {
+  if (!problems || count < 0 || !bytes) return CTS_ERR_INVALID_ARGUMENT;
+  size_t f = 0;
+  for (int i = 0; i < count; ++i) f += jd_problem_floats(problems[i], r);
+  *bytes = f * 4;
+  return CTS_OK;
+}
+
+cts_status_t cts_jd_eigen_iteration(const cts_jd_problem_t* problems, int32_t count, int32_t r, int32_t iters,
+                                    void* workspace, size_t ws_bytes, cudaStream_t stream) {
+  if (!problems || count < 0 || iters < 0 || (count > 0 && !workspace)) return CTS_ERR_INVALID_ARGUMENT;
+  if (r != 8 && r != 16 && r != 32 && r != 64) return CTS_ERR_UNSUPPORTED;
+  size_t need = 0;
+  cts_status_t st = cts_jd_workspace_bytes(problems, count, r, &need);
+  if (st != CTS_OK) return st;
+  if (ws_bytes < need || !aligned16(workspace)) return CTS_ERR_SHAPE;
+  for (int i = 0; i < count; ++i) {
+    const cts_jd_problem_t& q = problems[i];
+    if (!q.a_stack || !q.bt_stack || !q.U || !q.V || !q.sigma) return CTS_ERR_INVALID_ARGUMENT;
+    if (q.n < 1 || q.r_i < 1 || q.d_in < r || q.d_out < r) return CTS_ERR_SHAPE;
+  }
+  float* ws = static_cast<float*>(workspace);
+  switch (r) {
+    case 8: return jd_run<8>(problems, count, iters, ws, stream);
+    case 16: return jd_run<16>(problems, count, iters, ws, stream);
+    case 32: return jd_run<32>(problems, count, iters, ws, stream);
+    default: return jd_run<64>(problems, count, iters, ws, stream);
+  }
 }
 
 #ifdef CTS_TRACE

@@ -547,3 +547,40 @@ def test_fused_projection_full_size_sampled(cts):
         assert err.max() <= PARITY_TOL, f"{di}->{do}: max per-row rel err {err.max():.3e}"
         plan.close()
         bank.close()
+
+
+# ---------------------------------------------------------------- GPU compression (App A.2)
+def _jd_problem(Bs, As, U0, V0):
+    f32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()  # noqa: E731
+    n, r = len(Bs), U0.shape[1]
+    return {"a_stack": f32(np.concatenate(As, axis=0)), "bt_stack": f32(np.concatenate([B.T for B in Bs], axis=0)),
+            "U": f32(U0), "V": f32(V0), "sigma": torch.empty(n, r, r, device="cuda")}
+
+
+@pytest.mark.parametrize("r,dims,iters", [(8, (96, 80), 6), (16, (256, 192), 8), (16, (4096, 4096), 4)])
+def test_gpu_jd_eigen_iteration(cts, r, dims, iters):
+    """cts_jd_eigen_iteration vs the fp64 oracle of App A.2 on the
+    same fp32 factors and the same initial bases: a batch of clusters with different sizes and
+    LoRA ranks; U, V unique (QR with positive R diagonal) -> compared elementwise, Sigma per adapter."""
+    from oracle import jd_eigen_iteration, orthogonalize
+    d_in, d_out = dims
+    g = np.random.default_rng(r + d_in)
+    probs, refs = [], []
+    for k, (n, ri) in enumerate(((5, 16), (9, 8), (3, 16)) if d_in < 1000 else ((40, 16),)):
+        Bs, As, _ = gen_loras("trained_like", d_in, d_out, n, ri, seed=100 * k + r, n_families=2)
+        Bs = [B.astype(np.float32).astype(np.float64) for B in Bs]
+        As = [A.astype(np.float32).astype(np.float64) for A in As]
+        U0 = orthogonalize(g.standard_normal((d_out, r))).astype(np.float32).astype(np.float64)
+        V0 = orthogonalize(g.standard_normal((d_in, r))).astype(np.float32).astype(np.float64)
+        probs.append(_jd_problem(Bs, As, U0, V0))
+        refs.append(jd_eigen_iteration(Bs, As, U0, V0, iters))
+    ws = cts.cts_jd_eigen_iteration(probs, r, iters)
+    torch.cuda.synchronize()
+    del ws
+    for q, ref in zip(probs, refs):
+        U, V, S = (q[k].cpu().numpy().astype(np.float64) for k in ("U", "V", "sigma"))
+        assert np.abs(U - ref["U"]).max() <= 2e-4, np.abs(U - ref["U"]).max()
+        assert np.abs(V - ref["V"]).max() <= 2e-4, np.abs(V - ref["V"]).max()
+        rel = np.linalg.norm(S - ref["sigma"], axis=(1, 2)) / np.linalg.norm(ref["sigma"], axis=(1, 2))
+        assert rel.max() <= 1e-4, rel.max()
+        assert np.allclose(U.T @ U, np.eye(r), atol=1e-5) and np.allclose(V.T @ V, np.eye(r), atol=1e-5)
