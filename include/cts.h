@@ -240,7 +240,7 @@ const char* cts_status_string(cts_status_t status);
  * plans; launches recorded into a CUDA graph under stream capture count once, at capture).  The
  * difference across a call sequence is that sequence's kernel count: cts_segment = 1,
  * cts_apply / cts_apply_group = 1 (fused kernel; 2 with CTS_FUSED=0), cts_shrink* = cts_expand* = 1,
- * cts_expand_reduced_group = 2, cts_project = 2, cts_jd_eigen_iteration = 6 per iteration + 3 per
+ * cts_expand_reduced_group = 2, cts_project = 2, cts_jd_eigen_iteration = 12 per iteration + 3 per
  * batch of 32 problems,
  * cts_bank_load = 3 per module.  Never fails. */
 uint64_t cts_launch_count(void);

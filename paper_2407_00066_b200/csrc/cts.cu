@@ -534,7 +534,8 @@ cts_status_t launch_project(cts_plan_t p, int32_t module, const void* x, int64_t
 // ------------------------------------------------------------------ GPU compression (App A.2)
 size_t jd_problem_floats(const cts_jd_problem_t& q, int r) {
   const size_t K = size_t(q.n) * q.r_i;
-  return 4 * K * r + size_t(q.d_in + q.d_out) * r + 64;   // P, Q, W, Z, U0, V0 (+ alignment slack)
+  const size_t gb = (size_t(q.d_in) + 255) / 256 + (size_t(q.d_out) + 255) / 256;
+  return 4 * K * r + size_t(q.d_in + q.d_out) * r + gb * r * r + 64;   // P, Q, W, Z, U0, V0, Gram partials
 }
 
 template <int R>
@@ -560,7 +561,9 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
       p.W = w; w += K * R;
       p.Z = w; w += K * R;
       p.U0 = w; w += size_t(q.d_out) * R;
-      p.V0 = w;
+      p.V0 = w; w += size_t(q.d_in) * R;
+      p.Gu = w; w += (size_t(q.d_out) + 255) / 256 * R * R;
+      p.Gv = w;
       ws += jd_problem_floats(q, R);
       kmax = std::max<int>(kmax, int(K));
       dmax = std::max({dmax, q.d_in, q.d_out});
@@ -568,7 +571,8 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
       rimax = std::max(rimax, q.r_i);
     }
     const dim3 g_rows((kmax + 31) / 32, 1, jb.count), g_cols((dmax + 63) / 64, 1, jb.count);
-    const dim3 g_small(nmax, jb.count), g_orth(2, jb.count);
+    const dim3 g_small(nmax, jb.count), g_gram((dmax + kJdGramRows - 1) / kJdGramRows, jb.count, 2);
+    const dim3 g_one(1, jb.count, 2), g_ew(std::max(1, dmax * R / 256 / 4), jb.count, 2);
     const size_t small_smem = (2 * size_t(rimax) * R + R * R) * 4;
     if (small_smem > 96 * 1024) return CTS_ERR_SHAPE;
     for (int it = 0; it < iters; ++it) {
@@ -577,8 +581,13 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
       jd_small<R><<<g_small, 256, small_smem, stream>>>(jb);
       jd_cols_times<R><<<g_cols, 256, 0, stream>>>(jb, 0);
       jd_cols_times<R><<<g_cols, 256, 0, stream>>>(jb, 1);
-      jd_orth<R><<<g_orth, 256, 0, stream>>>(jb);
-      g_launches.fetch_add(6, std::memory_order_relaxed);
+      for (int pass = 0; pass < 2; ++pass) {
+        jd_gram<R><<<g_gram, 256, 0, stream>>>(jb, pass);
+        jd_chol<R><<<g_one, 32, 0, stream>>>(jb, pass);
+        jd_apply<R><<<g_ew, 256, 0, stream>>>(jb, pass);
+      }
+      jd_copy_back<R><<<g_ew, 256, 0, stream>>>(jb);
+      g_launches.fetch_add(12, std::memory_order_relaxed);
     }
     jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 0);
     jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 1);

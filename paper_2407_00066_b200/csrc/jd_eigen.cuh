@@ -34,6 +34,8 @@ struct JdProblem {
   float* Z;              // [n*r_i][R]
   float* U0;             // [d_out][R]
   float* V0;             // [d_in][R]
+  float* Gu;             // [ceil(d_out/256)][R][R] partial Gram matrices; slot 0 then holds R^-1
+  float* Gv;             // [ceil(d_in/256)][R][R]
   int n, ri, d_in, d_out;
 };
 
@@ -161,82 +163,146 @@ __global__ void __launch_bounds__(256) jd_cols_times(const __grid_constant__ JdB
   }
 }
 
-// orthogonalize X[d][R] (U0 -> U or V0 -> V) by Cholesky-QR, twice; one block per problem and
-// matrix (blockIdx.x = 0: U, 1: V).  G = X^T X in fixed order (deterministic), Cholesky
-// G = R^T R and R^-1 by warp 0, then X <- X R^-1.
+// orthogonalize (U0 -> U, V0 -> V) by Cholesky-QR, twice, in three parallel steps per pass:
+//   jd_gram:  partial Gram matrices X_b^T X_b of 256-row blocks b          (blockIdx.x = block)
+//   jd_chol:  G = sum_b partials in block order (deterministic), Cholesky G = R^T R, R^-1
+//   jd_apply: Y = X R^-1                                                   (rows in parallel)
+// blockIdx.y = problem, blockIdx.z = matrix (0: U, 1: V).  Pass 0 maps X = U0 -> Y = U, pass 1
+// maps U -> U0, and jd_copy_back moves the result into U (V likewise).
+constexpr int kJdGramRows = 256;
+
 template <int R>
-__global__ void __launch_bounds__(256) jd_orth(const __grid_constant__ JdBatch b) {
+__device__ __forceinline__ void jd_orth_mats(const JdProblem& p, int z, int pass, const float*& src, float*& dst,
+                                             int& d, float*& gram) {
+  const bool u = z == 0;
+  d = u ? p.d_out : p.d_in;
+  float* X0 = u ? p.U0 : p.V0;
+  float* X1 = u ? p.U : p.V;
+  src = pass == 0 ? X0 : X1;
+  dst = pass == 0 ? X1 : X0;
+  gram = u ? p.Gu : p.Gv;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) jd_gram(const __grid_constant__ JdBatch b, int pass) {
   const JdProblem& p = b.pr[blockIdx.y];
-  float* X = blockIdx.x == 0 ? p.U0 : p.V0;
-  float* out = blockIdx.x == 0 ? p.U : p.V;
-  const int d = blockIdx.x == 0 ? p.d_out : p.d_in;
-  __shared__ float G[R][R + 1];
-  __shared__ float Ri[R][R + 1];      // R^-1 (upper triangular)
-  constexpr int kRows = 2048 / R;     // rows of X per smem chunk (8 KB)
-  __shared__ float xs[kRows][R];
-  for (int pass = 0; pass < 2; ++pass) {
-    const float* src = pass == 0 ? X : out;        // pass 0: X -> out, pass 1: out -> X (then X -> out)
-    float* dst = pass == 0 ? out : X;
-    // G = X^T X: entries (a, c), thread-strided; chunks of kRows rows through smem
-    float g[(R * R + 255) / 256];
+  const float* src;
+  float* dst;
+  int d;
+  float* gram;
+  jd_orth_mats<R>(p, blockIdx.z, pass, src, dst, d, gram);
+  const int r0 = blockIdx.x * kJdGramRows;
+  if (r0 >= d) return;
+  __shared__ float xs[64][R + 1];
+  constexpr int E = (R * R + 255) / 256;
+  float g[E];
 #pragma unroll
-    for (int q = 0; q < (R * R + 255) / 256; ++q) g[q] = 0.f;
-    for (int r0 = 0; r0 < d; r0 += kRows) {
-      for (int i = threadIdx.x; i < kRows * R; i += 256) {
-        const int r = i / R, c = i % R;
-        xs[r][c] = r0 + r < d ? src[static_cast<size_t>(r0 + r) * R + c] : 0.f;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < (R * R + 255) / 256; ++q) {
-        const int e = threadIdx.x + 256 * q;
-        if (e < R * R) {
-          const int a = e / R, c = e % R;
-          float s = g[q];
-          for (int r = 0; r < kRows; ++r) s = fmaf(xs[r][a], xs[r][c], s);
-          g[q] = s;
-        }
-      }
-      __syncthreads();
-    }
-#pragma unroll
-    for (int q = 0; q < (R * R + 255) / 256; ++q) {
-      const int e = threadIdx.x + 256 * q;
-      if (e < R * R) G[e / R][e % R] = g[q];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      // Cholesky G = L L^T in place (lower), then Ri = (L^T)^-1 (upper)
-      for (int j = 0; j < R; ++j) {
-        float s = G[j][j];
-        for (int k = 0; k < j; ++k) s -= G[j][k] * G[j][k];
-        const float ljj = sqrtf(fmaxf(s, 1e-30f));
-        G[j][j] = ljj;
-        for (int i = j + 1; i < R; ++i) {
-          float t = G[i][j];
-          for (int k = 0; k < j; ++k) t -= G[i][k] * G[j][k];
-          G[i][j] = t / ljj;
-        }
-      }
-      for (int c = 0; c < R; ++c) {            // column c of (L^T)^-1: solve L^T x = e_c (upper)
-        for (int i = R - 1; i >= 0; --i) {
-          float t = i == c ? 1.f : 0.f;
-          for (int k = i + 1; k < R; ++k) t -= G[k][i] * Ri[k][c];
-          Ri[i][c] = i <= c ? t / G[i][i] : 0.f;
-        }
-      }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < d * R; i += 256) {
+  for (int q = 0; q < E; ++q) g[q] = 0.f;
+  for (int c0 = r0; c0 < min(d, r0 + kJdGramRows); c0 += 64) {
+    for (int i = threadIdx.x; i < 64 * R; i += 256) {
       const int r = i / R, c = i % R;
-      const float* row = src + static_cast<size_t>(r) * R;
-      float s = 0.f;
-      for (int a = 0; a <= c; ++a) s = fmaf(row[a], Ri[a][c], s);
-      dst[static_cast<size_t>(r) * R + c] = s;
+      xs[r][c] = c0 + r < d ? src[static_cast<size_t>(c0 + r) * R + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const int e = threadIdx.x + 256 * q;
+      if (e < R * R) {
+        const int a = e / R, c = e % R;
+        float s = g[q];
+#pragma unroll 16
+        for (int r = 0; r < 64; ++r) s = fmaf(xs[r][a], xs[r][c], s);
+        g[q] = s;
+      }
     }
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < d * R; i += 256) out[i] = X[i];
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    const int e = threadIdx.x + 256 * q;
+    if (e < R * R) gram[static_cast<size_t>(blockIdx.x) * R * R + e] = g[q];
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) jd_chol(const __grid_constant__ JdBatch b, int pass) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  const float* src;
+  float* dst;
+  int d;
+  float* gram;
+  jd_orth_mats<R>(p, blockIdx.z, pass, src, dst, d, gram);
+  __shared__ float G[R][R + 1];
+  const int nb = (d + kJdGramRows - 1) / kJdGramRows;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < nb; ++k) s += gram[static_cast<size_t>(k) * R * R + e];   // block order
+    G[e / R][e % R] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    // Cholesky G = L L^T (lower, in place), one column at a time; the warp splits each column's rows
+    const int lane = threadIdx.x;
+    for (int j = 0; j < R; ++j) {
+      if (lane == 0) {
+        float s = G[j][j];
+        for (int k = 0; k < j; ++k) s -= G[j][k] * G[j][k];
+        G[j][j] = sqrtf(fmaxf(s, 1e-30f));
+      }
+      __syncwarp();
+      for (int i = j + 1 + lane; i < R; i += 32) {
+        float t = G[i][j];
+        for (int k = 0; k < j; ++k) t -= G[i][k] * G[j][k];
+        G[i][j] = t / G[j][j];
+      }
+      __syncwarp();
+    }
+    // R^-1 = (L^T)^-1, upper triangular: lane c solves L^T x = e_c for columns c = lane, lane+32
+    float* Rinv = gram;                              // reuse partial slot 0 as [R][R] output
+    for (int c = lane; c < R; c += 32) {
+      float x[R];
+#pragma unroll
+      for (int i = R - 1; i >= 0; --i) {
+        float t = i == c ? 1.f : 0.f;
+#pragma unroll
+        for (int k = i + 1; k < R; ++k) t -= G[k][i] * x[k];
+        x[i] = i <= c ? t / G[i][i] : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i) Rinv[i * R + c] = x[i];
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) jd_apply(const __grid_constant__ JdBatch b, int pass) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  const float* src;
+  float* dst;
+  int d;
+  float* gram;
+  jd_orth_mats<R>(p, blockIdx.z, pass, src, dst, d, gram);
+  __shared__ float Ri[R][R];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Ri[e / R][e % R] = gram[e];
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d * R; i += gridDim.x * blockDim.x) {
+    const int r = i / R, c = i % R;
+    const float* row = src + static_cast<size_t>(r) * R;
+    float s = 0.f;
+    for (int a = 0; a <= c; ++a) s = fmaf(row[a], Ri[a][c], s);
+    dst[i] = s;
+  }
+}
+
+// pass 1 wrote into U0 / V0: copy back into U / V
+template <int R>
+__global__ void __launch_bounds__(256) jd_copy_back(const __grid_constant__ JdBatch b) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  const bool u = blockIdx.z == 0;
+  const int n = (u ? p.d_out : p.d_in) * R;
+  const float* s = u ? p.U0 : p.V0;
+  float* t = u ? p.U : p.V;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = s[i];
 }
 
 // Sigma_i = Q_i^T P_i (R x R; row = out index); blockIdx.x = adapter
