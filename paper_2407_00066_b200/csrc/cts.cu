@@ -273,7 +273,13 @@ __nv_bfloat16* module_tbuf(cts_plan_t p, int module) {
 // SM over the slots the segment kernel produced); the host only caps them: each chunk >= 4 K
 // blocks, <= 16 chunks.  The workspace holds (target * SMs + slots) * 128 rows per module, which
 // bounds slots * ks for any slot count.
-int ks_cap(int min_kblocks) { return std::max(1, std::min(16, min_kblocks / 4)); }
+int ks_cap(int min_kblocks) {
+  static int cap = [] {
+    const char* e = std::getenv("CTS_KS_MAX");   // tuning aid
+    return e ? std::max(1, std::min(16, std::atoi(e))) : 16;
+  }();
+  return std::max(1, std::min(cap, min_kblocks / 4));
+}
 
 // Segment outputs may be read before griddep_wait by every kernel but the first after cts_segment:
 // each kernel triggers its dependents only after its own griddep_wait, so when launch k starts,
