@@ -121,10 +121,12 @@ cts_status_t cts_segment_readback(cts_plan_t plan, int32_t module, int32_t* perm
  *     y[t, :] = bf16_rne( y[t, :] + scale * U_c (Sigma_i (V_c^T x[t, :])) )  for bound tokens t
  * x: bf16 [T][ld_x] (first d_in columns used), y: bf16 [T][ld_y] read and written IN PLACE (the
  * base projection output, Punica's in-place slice update P:L1118).  scale (fp32) multiplies the
- * rank-r intermediate before the expand.  Rows of unbound tokens are not touched.
- * Two persistent kernels (one CTA per SM): shrink + Sigma (tcgen05 GEMM over 128-token cluster
- * tiles, split-K chunks reduced in a fixed order by the last-arriving CTA, per-token Sigma_i matvec
- * in the epilogue) and expand + residual (tcgen05, y rows gathered/scattered by TMA).
+ * rank-r intermediate before the expand.  Rows of unbound tokens are not touched.  An empty batch
+ * (T = 0) is a no-op and may pass NULL x / y (also for cts_apply_group and cts_project).
+ * One persistent launch (one CTA per SM; apply_fused.cuh): shrink + Sigma (tcgen05 GEMM over
+ * 128-token cluster slots, split-K chunks reduced in a fixed order by the last-arriving CTA,
+ * per-token Sigma_i matvec in its epilogue), then expand + residual (tcgen05, y rows moved by TMA)
+ * as each slot's rank-r intermediate is published (CTS_FUSED=0: the two as separate launches).
  * Deterministic (no float atomics; the reduction order does not depend on scheduling).
  * Host validation: CTS_ERR_INVALID_ARGUMENT (null, x/y overlap), CTS_ERR_SHAPE (module index,
  * ld_x < d_in, ld_y < d_out, ld or pointer not 16-byte aligned). */

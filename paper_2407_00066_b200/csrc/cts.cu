@@ -413,7 +413,7 @@ cts_status_t check_group(cts_plan_t p, int32_t n, const int32_t* modules, const 
     if (modules[i] < 0 || modules[i] >= p->bank->n_modules) return CTS_ERR_SHAPE;
     for (int j = 0; j < i; ++j)
       if (modules[j] == modules[i]) return CTS_ERR_INVALID_ARGUMENT;
-    if (!ptrs[i]) return CTS_ERR_INVALID_ARGUMENT;
+    if (!ptrs[i] && p->T > 0) return CTS_ERR_INVALID_ARGUMENT;   // an empty batch may pass null tensors
     const Module& m = p->bank->mods[modules[i]];
     const int64_t need = is_x ? m.d_in : m.d_out;
     if (lds[i] < need || (lds[i] * 2) % 16 || !aligned16(ptrs[i])) return CTS_ERR_SHAPE;
@@ -982,7 +982,7 @@ cts_status_t cts_apply(cts_plan_t p, int32_t module, const void* x, int64_t ld_x
 
 cts_status_t cts_project(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, const void* w0, int64_t ld_w,
                          void* y, int64_t ld_y, float scale, cudaStream_t stream) {
-  if (!p || !x || !w0 || !y) return CTS_ERR_INVALID_ARGUMENT;
+  if (!p || !w0 || (p->T > 0 && (!x || !y))) return CTS_ERR_INVALID_ARGUMENT;
   const cts_bank_t b = p->bank;
   if (module < 0 || module >= b->n_modules) return CTS_ERR_SHAPE;
   if (b->rp != 16) return CTS_ERR_UNSUPPORTED;

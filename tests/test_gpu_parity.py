@@ -584,3 +584,58 @@ def test_gpu_jd_eigen_iteration(cts, r, dims, iters):
         rel = np.linalg.norm(S - ref["sigma"], axis=(1, 2)) / np.linalg.norm(ref["sigma"], axis=(1, 2))
         assert rel.max() <= 1e-4, rel.max()
         assert np.allclose(U.T @ U, np.eye(r), atol=1e-5) and np.allclose(V.T @ V, np.eye(r), atol=1e-5)
+
+
+# ---------------------------------------------------------------- edge cases
+def test_empty_batch_then_normal_batch(cts):
+    """T = 0: segment, grouped apply and projection are no-ops (y untouched); the same plan then
+    serves a normal batch correctly."""
+    bits, f64 = quantized_bank(256, 256, 20, 3, 16, seed=71)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, 64)
+    plan.segment(torch.empty(0, dtype=torch.int32, device="cuda"))
+    x = torch.zeros(0, 256, dtype=torch.bfloat16, device="cuda")
+    y = torch.zeros(0, 256, dtype=torch.bfloat16, device="cuda")
+    plan.apply_group([0], [x], [y], 1.0)
+    plan.project(0, x, torch.zeros(256, 256, dtype=torch.bfloat16, device="cuda"), y, 1.0)
+    torch.cuda.synchronize()
+    assert plan.error() == (0, -1)
+    ta = decode_tokens(64, 20, 72)
+    plan.segment(torch.from_numpy(ta).cuda())
+    xb = bf16_round(activations(64, 256, 73))
+    got = run_apply(cts, plan, 0, xb, np.zeros((64, 256), np.uint16), 1.0)
+    check_delta(ta, got, f64, xb, 1.0)
+    plan.close()
+    bank.close()
+
+
+def test_all_tokens_one_adapter_prefill(cts):
+    """Degenerate batch: all 16384 tokens bound to ONE adapter (one cluster holds every slot, the
+    other clusters are empty); sampled rows vs the oracle."""
+    N, C, T = 100, 10, 16384
+    bits, f64 = quantized_bank(1024, 512, N, C, 16, seed=74)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    ta = np.full(T, 37, np.int32)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(T, 1024, 75))
+    got = run_apply(cts, plan, 0, x, np.zeros((T, 512), np.uint16), 2.0)
+    check_delta(ta, got, f64, x, 2.0, rows=np.random.default_rng(2).choice(T, 300, replace=False))
+    plan.close()
+    bank.close()
+
+
+def test_maximum_clusters_singletons(cts):
+    """C = N = 1024 (the library's cluster limit, segment.cuh) with every token on a distinct
+    adapter (1024 one-token tiles, packed two per slot): every row vs the oracle."""
+    N = C = T = 1024
+    bits, f64 = quantized_bank(256, 192, N, C, 16, seed=76, cluster_of=np.arange(N, dtype=np.int32))
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    ta = np.random.default_rng(77).permutation(N).astype(np.int32)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(T, 256, 78))
+    got = run_apply(cts, plan, 0, x, np.zeros((T, 192), np.uint16), 1.0)
+    check_delta(ta, got, f64, x, 1.0)
+    plan.close()
+    bank.close()
