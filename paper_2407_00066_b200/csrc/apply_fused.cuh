@@ -107,12 +107,9 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
     if (threadIdx.x == 0) CTS_STAMP(7);
     expand_producer<RP>(p.e, RE, nt_lane, warp, lane);
   } else if (warp == kMmaWarp) {
-    int slot = 0;
-    uint32_t aphase = 0;
-    shrink_mma<RP>(p.s, RS, W, lane, &slot, &aphase);
+    shrink_mma<RP>(p.s, RS, W, lane);
     if (lane == 0) { umma_commit(arena_free); CTS_STAMP(4); }
     __syncwarp();
-    (void)slot; (void)aphase;
     mbar_wait(tmem_free, 0);                  // shrink accumulators and staged Sigma all read
     tc_fence_after();
     expand_mma<RP>(p.e, RE, nt_lane, lane);

@@ -282,11 +282,10 @@ __device__ void shrink_producer(const ShrinkParams& p, const ShrinkRing& R, cons
 }
 
 // ------------------------------------------------------------------ MMA issuer (warp 4)
-// Returns once every MMA is issued; on return the accumulator ring position is (*acc_slot, *acc_phase)
-// so the fused kernel can wait for the epilogue to drain it (shrink_drain_tmem).
+// Returns once every MMA is issued (the fused kernel then waits for its tmem_free barrier before
+// reusing the TMEM columns).
 template <int RP>
-__device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, const ShrinkWork& W, int lane,
-                           int* acc_slot = nullptr, uint32_t* acc_phase = nullptr) {
+__device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, const ShrinkWork& W, int lane) {
   using L = ShrinkCfg<RP>;
   // N = 2 r_pad: the two halves' basis slabs are contiguous in the B stage, so ONE MMA per K step
   // yields D0 = A B0^T (cols [0, rp)) and D1 = A B1^T (cols [rp, 2rp)); for an unshared slot the
@@ -325,17 +324,6 @@ __device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, const Shr
     __syncwarp();
     if (++slot == kShrinkAccSlots) { slot = 0; aphase ^= 1; }
   }
-  if (acc_slot) { *acc_slot = slot; *acc_phase = aphase; }
-}
-
-// MMA warp: wait until the epilogue has read every accumulator slot the shrink used (the next
-// kShrinkAccSlots acquisitions of the ring), so the TMEM columns can be reused.
-__device__ __forceinline__ void shrink_drain_tmem(const ShrinkRing& R, int slot, uint32_t aphase) {
-  for (int k = 0; k < kShrinkAccSlots; ++k) {
-    mbar_wait(&R.acc_empty[slot], aphase ^ 1);
-    if (++slot == kShrinkAccSlots) { slot = 0; aphase ^= 1; }
-  }
-  tc_fence_after();
 }
 
 // ------------------------------------------------------------------ epilogue (warps 5-12)
