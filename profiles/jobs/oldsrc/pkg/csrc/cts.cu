@@ -348,7 +348,6 @@ cts_status_t fill_expand(cts_plan_t p, int n, const int32_t* modules, void* cons
     em.tile_rows = p->tile_rows + mid * p->max_tiles * kTileM;
     em.ready = fused ? p->ready + size_t(i) * p->max_tiles : nullptr;
     em.y = static_cast<__nv_bfloat16*>(ys[i]);
-    em.y32 = (reinterpret_cast<uintptr_t>(ys[i]) % 32 == 0 && (ld_y[i] * 2) % 32 == 0 && m.d_out % 16 == 0) ? 1 : 0;
     em.ld_y = ld_y[i];
     em.nblk = (m.d_out + kBN - 1) / kBN;
     em.d_out = m.d_out;

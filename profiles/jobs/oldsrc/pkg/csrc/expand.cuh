@@ -42,9 +42,6 @@ constexpr int kExpandThreads = kApplyThreads;
 constexpr int kBN = CTS_EXPAND_BN;       // d_out columns per work item
 constexpr int kExpandAccSlots = 512 / (2 * kBN);   // (D0 | D1) x kBN fp32 columns each: all of TMEM
 constexpr int kStoreScatter = 0, kStoreDirect = 1, kStoreCoalesced = 2;   // expand epilogue store paths
-#ifndef CTS_Y_STORE_HINT
-#define CTS_Y_STORE_HINT ""       // e.g. ".cs" (evict-first) -- tuning aid
-#endif
 #ifndef CTS_EXPAND_BOXES
 #define CTS_EXPAND_BOXES 1   // runs of consecutive tokens as box loads / stores (row_boxes)
 #endif
@@ -68,7 +65,6 @@ struct alignas(64) ExpandMod {
   const int32_t* tile_rows;              // [slot*128 + row] token index
   const int32_t* ready;                  // [slot] "t ready" flags (fused kernel only; else null)
   __nv_bfloat16* y;                      // y base (register-direct stores)
-  int y32;                               // y base and row stride 32-byte aligned: 256-bit stores
   int64_t ld_y;                          // elements
   int nblk;                              // ceil(d_out / kBN)
   int d_out;
@@ -312,31 +308,19 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
           __nv_bfloat16* yrow =
               DIRECT ? mo.y + static_cast<size_t>(stage_rows<RP>(R, stage)[row]) * mo.ld_y + col0 : nullptr;
 #pragma unroll
-          for (int qd = 0; qd < 8; qd += 2) {
-            uint4 w[2];
+          for (int qd = 0; qd < 8; ++qd) {
+            const int phys = (qd ^ (row & 7)) * 16;
+            uint4 w = *reinterpret_cast<uint4*>(base + phys);
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int phys = ((qd + u) ^ (row & 7)) * 16;
-              w[u] = *reinterpret_cast<uint4*>(base + phys);
-              __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w[u]);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h[e]);
-                h[e] = __floats2bfloat162_rn(f.x + v[(qd + u) * 8 + 2 * e], f.y + v[(qd + u) * 8 + 2 * e + 1]);
-              }
-              if (!DIRECT) *reinterpret_cast<uint4*>(base + phys) = w[u];
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h[e]);
+              h[e] = __floats2bfloat162_rn(f.x + v[qd * 8 + 2 * e], f.y + v[qd * 8 + 2 * e + 1]);
             }
-            if (DIRECT && col0 + qd * 8 < mo.d_out) {
-              if (mo.y32) {
-                // one 32-byte (full-sector) store for the two 16-byte chunks (256-bit LSU path, sm_100)
-                asm volatile("st.global" CTS_Y_STORE_HINT ".v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(yrow + qd * 8),
-                             "r"(w[0].x), "r"(w[0].y), "r"(w[0].z), "r"(w[0].w), "r"(w[1].x), "r"(w[1].y), "r"(w[1].z),
-                             "r"(w[1].w)
-                             : "memory");
-              } else {
-                *reinterpret_cast<uint4*>(yrow + qd * 8) = w[0];
-                *reinterpret_cast<uint4*>(yrow + qd * 8 + 8) = w[1];
-              }
+            if (DIRECT) {
+              if (col0 + qd * 8 < mo.d_out) *reinterpret_cast<uint4*>(yrow + qd * 8) = w;
+            } else {
+              *reinterpret_cast<uint4*>(base + phys) = w;
             }
           }
         }

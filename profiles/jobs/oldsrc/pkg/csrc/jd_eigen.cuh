@@ -1,0 +1,323 @@
+// jd_eigen.cuh -- SURVEY 8(f) NEXT 3: GPU compression.  The joint diagonalization of a cluster's
+// LoRAs by the paper's GPU-oriented "Additional Eigenvalue Iteration Algorithm" (App A.2,
+// P:L528-562), batched over clusters / modules:
+//     P_i = A_i V,  Q_i = B_i^T U                                    (r_i x r each)
+//     U0  = sum_i B_i (P_i (P_i^T Q_i)),   V0 = sum_i A_i^T (Q_i (Q_i^T P_i))
+//     U <- orthogonalize(U0),  V <- orthogonalize(V0)                 (both from the k-th iterates)
+// and finally Sigma_i = U^T B_i A_i V = Q_i^T P_i (Eq. sigmastar).  The paper's
+// parenthesization is kept: nothing d x d is ever formed.  With the factors stacked --
+// A_stack = [A_1; ..; A_n] (n r_i x d_in), Bt_stack = [B_1^T; ..; B_n^T] (n r_i x d_out) -- the four
+// sums are four thin GEMMs (P = A_stack V, Q = Bt_stack U, U0 = Bt_stack^T W, V0 = A_stack^T Z) and
+// W_i = P_i S_i, Z_i = Q_i S_i^T with S_i = P_i^T Q_i are per-adapter r x r products.
+// orthogonalize = Cholesky-QR applied twice (Q = X R^-1 with R^T R = X^T X, diag(R) > 0: the
+// reduced QR with a positive R diagonal, the oracle's convention).  fp32 (an offline step).
+//
+// All kernels take a batch of independent problems (blockIdx.z / blockIdx.y = problem), so one
+// launch covers every cluster of a module (or several modules) and fills the SMs.
+#pragma once
+#include <cstdint>
+#include "sm100.cuh"
+
+namespace cts {
+
+constexpr int kJdMaxBatch = 32;
+
+struct JdProblem {
+  const float* a;        // A_stack [n*r_i][d_in]
+  const float* bt;       // Bt_stack [n*r_i][d_out]
+  float* U;              // [d_out][R] in/out
+  float* V;              // [d_in][R] in/out
+  float* sigma;          // [n][R][R] out (row = out index)
+  float* P;              // workspace [n*r_i][R]
+  float* Q;              // [n*r_i][R]
+  float* W;              // [n*r_i][R]
+  float* Z;              // [n*r_i][R]
+  float* U0;             // [d_out][R]
+  float* V0;             // [d_in][R]
+  float* Gu;             // [ceil(d_out/256)][R][R] partial Gram matrices; slot 0 then holds R^-1
+  float* Gv;             // [ceil(d_in/256)][R][R]
+  int n, ri, d_in, d_out;
+};
+
+struct JdBatch {
+  JdProblem pr[kJdMaxBatch];
+  int count;
+};
+
+// out[K][R] = X[K][d] * Y[d][R]; block = 32 rows of X, thread (row, column group of R/8)
+template <int R>
+__global__ void __launch_bounds__(256) jd_rows_times(const __grid_constant__ JdBatch b, int which) {
+  const JdProblem& p = b.pr[blockIdx.z];
+  const float* X = which == 0 ? p.a : p.bt;          // 0: P = A V, 1: Q = Bt U
+  const float* Y = which == 0 ? p.V : p.U;
+  float* out = which == 0 ? p.P : p.Q;
+  const int d = which == 0 ? p.d_in : p.d_out;
+  const int K = p.n * p.ri;
+  const int row0 = blockIdx.x * 32;
+  if (row0 >= K) return;
+  __shared__ float xs[32][65];
+  __shared__ float ys[64][R];
+  constexpr int CG = R / 8;                             // columns per thread
+  const int tr = threadIdx.x >> 3, tc = (threadIdx.x & 7) * CG;
+  float acc[CG];
+#pragma unroll
+  for (int c = 0; c < CG; ++c) acc[c] = 0.f;
+  for (int d0 = 0; d0 < d; d0 += 64) {
+    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
+      const int r = i >> 6, c = i & 63;
+      xs[r][c] = (row0 + r < K && d0 + c < d) ? X[static_cast<size_t>(row0 + r) * d + d0 + c] : 0.f;
+    }
+    for (int i = threadIdx.x; i < 64 * R; i += 256) {
+      const int r = i / R, c = i % R;
+      ys[r][c] = d0 + r < d ? Y[static_cast<size_t>(d0 + r) * R + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < 64; ++k) {
+      const float xv = xs[tr][k];
+#pragma unroll
+      for (int c = 0; c < CG; ++c) acc[c] = fmaf(xv, ys[k][tc + c], acc[c]);
+    }
+    __syncthreads();
+  }
+  if (row0 + tr < K) {
+#pragma unroll
+    for (int c = 0; c < CG; ++c) out[static_cast<size_t>(row0 + tr) * R + tc + c] = acc[c];
+  }
+}
+
+// per adapter i: S = P_i^T Q_i (R x R), W_i = P_i S, Z_i = Q_i S^T  (blockIdx.x = adapter)
+template <int R>
+__global__ void __launch_bounds__(256) jd_small(const __grid_constant__ JdBatch b) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  const int i = blockIdx.x;
+  if (i >= p.n) return;
+  extern __shared__ float sm[];
+  float* Ps = sm;                      // [ri][R]
+  float* Qs = Ps + p.ri * R;           // [ri][R]
+  float* S = Qs + p.ri * R;            // [R][R]
+  const size_t base = static_cast<size_t>(i) * p.ri * R;
+  for (int e = threadIdx.x; e < p.ri * R; e += blockDim.x) {
+    Ps[e] = p.P[base + e];
+    Qs[e] = p.Q[base + e];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int a = e / R, c = e % R;
+    float s = 0.f;
+    for (int j = 0; j < p.ri; ++j) s = fmaf(Ps[j * R + a], Qs[j * R + c], s);
+    S[e] = s;                          // S[a][c] = (P_i^T Q_i)[a][c]
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < p.ri * R; e += blockDim.x) {
+    const int j = e / R, c = e % R;
+    float w = 0.f, z = 0.f;
+    for (int a = 0; a < R; ++a) {
+      w = fmaf(Ps[j * R + a], S[a * R + c], w);   // (P_i S)[j][c]
+      z = fmaf(Qs[j * R + a], S[c * R + a], z);   // (Q_i S^T)[j][c]
+    }
+    p.W[base + e] = w;
+    p.Z[base + e] = z;
+  }
+}
+
+// out[d][R] = X[K][d]^T * M[K][R]; block = 64 columns of X, thread (column, group of R/4)
+template <int R>
+__global__ void __launch_bounds__(256) jd_cols_times(const __grid_constant__ JdBatch b, int which) {
+  const JdProblem& p = b.pr[blockIdx.z];
+  const float* X = which == 0 ? p.bt : p.a;           // 0: U0 = Bt^T W, 1: V0 = A^T Z
+  const float* Mt = which == 0 ? p.W : p.Z;
+  float* out = which == 0 ? p.U0 : p.V0;
+  const int d = which == 0 ? p.d_out : p.d_in;
+  const int K = p.n * p.ri;
+  const int col0 = blockIdx.x * 64;
+  if (col0 >= d) return;
+  __shared__ float xs[32][64];
+  __shared__ float ms[32][R];
+  constexpr int CG = R / 4;
+  const int tcol = threadIdx.x & 63, tg = (threadIdx.x >> 6) * CG;
+  float acc[CG];
+#pragma unroll
+  for (int c = 0; c < CG; ++c) acc[c] = 0.f;
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
+      const int r = i >> 6, c = i & 63;
+      xs[r][c] = (k0 + r < K && col0 + c < d) ? X[static_cast<size_t>(k0 + r) * d + col0 + c] : 0.f;
+    }
+    for (int i = threadIdx.x; i < 32 * R; i += 256) {
+      const int r = i / R, c = i % R;
+      ms[r][c] = k0 + r < K ? Mt[static_cast<size_t>(k0 + r) * R + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const float xv = xs[k][tcol];
+#pragma unroll
+      for (int c = 0; c < CG; ++c) acc[c] = fmaf(xv, ms[k][tg + c], acc[c]);
+    }
+    __syncthreads();
+  }
+  if (col0 + tcol < d) {
+#pragma unroll
+    for (int c = 0; c < CG; ++c) out[static_cast<size_t>(col0 + tcol) * R + tg + c] = acc[c];
+  }
+}
+
+// orthogonalize (U0 -> U, V0 -> V) by Cholesky-QR, twice, in three parallel steps per pass:
+//   jd_gram:  partial Gram matrices X_b^T X_b of 256-row blocks b          (blockIdx.x = block)
+//   jd_chol:  G = sum_b partials in block order (deterministic), Cholesky G = R^T R, R^-1
+//   jd_apply: Y = X R^-1                                                   (rows in parallel)
+// blockIdx.y = problem, blockIdx.z = matrix (0: U, 1: V).  Pass 0 maps X = U0 -> Y = U, pass 1
+// maps U -> U0, and jd_copy_back moves the result into U (V likewise).
+constexpr int kJdGramRows = 256;
+
+template <int R>
+__device__ __forceinline__ void jd_orth_mats(const JdProblem& p, int z, int pass, const float*& src, float*& dst,
+                                             int& d, float*& gram) {
+  const bool u = z == 0;
+  d = u ? p.d_out : p.d_in;
+  float* X0 = u ? p.U0 : p.V0;
+  float* X1 = u ? p.U : p.V;
+  src = pass == 0 ? X0 : X1;
+  dst = pass == 0 ? X1 : X0;
+  gram = u ? p.Gu : p.Gv;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) jd_gram(const __grid_constant__ JdBatch b, int pass) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  const float* src;
+  float* dst;
+  int d;
+  float* gram;
+  jd_orth_mats<R>(p, blockIdx.z, pass, src, dst, d, gram);
+  const int r0 = blockIdx.x * kJdGramRows;
+  if (r0 >= d) return;
+  __shared__ float xs[64][R + 1];
+  constexpr int E = (R * R + 255) / 256;
+  float g[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) g[q] = 0.f;
+  for (int c0 = r0; c0 < min(d, r0 + kJdGramRows); c0 += 64) {
+    for (int i = threadIdx.x; i < 64 * R; i += 256) {
+      const int r = i / R, c = i % R;
+      xs[r][c] = c0 + r < d ? src[static_cast<size_t>(c0 + r) * R + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const int e = threadIdx.x + 256 * q;
+      if (e < R * R) {
+        const int a = e / R, c = e % R;
+        float s = g[q];
+#pragma unroll 16
+        for (int r = 0; r < 64; ++r) s = fmaf(xs[r][a], xs[r][c], s);
+        g[q] = s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    const int e = threadIdx.x + 256 * q;
+    if (e < R * R) gram[static_cast<size_t>(blockIdx.x) * R * R + e] = g[q];
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) jd_chol(const __grid_constant__ JdBatch b, int pass) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  const float* src;
+  float* dst;
+  int d;
+  float* gram;
+  jd_orth_mats<R>(p, blockIdx.z, pass, src, dst, d, gram);
+  __shared__ float G[R][R + 1];
+  const int nb = (d + kJdGramRows - 1) / kJdGramRows;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < nb; ++k) s += gram[static_cast<size_t>(k) * R * R + e];   // block order
+    G[e / R][e % R] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    // Cholesky G = L L^T (lower, in place), one column at a time; the warp splits each column's rows
+    const int lane = threadIdx.x;
+    for (int j = 0; j < R; ++j) {
+      if (lane == 0) {
+        float s = G[j][j];
+        for (int k = 0; k < j; ++k) s -= G[j][k] * G[j][k];
+        G[j][j] = sqrtf(fmaxf(s, 1e-30f));
+      }
+      __syncwarp();
+      for (int i = j + 1 + lane; i < R; i += 32) {
+        float t = G[i][j];
+        for (int k = 0; k < j; ++k) t -= G[i][k] * G[j][k];
+        G[i][j] = t / G[j][j];
+      }
+      __syncwarp();
+    }
+    // R^-1 = (L^T)^-1, upper triangular: lane c solves L^T x = e_c for columns c = lane, lane+32
+    float* Rinv = gram;                              // reuse partial slot 0 as [R][R] output
+    for (int c = lane; c < R; c += 32) {
+      float x[R];
+#pragma unroll
+      for (int i = R - 1; i >= 0; --i) {
+        float t = i == c ? 1.f : 0.f;
+#pragma unroll
+        for (int k = i + 1; k < R; ++k) t -= G[k][i] * x[k];
+        x[i] = i <= c ? t / G[i][i] : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i) Rinv[i * R + c] = x[i];
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) jd_apply(const __grid_constant__ JdBatch b, int pass) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  const float* src;
+  float* dst;
+  int d;
+  float* gram;
+  jd_orth_mats<R>(p, blockIdx.z, pass, src, dst, d, gram);
+  __shared__ float Ri[R][R];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Ri[e / R][e % R] = gram[e];
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d * R; i += gridDim.x * blockDim.x) {
+    const int r = i / R, c = i % R;
+    const float* row = src + static_cast<size_t>(r) * R;
+    float s = 0.f;
+    for (int a = 0; a <= c; ++a) s = fmaf(row[a], Ri[a][c], s);
+    dst[i] = s;
+  }
+}
+
+// pass 1 wrote into U0 / V0: copy back into U / V
+template <int R>
+__global__ void __launch_bounds__(256) jd_copy_back(const __grid_constant__ JdBatch b) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  const bool u = blockIdx.z == 0;
+  const int n = (u ? p.d_out : p.d_in) * R;
+  const float* s = u ? p.U0 : p.V0;
+  float* t = u ? p.U : p.V;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = s[i];
+}
+
+// Sigma_i = Q_i^T P_i (R x R; row = out index); blockIdx.x = adapter
+template <int R>
+__global__ void __launch_bounds__(256) jd_sigma(const __grid_constant__ JdBatch b) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  const int i = blockIdx.x;
+  if (i >= p.n) return;
+  const size_t base = static_cast<size_t>(i) * p.ri * R;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int o = e / R, k = e % R;
+    float s = 0.f;
+    for (int j = 0; j < p.ri; ++j) s = fmaf(p.Q[base + j * R + o], p.P[base + j * R + k], s);
+    p.sigma[static_cast<size_t>(i) * R * R + e] = s;
+  }
+}
+
+}  // namespace cts
