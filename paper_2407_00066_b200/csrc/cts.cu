@@ -528,6 +528,7 @@ cts_status_t launch_project(cts_plan_t p, int32_t module, const void* x, int64_t
   prm.n_unbound = p->n_unbound;
   prm.y = static_cast<__nv_bfloat16*>(y);
   prm.ld_y = ld_y;
+  prm.y32 = (reinterpret_cast<uintptr_t>(y) % 32 == 0 && (ld_y * 2) % 32 == 0) ? 1 : 0;
   prm.kblocks = m.d_in / kBK;
   prm.nblk = m.d_out / kProjBN;
   prm.d_out = m.d_out;

@@ -53,6 +53,7 @@ struct ProjParams {
   int nblk;                              // d_out / 256
   int d_out;
   int meta_ready;
+  int y32;                               // y base and row stride 32-byte aligned: 256-bit stores
   CUtensorMap tm_x4;                     // x [T][d_in], box {64, 1}, 128B swizzle (gather4)
   CUtensorMap tm_x8;                     // x [T][d_in], box {64, 8}, 128B swizzle (runs of 8 tokens)
   CUtensorMap tm_x32;                    // x [T][d_in], box {64, 32} (runs of 32 tokens)
@@ -274,13 +275,19 @@ __global__ void __launch_bounds__(kApplyThreads, 1) proj_fused_kernel(const __gr
         tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * kProjBN + set * 128 + c, v);
         tmem_ld_wait();
         if (valid) {
+          uint4 w[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            uint4 w;
-            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w);
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&w[q]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
-            *reinterpret_cast<uint4*>(yrow + c + 8 * q) = w;
+          }
+          if (p.y32) {                                   // 32-byte (full-sector) stores
+            st_global_v8(yrow + c, w[0], w[1]);
+            st_global_v8(yrow + c + 16, w[2], w[3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(yrow + c + 8 * q) = w[q];
           }
         }
       }

@@ -395,7 +395,11 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
       if (rvalid) {
         float4* dst = reinterpret_cast<float4*>(wbase + static_cast<size_t>(kc) * kTileM * RP);
 #pragma unroll
-        for (int c = 0; c < RP / 4; ++c) dst[c] = make_float4(s[4 * c], s[4 * c + 1], s[4 * c + 2], s[4 * c + 3]);
+        for (int c = 0; c < RP / 4; c += 2)            // 32-byte stores (full sectors)
+          st_global_v8(dst + c, make_uint4(__float_as_uint(s[4 * c]), __float_as_uint(s[4 * c + 1]),
+                                           __float_as_uint(s[4 * c + 2]), __float_as_uint(s[4 * c + 3])),
+                       make_uint4(__float_as_uint(s[4 * c + 4]), __float_as_uint(s[4 * c + 5]),
+                                  __float_as_uint(s[4 * c + 6]), __float_as_uint(s[4 * c + 7])));
       }
       named_bar_sync(1 + set, 128);
       if (set_tid == 0) R.s_last[set] = (atom_add_acq_rel_gpu(&m.counters[tile], 1) == ks - 1);
@@ -417,7 +421,14 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
               if (q0 + j < ks) {
                 const float4* src = reinterpret_cast<const float4*>(wbase + static_cast<size_t>(q0 + j) * kTileM * RP);
 #pragma unroll
-                for (int c = 0; c < RP / 4; ++c) buf[j][c] = __ldcg(src + c);
+                for (int c = 0; c < RP / 4; c += 2) {
+                  uint4 a, b;
+                  ld_global_cg_v8(src + c, a, b);
+                  buf[j][c] = make_float4(__uint_as_float(a.x), __uint_as_float(a.y), __uint_as_float(a.z),
+                                          __uint_as_float(a.w));
+                  buf[j][c + 1] = make_float4(__uint_as_float(b.x), __uint_as_float(b.y), __uint_as_float(b.z),
+                                              __uint_as_float(b.w));
+                }
               }
             }
 #pragma unroll
@@ -464,11 +475,11 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
           for (int c = 0; c < RP / 4; ++c) dp[c] = make_float4(t[4 * c], t[4 * c + 1], t[4 * c + 2], t[4 * c + 3]);
         } else {
           __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP);
+          uint4 hi[RP / 8], lo[RP / 8];
 #pragma unroll
           for (int o0 = 0; o0 < RP; o0 += 8) {
-            uint4 hi, lo;
-            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&hi);
-            __nv_bfloat162* ll = reinterpret_cast<__nv_bfloat162*>(&lo);
+            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&hi[o0 / 8]);
+            __nv_bfloat162* ll = reinterpret_cast<__nv_bfloat162*>(&lo[o0 / 8]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const __nv_bfloat162 h2 = __floats2bfloat162_rn(t[o0 + 2 * e], t[o0 + 2 * e + 1]);
@@ -476,8 +487,11 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
               hh[e] = h2;
               ll[e] = __floats2bfloat162_rn(t[o0 + 2 * e] - hf.x, t[o0 + 2 * e + 1] - hf.y);
             }
-            *reinterpret_cast<uint4*>(dst + o0) = hi;
-            *reinterpret_cast<uint4*>(dst + RP + o0) = lo;
+          }
+#pragma unroll
+          for (int q = 0; q < RP / 8; q += 2) {           // 32-byte stores: hi | lo rows of 2*RP bf16
+            st_global_v8(dst + 8 * q, hi[q], hi[q + 1]);
+            st_global_v8(dst + RP + 8 * q, lo[q], lo[q + 1]);
           }
         }
       }
