@@ -361,9 +361,11 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
       for (int h = 0; h < 2; ++h) {
         uint32_t w[64];
 #pragma unroll
-        for (int v = 0; v < 16; ++v) {
-          const uint4 q = rvalid ? __ldg(sg + 16 * h + v) : make_uint4(0, 0, 0, 0);
-          w[4 * v] = q.x; w[4 * v + 1] = q.y; w[4 * v + 2] = q.z; w[4 * v + 3] = q.w;
+        for (int v = 0; v < 16; v += 2) {              // 32-byte loads
+          uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+          if (rvalid) ld_global_nc_v8(sg + 16 * h + v, q0, q1);
+          w[4 * v] = q0.x; w[4 * v + 1] = q0.y; w[4 * v + 2] = q0.z; w[4 * v + 3] = q0.w;
+          w[4 * v + 4] = q1.x; w[4 * v + 5] = q1.y; w[4 * v + 6] = q1.z; w[4 * v + 7] = q1.w;
         }
         tmem_st32(tsig + 64 * h, w);
         tmem_st32(tsig + 64 * h + 32, w + 32);

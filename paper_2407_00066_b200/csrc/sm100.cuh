@@ -309,6 +309,11 @@ __device__ __forceinline__ void ld_global_cg_v8(const void* p, uint4& a, uint4& 
                : "l"(p)
                : "memory");
 }
+__device__ __forceinline__ void ld_global_nc_v8(const void* p, uint4& a, uint4& b) {   // read-only path
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
 __device__ __forceinline__ void nanosleep_ns(uint32_t ns) { asm volatile("nanosleep.u32 %0;" ::"r"(ns)); }
 
 // ------------------------------------------------------------------ debug timeline (off unless traced)
