@@ -127,6 +127,10 @@ cts_status_t cts_segment_readback(cts_plan_t plan, int32_t module, int32_t* perm
  * 128-token cluster slots, split-K chunks reduced in a fixed order by the last-arriving CTA,
  * per-token Sigma_i matvec in its epilogue), then expand + residual (tcgen05, y rows moved by TMA)
  * as each slot's rank-r intermediate is published (CTS_FUSED=0: the two as separate launches).
+ * Progress of the single launch relies on its CTAs (at most one per SM) being co-resident: expand
+ * work waits on flags that other CTAs' shrink work publishes.  With exclusive use of the GPU that
+ * always holds; when other kernels may occupy SMs for long (another stream, MPS), run with
+ * CTS_FUSED=0 -- the two-launch path has no inter-CTA waits.
  * Deterministic (no float atomics; the reduction order does not depend on scheduling).
  * Host validation: CTS_ERR_INVALID_ARGUMENT (null, x/y overlap), CTS_ERR_SHAPE (module index,
  * ld_x < d_in, ld_y < d_out, ld or pointer not 16-byte aligned). */
