@@ -219,7 +219,8 @@ cts_status_t cts_project(cts_plan_t plan, int32_t module, const void* x, int64_t
  *   U [d_out][r], V [d_in][r]: IN the initial bases (orthonormal columns; the paper fixes no
  *                 initialization), OUT the result (U = out_basis, V = in_basis of the bank)
  *   sigma [n][r][r]: OUT, row = out index (the bank's Sigma layout before bf16 rounding)
- * r in {8, 16, 32, 64} (else CTS_ERR_UNSUPPORTED); d_in, d_out >= r.  workspace: device, >=
+ * r in {8, 16, 32, 64} (else CTS_ERR_UNSUPPORTED); d_in, d_out >= r and multiples of 4, the
+ * factor and basis pointers 16-byte aligned (else CTS_ERR_SHAPE).  workspace: device, >=
  * cts_jd_workspace_bytes(...), 16-byte aligned (CTS_ERR_SHAPE otherwise).  No normalization is
  * applied (do it on the factors beforehand, Sec. 6.1, if wanted).  Stream-ordered, deterministic.
  */
@@ -246,7 +247,7 @@ const char* cts_status_string(cts_status_t status);
  * plans; launches recorded into a CUDA graph under stream capture count once, at capture).  The
  * difference across a call sequence is that sequence's kernel count: cts_segment = 1,
  * cts_apply / cts_apply_group = 1 (fused kernel; 2 with CTS_FUSED=0), cts_shrink* = cts_expand* = 1,
- * cts_expand_reduced_group = 2, cts_project = 2, cts_jd_eigen_iteration = 12 per iteration + 3 per
+ * cts_expand_reduced_group = 2, cts_project = 2, cts_jd_eigen_iteration = 16 per iteration + 5 per
  * batch of 32 problems,
  * cts_bank_load = 3 per module.  Never fails. */
 uint64_t cts_launch_count(void);

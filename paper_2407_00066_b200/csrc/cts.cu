@@ -543,7 +543,9 @@ cts_status_t launch_project(cts_plan_t p, int32_t module, const void* x, int64_t
 size_t jd_problem_floats(const cts_jd_problem_t& q, int r) {
   const size_t K = size_t(q.n) * q.r_i;
   const size_t gb = (size_t(q.d_in) + 255) / 256 + (size_t(q.d_out) + 255) / 256;
-  return 4 * K * r + size_t(q.d_in + q.d_out) * r + gb * r * r + 64;   // P, Q, W, Z, U0, V0, Gram partials
+  const size_t dmax = size_t(std::max(q.d_in, q.d_out));
+  const size_t part = std::max((dmax + kJdSeg - 1) / kJdSeg * K, (K + kJdKSeg - 1) / kJdKSeg * dmax) * r;
+  return 4 * K * r + size_t(q.d_in + q.d_out) * r + gb * r * r + part + 64;   // + Gram, segment partials
 }
 
 template <int R>
@@ -571,36 +573,45 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
       p.U0 = w; w += size_t(q.d_out) * R;
       p.V0 = w; w += size_t(q.d_in) * R;
       p.Gu = w; w += (size_t(q.d_out) + 255) / 256 * R * R;
-      p.Gv = w;
+      p.Gv = w; w += (size_t(q.d_in) + 255) / 256 * R * R;
+      p.part = w;
       ws += jd_problem_floats(q, R);
       kmax = std::max<int>(kmax, int(K));
       dmax = std::max({dmax, q.d_in, q.d_out});
       nmax = std::max(nmax, q.n);
       rimax = std::max(rimax, q.r_i);
     }
-    const dim3 g_rows((kmax + 31) / 32, 1, jb.count), g_cols((dmax + 63) / 64, 1, jb.count);
+    const dim3 g_rows((kmax + 63) / 64, (dmax + kJdSeg - 1) / kJdSeg, jb.count);
+    const dim3 g_cols((dmax + 127) / 128, (kmax + kJdKSeg - 1) / kJdKSeg, jb.count);
+    const dim3 g_red(std::max(1, kmax * R / 1024), jb.count), g_cred(std::max(1, dmax * R / 1024), jb.count);
     const dim3 g_small(nmax, jb.count), g_gram((dmax + kJdGramRows - 1) / kJdGramRows, jb.count, 2);
     const dim3 g_one(1, jb.count, 2), g_ew(std::max(1, dmax * R / 256 / 4), jb.count, 2);
     const size_t small_smem = (2 * size_t(rimax) * R + R * R) * 4;
     if (small_smem > 96 * 1024) return CTS_ERR_SHAPE;
     for (int it = 0; it < iters; ++it) {
       jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 0);
+      jd_rows_reduce<R><<<g_red, 256, 0, stream>>>(jb, 0);
       jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 1);
+      jd_rows_reduce<R><<<g_red, 256, 0, stream>>>(jb, 1);
       jd_small<R><<<g_small, 256, small_smem, stream>>>(jb);
       jd_cols_times<R><<<g_cols, 256, 0, stream>>>(jb, 0);
+      jd_cols_reduce<R><<<g_cred, 256, 0, stream>>>(jb, 0);
       jd_cols_times<R><<<g_cols, 256, 0, stream>>>(jb, 1);
+      jd_cols_reduce<R><<<g_cred, 256, 0, stream>>>(jb, 1);
       for (int pass = 0; pass < 2; ++pass) {
         jd_gram<R><<<g_gram, 256, 0, stream>>>(jb, pass);
         jd_chol<R><<<g_one, 32, 0, stream>>>(jb, pass);
         jd_apply<R><<<g_ew, 256, 0, stream>>>(jb, pass);
       }
       jd_copy_back<R><<<g_ew, 256, 0, stream>>>(jb);
-      g_launches.fetch_add(12, std::memory_order_relaxed);
+      g_launches.fetch_add(16, std::memory_order_relaxed);
     }
     jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 0);
+    jd_rows_reduce<R><<<g_red, 256, 0, stream>>>(jb, 0);
     jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 1);
+    jd_rows_reduce<R><<<g_red, 256, 0, stream>>>(jb, 1);
     jd_sigma<R><<<g_small, 256, 0, stream>>>(jb);
-    g_launches.fetch_add(3, std::memory_order_relaxed);
+    g_launches.fetch_add(5, std::memory_order_relaxed);
     CTS_CUDA(cudaGetLastError());
   }
   return CTS_OK;
@@ -1018,7 +1029,8 @@ cts_status_t cts_jd_eigen_iteration(const cts_jd_problem_t* problems, int32_t co
   for (int i = 0; i < count; ++i) {
     const cts_jd_problem_t& q = problems[i];
     if (!q.a_stack || !q.bt_stack || !q.U || !q.V || !q.sigma) return CTS_ERR_INVALID_ARGUMENT;
-    if (q.n < 1 || q.r_i < 1 || q.d_in < r || q.d_out < r) return CTS_ERR_SHAPE;
+    if (q.n < 1 || q.r_i < 1 || q.d_in < r || q.d_out < r || q.d_in % 4 || q.d_out % 4) return CTS_ERR_SHAPE;
+    if (!aligned16(q.a_stack) || !aligned16(q.bt_stack) || !aligned16(q.U) || !aligned16(q.V)) return CTS_ERR_SHAPE;
   }
   float* ws = static_cast<float*>(workspace);
   switch (r) {

@@ -34,6 +34,7 @@ struct JdProblem {
   float* Z;              // [n*r_i][R]
   float* U0;             // [d_out][R]
   float* V0;             // [d_in][R]
+  float* part;           // partials: [ceil(d/1024)][n*r_i][R] of P / Q, [ceil(n*r_i/128)][d][R] of U0 / V0
   float* Gu;             // [ceil(d_out/256)][R][R] partial Gram matrices; slot 0 then holds R^-1
   float* Gv;             // [ceil(d_in/256)][R][R]
   int n, ri, d_in, d_out;
@@ -44,45 +45,89 @@ struct JdBatch {
   int count;
 };
 
-// out[K][R] = X[K][d] * Y[d][R]; block = 32 rows of X, thread (row, column group of R/8)
+// out[K][R] = X[K][d] * Y[d][R], split over d: block (row block of 64, d segment of kJdSeg) writes a
+// partial [seg][K][R] to the workspace (jd_rows_reduce sums the segments in order -- deterministic).
+// Chunks of 64 d: X [64 x 64] and Y [64 x R] staged by float4 loads; thread = (row, 4 columns).
+constexpr int kJdSeg = 1024;
+
 template <int R>
 __global__ void __launch_bounds__(256) jd_rows_times(const __grid_constant__ JdBatch b, int which) {
   const JdProblem& p = b.pr[blockIdx.z];
   const float* X = which == 0 ? p.a : p.bt;          // 0: P = A V, 1: Q = Bt U
   const float* Y = which == 0 ? p.V : p.U;
-  float* out = which == 0 ? p.P : p.Q;
   const int d = which == 0 ? p.d_in : p.d_out;
   const int K = p.n * p.ri;
-  const int row0 = blockIdx.x * 32;
-  if (row0 >= K) return;
-  __shared__ float xs[32][65];
+  const int row0 = blockIdx.x * 64, d_lo = blockIdx.y * kJdSeg;
+  if (row0 >= K || d_lo >= d) return;
+  const int d_hi = min(d, d_lo + kJdSeg);
+  float* part = p.part + (static_cast<size_t>(blockIdx.y) * K) * R;
+  __shared__ float4 xs4[64][16 + 1];                   // [row][64 d as 16 float4] (+1 float4 pad)
   __shared__ float ys[64][R];
-  constexpr int CG = R / 8;                             // columns per thread
-  const int tr = threadIdx.x >> 3, tc = (threadIdx.x & 7) * CG;
-  float acc[CG];
+  constexpr int RQ = R / 4;                            // threads per row (4 columns each)
+  constexpr int RPB = 256 / RQ;                        // rows computed per pass
+  const int tr = threadIdx.x / RQ, tc = (threadIdx.x % RQ) * 4;
+  float acc[(64 + RPB - 1) / RPB][4];
 #pragma unroll
-  for (int c = 0; c < CG; ++c) acc[c] = 0.f;
-  for (int d0 = 0; d0 < d; d0 += 64) {
-    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
-      const int r = i >> 6, c = i & 63;
-      xs[r][c] = (row0 + r < K && d0 + c < d) ? X[static_cast<size_t>(row0 + r) * d + d0 + c] : 0.f;
+  for (int q = 0; q < (64 + RPB - 1) / RPB; ++q)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[q][c] = 0.f;
+  for (int d0 = d_lo; d0 < d_hi; d0 += 64) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      const int r = i >> 4, c4 = i & 15;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row0 + r < K && d0 + 4 * c4 < d_hi)
+        v = *reinterpret_cast<const float4*>(X + static_cast<size_t>(row0 + r) * d + d0 + 4 * c4);
+      xs4[r][c4] = v;
     }
-    for (int i = threadIdx.x; i < 64 * R; i += 256) {
-      const int r = i / R, c = i % R;
-      ys[r][c] = d0 + r < d ? Y[static_cast<size_t>(d0 + r) * R + c] : 0.f;
+    for (int i = threadIdx.x; i < 64 * R / 4; i += 256) {
+      const int r = i / (R / 4), c4 = i % (R / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (d0 + r < d_hi) v = *reinterpret_cast<const float4*>(Y + static_cast<size_t>(d0 + r) * R + 4 * c4);
+      *reinterpret_cast<float4*>(&ys[r][4 * c4]) = v;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int k = 0; k < 64; ++k) {
-      const float xv = xs[tr][k];
 #pragma unroll
-      for (int c = 0; c < CG; ++c) acc[c] = fmaf(xv, ys[k][tc + c], acc[c]);
+    for (int q = 0; q < (64 + RPB - 1) / RPB; ++q) {
+      const int r = tr + q * RPB;
+      if (r < 64) {
+#pragma unroll 4
+        for (int k4 = 0; k4 < 16; ++k4) {
+          const float4 xv = xs4[r][k4];
+          const float xk[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 yv = *reinterpret_cast<const float4*>(&ys[4 * k4 + u][tc]);
+            acc[q][0] = fmaf(xk[u], yv.x, acc[q][0]);
+            acc[q][1] = fmaf(xk[u], yv.y, acc[q][1]);
+            acc[q][2] = fmaf(xk[u], yv.z, acc[q][2]);
+            acc[q][3] = fmaf(xk[u], yv.w, acc[q][3]);
+          }
+        }
+      }
     }
     __syncthreads();
   }
-  if (row0 + tr < K) {
 #pragma unroll
-    for (int c = 0; c < CG; ++c) out[static_cast<size_t>(row0 + tr) * R + tc + c] = acc[c];
+  for (int q = 0; q < (64 + RPB - 1) / RPB; ++q) {
+    const int r = tr + q * RPB;
+    if (r < 64 && row0 + r < K)
+      *reinterpret_cast<float4*>(part + static_cast<size_t>(row0 + r) * R + tc) =
+          make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+  }
+}
+
+// out = sum over d segments of the partials, in segment order
+template <int R>
+__global__ void __launch_bounds__(256) jd_rows_reduce(const __grid_constant__ JdBatch b, int which) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  float* out = which == 0 ? p.P : p.Q;
+  const int d = which == 0 ? p.d_in : p.d_out;
+  const int K = p.n * p.ri;
+  const int S = (d + kJdSeg - 1) / kJdSeg;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K * R; i += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int g = 0; g < S; ++g) s += p.part[static_cast<size_t>(g) * K * R + i];
+    out[i] = s;
   }
 }
 
@@ -121,32 +166,40 @@ __global__ void __launch_bounds__(256) jd_small(const __grid_constant__ JdBatch 
   }
 }
 
-// out[d][R] = X[K][d]^T * M[K][R]; block = 64 columns of X, thread (column, group of R/4)
+// out[d][R] = X[K][d]^T * M[K][R], split over K: block (128 columns of d, K segment of kJdKSeg rows)
+// writes a partial [kseg][d][R] (jd_cols_reduce sums the segments in order); X chunks [32 x 128] by
+// float4 loads; thread = (column, half of the R outputs).
+constexpr int kJdKSeg = 128;
+
 template <int R>
 __global__ void __launch_bounds__(256) jd_cols_times(const __grid_constant__ JdBatch b, int which) {
   const JdProblem& p = b.pr[blockIdx.z];
   const float* X = which == 0 ? p.bt : p.a;           // 0: U0 = Bt^T W, 1: V0 = A^T Z
   const float* Mt = which == 0 ? p.W : p.Z;
-  float* out = which == 0 ? p.U0 : p.V0;
   const int d = which == 0 ? p.d_out : p.d_in;
   const int K = p.n * p.ri;
-  const int col0 = blockIdx.x * 64;
-  if (col0 >= d) return;
-  __shared__ float xs[32][64];
+  const int col0 = blockIdx.x * 128, k_lo = blockIdx.y * kJdKSeg;
+  if (col0 >= d || k_lo >= K) return;
+  const int k_hi = min(K, k_lo + kJdKSeg);
+  float* part = p.part + static_cast<size_t>(blockIdx.y) * d * R;
+  __shared__ float xs[32][128 + 4];
   __shared__ float ms[32][R];
-  constexpr int CG = R / 4;
-  const int tcol = threadIdx.x & 63, tg = (threadIdx.x >> 6) * CG;
+  constexpr int CG = R / 2;
+  const int tcol = threadIdx.x & 127, tg = (threadIdx.x >> 7) * CG;
   float acc[CG];
 #pragma unroll
   for (int c = 0; c < CG; ++c) acc[c] = 0.f;
-  for (int k0 = 0; k0 < K; k0 += 32) {
-    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
-      const int r = i >> 6, c = i & 63;
-      xs[r][c] = (k0 + r < K && col0 + c < d) ? X[static_cast<size_t>(k0 + r) * d + col0 + c] : 0.f;
+  for (int k0 = k_lo; k0 < k_hi; k0 += 32) {
+    for (int i = threadIdx.x; i < 32 * 32; i += 256) {
+      const int r = i >> 5, c4 = i & 31;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k0 + r < k_hi && col0 + 4 * c4 < d)
+        v = *reinterpret_cast<const float4*>(X + static_cast<size_t>(k0 + r) * d + col0 + 4 * c4);
+      xs[r][4 * c4] = v.x; xs[r][4 * c4 + 1] = v.y; xs[r][4 * c4 + 2] = v.z; xs[r][4 * c4 + 3] = v.w;
     }
     for (int i = threadIdx.x; i < 32 * R; i += 256) {
       const int r = i / R, c = i % R;
-      ms[r][c] = k0 + r < K ? Mt[static_cast<size_t>(k0 + r) * R + c] : 0.f;
+      ms[r][c] = k0 + r < k_hi ? Mt[static_cast<size_t>(k0 + r) * R + c] : 0.f;
     }
     __syncthreads();
 #pragma unroll 8
@@ -159,7 +212,21 @@ __global__ void __launch_bounds__(256) jd_cols_times(const __grid_constant__ JdB
   }
   if (col0 + tcol < d) {
 #pragma unroll
-    for (int c = 0; c < CG; ++c) out[static_cast<size_t>(col0 + tcol) * R + tg + c] = acc[c];
+    for (int c = 0; c < CG; ++c) part[static_cast<size_t>(col0 + tcol) * R + tg + c] = acc[c];
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) jd_cols_reduce(const __grid_constant__ JdBatch b, int which) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  float* out = which == 0 ? p.U0 : p.V0;
+  const int d = which == 0 ? p.d_out : p.d_in;
+  const int K = p.n * p.ri;
+  const int S = (K + kJdKSeg - 1) / kJdKSeg;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d * R; i += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int g = 0; g < S; ++g) s += p.part[static_cast<size_t>(g) * d * R + i];
+    out[i] = s;
   }
 }
 
