@@ -236,6 +236,25 @@ cts_status_t cts_jd_workspace_bytes(const cts_jd_problem_t* problems, int32_t co
 cts_status_t cts_jd_eigen_iteration(const cts_jd_problem_t* problems, int32_t count, int32_t r, int32_t iters,
                                     void* workspace, size_t ws_bytes, cudaStream_t stream);
 
+/*
+ * Cluster-affinity placement across GPUs ("clustering offers opportunities for
+ * efficient scheduling"): each rank holds the bases of the clusters it owns only, and
+ * tokens travel to the owner of their cluster (an all-to-all of rows, as in expert parallelism).
+ * The collective itself is the caller's (NCCL all-to-all through torch.distributed, placement.py);
+ * these two kernels build and apply the routing.
+ * cts_route: token_adapter [T] (device, -1 = none), owner [N] (device, adapter -> rank in
+ *   [0, world)); writes perm [T] (device) = token indices stably partitioned by destination rank
+ *   (tokens without an adapter go to `self`) and counts [world] (device).  world <= 64.
+ * cts_rows_move: rows of row_bytes bytes (activation rows or int32 ids; a multiple of 4):
+ *   scatter == 0: dst[k] = src[idx[k]] (gather), else dst[idx[k]] = src[k]; ld_src / ld_dst are
+ *   row strides in BYTES (multiples of 4), idx [n] device int32.  Stream-ordered;
+ *   CTS_ERR_INVALID_ARGUMENT / CTS_ERR_SHAPE on bad arguments.
+ */
+cts_status_t cts_route(const int32_t* token_adapter, int32_t T, const int32_t* owner, int32_t N, int32_t world,
+                       int32_t self, int32_t* perm, int32_t* counts, cudaStream_t stream);
+cts_status_t cts_rows_move(const void* src, int64_t ld_src, void* dst, int64_t ld_dst, const int32_t* idx, int32_t n,
+                           int32_t row_bytes, int32_t scatter, cudaStream_t stream);
+
 /* Read the plan's device error word (call after synchronizing the stream that ran cts_segment).
  * *code = CTS_OK or CTS_ERR_INDEX_OUT_OF_RANGE; *first_bad_token = smallest offending t or -1. */
 cts_status_t cts_plan_error(cts_plan_t plan, int32_t* code, int32_t* first_bad_token);

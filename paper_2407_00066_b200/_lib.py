@@ -26,7 +26,7 @@ EXPORTS = (
     "cts_segment", "cts_segment_readback", "cts_apply", "cts_shrink", "cts_expand",
     "cts_apply_group", "cts_shrink_group", "cts_expand_group", "cts_plan_error", "cts_status_string",
     "cts_launch_count", "cts_plan_partial_elems", "cts_shrink_partial_group", "cts_expand_reduced_group",
-    "cts_project", "cts_jd_workspace_bytes", "cts_jd_eigen_iteration",
+    "cts_project", "cts_jd_workspace_bytes", "cts_jd_eigen_iteration", "cts_route", "cts_rows_move",
 )
 
 
@@ -110,6 +110,8 @@ def lib():
         "cts_project": ([P, I32, VP, I64, VP, I64, VP, I64, F, P], I32),
         "cts_jd_workspace_bytes": ([ctypes.POINTER(JdProblem), I32, I32, ctypes.POINTER(ctypes.c_size_t)], I32),
         "cts_jd_eigen_iteration": ([ctypes.POINTER(JdProblem), I32, I32, I32, VP, ctypes.c_size_t, P], I32),
+        "cts_route": ([VP, I32, VP, I32, I32, I32, VP, VP, P], I32),
+        "cts_rows_move": ([VP, I64, VP, I64, VP, I32, I32, I32, P], I32),
     }
     for name, (argt, rest) in sig.items():
         f = getattr(L, name)

@@ -158,6 +158,33 @@ def cts_jd_eigen_iteration(problems, r, iters, stream=None):
     return ws          # keep alive until the stream has consumed it
 
 
+def cts_route(token_adapter, owner, world, self_rank, stream=None):
+    """Cluster-affinity routing: (perm [T], counts [world]) int32 CUDA tensors; perm = token indices
+    stably partitioned by the rank that owns each token's adapter (owner [N] int32)."""
+    T = token_adapter.shape[0]
+    perm = torch.empty(max(T, 1), dtype=torch.int32, device=token_adapter.device)
+    counts = torch.empty(world, dtype=torch.int32, device=token_adapter.device)
+    check("cts_route", lib().cts_route(ctypes.c_void_p(token_adapter.data_ptr()), T,
+                                       ctypes.c_void_p(owner.data_ptr()), owner.shape[0], int(world), int(self_rank),
+                                       ctypes.c_void_p(perm.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
+                                       _stream_handle(stream)))
+    return perm[:T], counts
+
+
+def cts_rows_move(src, dst, idx, scatter, stream=None):
+    """Rows of a 2-D CUDA tensor (bf16 activations or int32 ids as [n, 1]): dst[k] = src[idx[k]]
+    (scatter=False) or dst[idx[k]] = src[k] (scatter=True)."""
+    for t, nm in ((src, "src"), (dst, "dst")):
+        if not t.is_cuda or t.dim() != 2 or t.stride(1) != 1 or t.dtype != src.dtype:
+            raise TypeError(f"{nm} must be a 2-D CUDA tensor with unit inner stride and src's dtype")
+    es = src.element_size()
+    n = idx.shape[0]
+    check("cts_rows_move", lib().cts_rows_move(ctypes.c_void_p(src.data_ptr()), src.stride(0) * es,
+                                               ctypes.c_void_p(dst.data_ptr()), dst.stride(0) * es,
+                                               ctypes.c_void_p(idx.data_ptr()), n, src.shape[1] * es,
+                                               int(bool(scatter)), _stream_handle(stream)))
+
+
 def cts_shrink(plan, module, x, scale=1.0, stream=None):
     """Kernel 1 only: t = scale * Sigma_i V_c^T x_t into the plan's scratch for `module`."""
     if x.dtype != torch.bfloat16 or not x.is_cuda or x.dim() != 2 or x.stride(1) != 1:

@@ -1041,6 +1041,37 @@ cts_status_t cts_jd_eigen_iteration(const cts_jd_problem_t* problems, int32_t co
   }
 }
 
+cts_status_t cts_route(const int32_t* token_adapter, int32_t T, const int32_t* owner, int32_t N, int32_t world,
+                       int32_t self, int32_t* perm, int32_t* counts, cudaStream_t stream) {
+  if (T < 0 || N < 1 || world < 1 || world > 64 || self < 0 || self >= world || !owner || !counts ||
+      (T > 0 && (!token_adapter || !perm)))
+    return CTS_ERR_INVALID_ARGUMENT;
+  RouteArgs a{token_adapter, owner, perm, counts, T, N, world, self};
+  route_kernel<<<1, kSegThreads, 0, stream>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CTS_CUDA(cudaGetLastError());
+  return CTS_OK;
+}
+
+cts_status_t cts_rows_move(const void* src, int64_t ld_src, void* dst, int64_t ld_dst, const int32_t* idx, int32_t n,
+                           int32_t row_bytes, int32_t scatter, cudaStream_t stream) {
+  if (n < 0 || row_bytes < 4 || (n > 0 && (!src || !dst || !idx))) return CTS_ERR_INVALID_ARGUMENT;
+  if (row_bytes % 4 || ld_src < row_bytes || ld_dst < row_bytes || ld_src % 4 || ld_dst % 4 ||
+      reinterpret_cast<uintptr_t>(src) % 4 || reinterpret_cast<uintptr_t>(dst) % 4)
+    return CTS_ERR_SHAPE;
+  if (n == 0) return CTS_OK;
+  RowsArgs a{static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), idx, ld_src, ld_dst, n, row_bytes,
+             scatter ? 1 : 0};
+  const bool v16 = row_bytes % 16 == 0 && ld_src % 16 == 0 && ld_dst % 16 == 0 && aligned16(src) && aligned16(dst);
+  const int64_t chunks = int64_t(n) * (row_bytes / (v16 ? 16 : 4));
+  const int grid = static_cast<int>(std::min<int64_t>(8 * sm_count(), (chunks + 255) / 256));
+  if (v16) rows_move_kernel<uint4><<<grid, 256, 0, stream>>>(a);
+  else rows_move_kernel<uint32_t><<<grid, 256, 0, stream>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CTS_CUDA(cudaGetLastError());
+  return CTS_OK;
+}
+
 #ifdef CTS_TRACE
 // debug-only (not part of cts.h): copy the per-CTA timeline of the last traced launch
 int cts_debug_trace(unsigned long long* host, int n) {

@@ -270,3 +270,66 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
 }
 
 }  // namespace cts
+
+namespace cts {
+
+// ------------------------------------------------------------------ cluster-affinity routing
+// SURVEY 8(f) NEXT 4 ("clustering offers opportunities for efficient scheduling"): tokens
+// go to the rank that owns their cluster.  route_kernel: one 1024-thread CTA; dest[t] =
+// owner[adapter[t]] (unbound tokens stay on `self`); perm = token indices stably partitioned by
+// destination rank, counts[r] = tokens for rank r.  Per destination a block scan per 1024-token
+// chunk (world <= 64): deterministic, no atomics.
+struct RouteArgs {
+  const int32_t* token_adapter;  // [T]
+  const int32_t* owner;          // [N] adapter -> rank
+  int32_t* perm;                 // [T]
+  int32_t* counts;               // [world]
+  int T, N, world, self;
+};
+
+__global__ void __launch_bounds__(kSegThreads, 1) route_kernel(RouteArgs a) {
+  __shared__ int warp_sums[33];
+  int base = 0;
+  for (int r = 0; r < a.world; ++r) {
+    const int start = base;
+    for (int t0 = 0; t0 < a.T; t0 += kSegThreads) {
+      const int t = t0 + threadIdx.x;
+      int dst = -1;
+      if (t < a.T) {
+        const int id = a.token_adapter[t];
+        dst = (id >= 0 && id < a.N) ? a.owner[id] : a.self;
+      }
+      const int f = dst == r ? 1 : 0;
+      int total;
+      const int pos = block_exclusive_scan(f, warp_sums, total);
+      if (f) a.perm[base + pos] = t;
+      base += total;
+    }
+    if (threadIdx.x == 0) a.counts[r] = base - start;
+  }
+}
+
+// dst[k] = src[idx[k]] (gather) or dst[idx[k]] = src[k] (scatter) for rows of row_bytes bytes:
+// 16-byte chunks when rows and strides are 16-byte multiples (bf16 activations), else 4-byte
+// chunks (int32 token ids)
+struct RowsArgs {
+  const uint8_t* src;
+  uint8_t* dst;
+  const int32_t* idx;
+  int64_t ld_src, ld_dst;        // bytes
+  int n, row_bytes, scatter;
+};
+
+template <typename V>
+__global__ void __launch_bounds__(256) rows_move_kernel(RowsArgs a) {
+  const int chunks = a.row_bytes / static_cast<int>(sizeof(V));
+  const int64_t total = static_cast<int64_t>(a.n) * chunks;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i / chunks), c = static_cast<int>(i % chunks);
+    const int64_t sr = a.scatter ? k : a.idx[k], dr = a.scatter ? a.idx[k] : k;
+    *reinterpret_cast<V*>(a.dst + dr * a.ld_dst + c * sizeof(V)) =
+        *reinterpret_cast<const V*>(a.src + sr * a.ld_src + c * sizeof(V));
+  }
+}
+
+}  // namespace cts

@@ -123,3 +123,87 @@ def test_shard_bounds_validation():
         shard_bounds(1024, 0, 32)           # 32-column slices: not a multiple of 64
     with pytest.raises(ValueError):
         shard_bounds(4096, 8, 8)
+
+
+# ---------------------------------------------------------------- cluster-affinity placement (2 ranks)
+def _affinity_worker(rank, world, port, q):
+    import numpy as np
+
+    from oracle import apply_ref
+    from paper_2407_00066_b200.placement import adapter_owner, affinity_apply_group, shard_bank_by_cluster
+    from workloads import cluster_map, decode_tokens, direct_bank
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    N, C, r, d_in, d_out, T = 40, 6, 4, 32, 24, 30
+    cmap = cluster_map(N, C, 3)                                   # ONE map shared by the group
+    banks = [direct_bank(d_in, d_out, N, C, r, seed=10 + m, cluster_of=cmap) for m in range(2)]
+    full = [{k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in b.items()} for b in banks]
+    shard = [shard_bank_by_cluster(b["in_basis"], b["out_basis"], b["cluster_of"], rank, world) for b in full]
+    owner = adapter_owner(full[0]["cluster_of"], world)
+    tokens = torch.from_numpy(decode_tokens(T, N, 5 + rank, frac_none=0.1))
+    g = torch.Generator().manual_seed(7 + rank)
+    x = torch.randn(T, d_in, generator=g, dtype=torch.float64)
+    ys = [torch.randn(T, d_out, generator=g, dtype=torch.float64) for _ in range(2)]
+    y0 = [y.clone() for y in ys]
+
+    def route(tok):                                               # stand-in for cts_route
+        dest = torch.where(tok >= 0, owner[tok.clamp(min=0)], torch.full_like(tok, rank))
+        perm = torch.from_numpy(np.argsort(dest.numpy(), kind="stable").astype(np.int64))
+        return perm, [int((dest == k).sum()) for k in range(world)]
+
+    def gather(src, perm):
+        return src[perm].contiguous()
+
+    def scatter(dst, src, perm):
+        dst[perm] = src
+
+    def all_to_all(send, send_counts):
+        cnt = torch.tensor(send_counts)
+        rc = torch.empty_like(cnt)
+        dist.all_to_all_single(rc, cnt)
+        recv = torch.empty((int(rc.sum()), send.shape[1]), dtype=send.dtype)
+        dist.all_to_all_single(recv, send.contiguous(), rc.tolist(), send_counts)
+        return recv, rc.tolist()
+
+    seen = []
+
+    def apply_local(modules, ids, xr, yr, scale):                 # stand-in: the oracle on the shard
+        seen.append(ids.clone())
+        for m, y in zip(modules, yr):
+            inb, outb, lmap = shard[m]
+            dy, _ = apply_ref(xr.numpy(), ids.numpy(), lmap.numpy(), inb.numpy(), outb.numpy(),
+                              full[m]["sigma"].numpy(), scale)
+            y += torch.from_numpy(dy)
+
+    affinity_apply_group([0, 1], x, ys, tokens, 2.0, route, gather, scatter, all_to_all, apply_local)
+    err = 0.0
+    for m in range(2):
+        dy, _ = apply_ref(x.numpy(), tokens.numpy(), cmap, banks[m]["in_basis"], banks[m]["out_basis"],
+                          banks[m]["sigma"], 2.0)
+        err = max(err, float(np.max(np.abs(ys[m].numpy() - (y0[m].numpy() + dy)))))
+    ids = seen[0].numpy()
+    owned_ok = bool(np.all((ids < 0) | (owner.numpy()[np.maximum(ids, 0)] == rank)))
+    q.put((rank, err, owned_ok, int(shard[0][0].shape[0])))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_cluster_affinity_placement():
+    """each rank keeps half the clusters' bases, tokens travel to their
+    cluster's owner and back; every rank's y equals the oracle on the FULL bank, and every token a
+    rank processed belongs to a cluster it owns (or has no adapter)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_affinity_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, err, owned_ok, n_clusters in res:
+        assert err < 1e-10, (rank, err)
+        assert owned_ok
+        assert n_clusters == 3                                     # 6 clusters over 2 ranks

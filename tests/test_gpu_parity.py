@@ -639,3 +639,63 @@ def test_maximum_clusters_singletons(cts):
     check_delta(ta, got, f64, x, 1.0)
     plan.close()
     bank.close()
+
+
+# ---------------------------------------------------------------- cluster-affinity placement
+def test_route_and_rows_move_exact(cts):
+    """cts_route == a stable partition of the token indices by owning rank (unbound tokens to
+    `self`), bit-exact; cts_rows_move gathers / scatters bf16 and int32 rows exactly."""
+    g = np.random.default_rng(90)
+    N, T, world, me = 300, 777, 4, 2
+    owner = g.integers(0, world, N).astype(np.int32)
+    ta = decode_tokens(T, N, 91, frac_none=0.1)
+    perm, counts = cts.cts_route(torch.from_numpy(ta).cuda(), torch.from_numpy(owner).cuda(), world, me)
+    dest = np.where(ta >= 0, owner[np.maximum(ta, 0)], me)
+    assert np.array_equal(perm.cpu().numpy(), np.argsort(dest, kind="stable"))
+    assert np.array_equal(counts.cpu().numpy(), np.bincount(dest, minlength=world))
+    x = torch.randn(T, 96, device="cuda").to(torch.bfloat16)
+    p = perm.long()
+    out = torch.empty_like(x)
+    cts.cts_rows_move(x, out, perm, scatter=False)
+    assert torch.equal(out, x[p])
+    back = torch.empty_like(x)
+    cts.cts_rows_move(out, back, perm, scatter=True)
+    assert torch.equal(back, x)
+    ids = torch.from_numpy(ta).cuda()[:, None]
+    ids_out = torch.empty_like(ids)
+    cts.cts_rows_move(ids, ids_out, perm, scatter=False)
+    assert torch.equal(ids_out[:, 0], ids[p, 0])
+
+
+def test_cluster_affinity_single_rank(cts):
+    """ClusterAffinityApply end to end on one GPU (world = 1, NCCL): route, pack, all-to-all,
+    segment + grouped apply on the (whole) shard, return, scatter -- y vs the oracle."""
+    import os
+
+    import torch.distributed as dist
+    from paper_2407_00066_b200.placement import ClusterAffinityApply, adapter_owner, shard_bank_by_cluster
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29561")
+    own_pg = not dist.is_initialized()
+    if own_pg:
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    N, C, r, T = 200, 8, 16, 300
+    cmap = cluster_map(N, C, 92)
+    mods = [(512, 384), (512, 256)]
+    bits, f64 = zip(*[quantized_bank(di, do, N, C, r, seed=93 + m, cluster_of=cmap) for m, (di, do) in enumerate(mods)])
+    shards = [shard_bank_by_cluster(dev_bf16(b["in_basis"]), dev_bf16(b["out_basis"]),
+                                    torch.from_numpy(b["cluster_of"]).cuda(), 0, 1) for b in bits]
+    bank = cts.Bank([s[0] for s in shards], [s[1] for s in shards], [dev_bf16(b["sigma"]) for b in bits],
+                    [s[2] for s in shards])
+    ta = decode_tokens(T, N, 94, frac_none=0.1)
+    aff = ClusterAffinityApply(bank, adapter_owner(torch.from_numpy(cmap).cuda(), 1), T, 1, 0)
+    x = bf16_round(activations(T, 512, 95))
+    ys = [dev_bf16(np.zeros((T, do), np.uint16)) for (_, do) in mods]
+    aff.apply_group([0, 1], dev_bf16(x), ys, torch.from_numpy(ta).cuda(), 2.0)
+    torch.cuda.synchronize()
+    for m in range(2):
+        check_delta(ta, host_bits(ys[m]), f64[m], x, 2.0)
+    aff.plan.close()
+    bank.close()
+    if own_pg:
+        dist.destroy_process_group()
