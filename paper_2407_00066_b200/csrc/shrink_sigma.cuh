@@ -51,6 +51,9 @@ constexpr int kEpiSets = 2;             // epilogue warp-sets working on alterna
 constexpr int kApplyThreads = 32 * (kProducerWarps + 1 + 4 * kEpiSets);   // producers, MMA, epilogue
 constexpr int kShrinkThreads = kApplyThreads;
 constexpr int kShrinkAccSlots = 4;
+#ifndef CTS_SHRINK_STAGES
+#define CTS_SHRINK_STAGES 8   // x / in_basis ring depth cap (the fused kernel shares its arena with the expand)
+#endif
 #ifndef CTS_KCHUNK_NUM
 #define CTS_KCHUNK_NUM 48   // finisher: partials fetched per L2 round trip = CTS_KCHUNK_NUM / r_pad
 #endif
@@ -88,7 +91,7 @@ struct ShrinkCfg {
   static constexpr int kA = kTileM * 128;           // bytes per A stage (x rows)
   static constexpr int kB1 = RP * 128;              // one in_basis K-slab (rp rows x 64 cols)
   static constexpr int kB = 2 * kB1;                // bytes per B stage: one slab per slot half
-  static constexpr int kStages = (200 * 1024) / (kA + kB) < 8 ? (200 * 1024) / (kA + kB) : 8;  // 8 / 8 / 6
+  static constexpr int kStages = (200 * 1024) / (kA + kB) < CTS_SHRINK_STAGES ? (200 * 1024) / (kA + kB) : CTS_SHRINK_STAGES;
   static constexpr int kOffA = 0;
   static constexpr int kOffB = kOffA + kStages * kA;
   static constexpr int kArena = kOffB + kStages * kB;          // bytes of staged operands
