@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import paper_2407_00066_b200 as cts  # noqa: E402
 from workloads.gen_torch import direct_bank_torch, tokens_torch  # noqa: E402
 
-T, N, C, r = int(os.environ.get("T", 1024)), 1000, 25, 16
+T, N, C, r = int(os.environ.get("T", 1024)), int(os.environ.get("N", 1000)), int(os.environ.get("C", 25)), 16
 dev = torch.device("cuda")
 mods = [(4096, 4096), (4096, 1024), (4096, 1024), (4096, 14336), (4096, 14336)]
 banks = [direct_bank_torch(di, do, N, C, r, seed=m, device=dev, cluster_seed=50 + m) for m, (di, do) in enumerate(mods)]
@@ -41,7 +41,7 @@ for grp in ([0, 1, 2], [3, 4]):
     a = np.array(buf, dtype=np.int64).reshape(160, 24)[:148].astype(np.float64)
     t0 = a[:, 0].min()
     rel = (a - t0) / 1e3
-    print(f"fused group {grp} (T={T}): us after first CTA start: min / median / max over CTAs")
+    print(f"fused group {grp} (T={T}, N={N}, C={C}): us after first CTA start: min / median / max over CTAs")
     for i, n in names.items():
         col = rel[:, i]
         col = col[(col >= 0) & (col < 1e4)]
