@@ -156,7 +156,8 @@ template <int RP> __device__ __forceinline__ int4* stage_info(const ExpandRing& 
 
 // ------------------------------------------------------------------ TMA producers (warps 0-3)
 template <int RP>
-__device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane) {
+__device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane,
+                                int ready_target = 1) {   // fused: arrivals on a slot's "t ready" flag
   using L = ExpandCfg<RP>;
   const ItemMap M = expand_map(p, nt_lane, lane);
   int li = 0;                                     // index over this CTA's items
@@ -179,7 +180,7 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
     const bool poll_late = m.ready != nullptr && early;
     if (m.ready != nullptr && !early) {
       if (lane == 0) {
-        while (ld_acquire_gpu(m.ready + tile) == 0) nanosleep_ns(64);
+        while (ld_acquire_gpu(m.ready + tile) < ready_target) nanosleep_ns(64);
         fence_proxy_async_global();
         if (my == 0) CTS_STAMP(8);
       }
@@ -221,7 +222,7 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
     }
     if (lane == 0) {
       if (poll_late) {                            // fused kernel: t of this slot published?
-        while (ld_acquire_gpu(m.ready + tile) == 0) nanosleep_ns(64);
+        while (ld_acquire_gpu(m.ready + tile) < ready_target) nanosleep_ns(64);
         fence_proxy_async_global();
         if (my == 0) CTS_STAMP(8);                // first expand item's t available
       }

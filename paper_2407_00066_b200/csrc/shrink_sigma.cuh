@@ -51,6 +51,9 @@ constexpr int kEpiSets = 2;             // epilogue warp-sets working on alterna
 constexpr int kApplyThreads = 32 * (kProducerWarps + 1 + 4 * kEpiSets);   // producers, MMA, epilogue
 constexpr int kShrinkThreads = kApplyThreads;
 constexpr int kShrinkAccSlots = 4;
+#ifndef CTS_DIST_FINISH
+#define CTS_DIST_FINISH 1     // r_pad >= 32: every CTA of a split slot finishes 1/ks of its rows
+#endif
 #ifndef CTS_SHRINK_STAGES
 #define CTS_SHRINK_STAGES 8   // x / in_basis ring depth cap (the fused kernel shares its arena with the expand)
 #endif
@@ -156,6 +159,18 @@ struct ShrinkWork {
   int ks;
   ItemMap M;
 };
+
+// Distributed finishing (r_pad >= 32).  The r x r Sigma_i matvec of a 128-row slot reads 128
+// different Sigma_i (8 KB each at r_pad = 64) with one L1 wavefront per lane and 32-byte load: ~40
+// us for the one last-arriving CTA (profiles/r01/decode_tuning/trace_fused_q*.txt).  Instead every
+// CTA of the slot waits until all ks partials are published and finishes rows [kc*128/ks, ...),
+// so the Sigma traffic spreads over ks SMs; the slot's "t ready" flag then counts ks arrivals.
+// Needs every CTA to hold at most one shrink item (all chunks of a slot in flight at once: the
+// floor K split guarantees it when items <= grid) -- the wait is on co-resident CTAs only.
+template <int RP>
+__device__ __forceinline__ bool shrink_dist_finish(const ShrinkWork& W) {
+  return CTS_DIST_FINISH && RP >= 32 && W.ks > 1 && W.M.total <= static_cast<int>(gridDim.x);
+}
 
 // item -> (module g, index within the module); warp-uniform item, all lanes participate
 __device__ __forceinline__ int map_item(const ItemMap& M, int n_mod, int item, int lane, int* local) {
@@ -329,6 +344,123 @@ __device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, const Shr
   }
 }
 
+// Distributed finishing of rows [kc*rpc, (kc+1)*rpc) of a slot (shrink_dist_finish), by the 128
+// threads of one epilogue set: kTpr = 16 threads per row, 8 rows per pass.  Thread `sub` of a row
+// sums the ks partials of its kCols = r_pad/16 columns of s (kc order, as the single finisher),
+// forms partial dot products Sigma_i[o][cols] . s[cols] for every output o (the 16 threads of a
+// row read each Sigma_i row as one contiguous 128-byte line), then a recursive-halving
+// reduce-scatter over the 16 threads leaves it kCols consecutive outputs of t.
+template <int RP>
+__device__ __forceinline__ void dist_finish(const ShrinkMod& m, int tile, int kc, int ks, int rpc, int set_tid,
+                                            int4 t0, int4 t1) {
+  constexpr int kTpr = 16, kCols = RP / kTpr;
+  static_assert(kCols == 2 || kCols == 4, "dist_finish: r_pad 32 or 64");
+  const int sub = set_tid & (kTpr - 1);
+  const int r_end = min((kc + 1) * rpc, kTileM);
+  const float* const wtile = m.ws + static_cast<size_t>(tile) * ks * kTileM * RP;
+  for (int r0 = kc * rpc; r0 < r_end; r0 += kTileM / kTpr) {     // set-uniform trip count
+    const int row = r0 + set_tid / kTpr;
+    const int half = (t1.z > 0 && row >= kTileM / 2) ? 1 : 0;
+    const int slen4 = ((half ? t1.z : t0.z) + 3) & ~3;
+    const bool rvalid = row < r_end && row - half * (kTileM / 2) < slen4;
+    float sc[kCols];
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) sc[c] = 0.f;
+    if (rvalid) {
+      const float* src = wtile + static_cast<size_t>(row) * RP + sub * kCols;
+      constexpr int kB = 8;                                        // partials per L2 round trip
+      for (int q0 = 0; q0 < ks; q0 += kB) {
+        float buf[kB][kCols];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          if (q0 + j < ks) {
+            const float* a = src + static_cast<size_t>(q0 + j) * kTileM * RP;
+            if constexpr (kCols == 4) {
+              const float4 f = __ldcg(reinterpret_cast<const float4*>(a));
+              buf[j][0] = f.x; buf[j][1] = f.y; buf[j][2] = f.z; buf[j][3] = f.w;
+            } else {
+              const float2 f = __ldcg(reinterpret_cast<const float2*>(a));
+              buf[j][0] = f.x; buf[j][1] = f.y;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          if (q0 + j >= ks) break;
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) sc[c] += buf[j][c];
+        }
+      }
+    }
+    const int adapter = rvalid ? m.tile_adapters[tile * kTileM + row] : 0;
+    const __nv_bfloat16* sg = m.sigma + static_cast<size_t>(adapter) * RP * RP + sub * kCols;
+    float v[RP];
+    constexpr int kOB = 16;                                        // Sigma rows per L2 round trip
+#pragma unroll
+    for (int o0 = 0; o0 < RP; o0 += kOB) {
+      uint32_t w[kOB][kCols / 2];
+#pragma unroll
+      for (int j = 0; j < kOB; ++j) {
+        if constexpr (kCols == 4) {
+          const uint2 q = rvalid ? __ldg(reinterpret_cast<const uint2*>(sg + (o0 + j) * RP)) : make_uint2(0, 0);
+          w[j][0] = q.x; w[j][1] = q.y;
+        } else {
+          w[j][0] = rvalid ? __ldg(reinterpret_cast<const unsigned int*>(sg + (o0 + j) * RP)) : 0u;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kOB; ++j) {
+        float acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < kCols / 2; ++e) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j][e]));
+          acc = fmaf(f.x, sc[2 * e], acc);
+          acc = fmaf(f.y, sc[2 * e + 1], acc);
+        }
+        v[o0 + j] = acc;
+      }
+    }
+    int base = 0;                                                  // first output this thread keeps
+#pragma unroll
+    for (int mk = kTpr / 2, n = RP / 2; mk >= 1; mk >>= 1, n >>= 1) {
+      const bool up = (sub & mk) != 0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const float keep = up ? v[n + i] : v[i];
+        const float give = up ? v[i] : v[n + i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, give, mk);
+      }
+      if (up) base += n;
+    }
+    if (rvalid) {
+      if (m.tpart != nullptr) {
+        float* dp = m.tpart + static_cast<size_t>(m.tile_rows[tile * kTileM + row]) * RP + base;
+#pragma unroll
+        for (int i = 0; i < kCols; ++i) dp[i] = v[i] * m.scale;
+      } else {
+        __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP) + base;
+        uint32_t hi[kCols / 2], lo[kCols / 2];
+#pragma unroll
+        for (int e = 0; e < kCols / 2; ++e) {
+          const float a = v[2 * e] * m.scale, b = v[2 * e + 1] * m.scale;
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+          const float2 hf = __bfloat1622float2(h2);
+          const __nv_bfloat162 l2 = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+          hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
+          lo[e] = *reinterpret_cast<const uint32_t*>(&l2);
+        }
+        if constexpr (kCols == 4) {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(hi[0], hi[1]);
+          *reinterpret_cast<uint2*>(dst + RP) = make_uint2(lo[0], lo[1]);
+        } else {
+          *reinterpret_cast<uint32_t*>(dst) = hi[0];
+          *reinterpret_cast<uint32_t*>(dst + RP) = lo[0];
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ epilogue (warps 5-12)
 template <int RP>
 __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, const ShrinkWork& W, int warp, int lane) {
@@ -340,12 +472,15 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
   const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
   const int row = quarter * 32 + lane;
   const int set_tid = (ew & 3) * 32 + lane;      // 0..127 within the set
+  const bool dist = shrink_dist_finish<RP>(W);   // launch-uniform
+  const int rpc = (kTileM + ks - 1) / ks;        // dist: rows finished per CTA of a slot
   int li = 0;                                    // index over this CTA's items
   for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
     int local;
     const int g = map_item(M, p.n_mod, item, lane, &local);
     const ShrinkMod& m = p.mod[g];
     const int tile = local / ks, kc = local % ks;
+    const bool my_rows = !dist || (row >= kc * rpc && row < (kc + 1) * rpc);
     const bool mine = (li % kEpiSets) == set;
     const int slot = li % kShrinkAccSlots;
     const uint32_t aphase = (li / kShrinkAccSlots) & 1;
@@ -374,7 +509,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
         tmem_st32(tsig + 64 * h + 32, w + 32);
       }
       tmem_st_wait();
-    } else if (rvalid) {                          // warm L2 with this row's Sigma_i while the MMA runs
+    } else if (rvalid && my_rows) {               // warm L2 with this row's Sigma_i while the MMA runs
       const uint8_t* sp = reinterpret_cast<const uint8_t*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
 #pragma unroll
       for (int off = 0; off < RP * RP * 2; off += 128) prefetch_l2(sp + off);
@@ -391,7 +526,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
     __syncwarp();
     if (lane == 0) mbar_arrive(&R.acc_empty[slot]);
 
-    bool finisher = true;
+    bool finisher = true;                          // this thread's row is finished here
     if (ks > 1) {
       // split-K: publish this chunk's partial; the LAST arriving CTA (acq_rel counter) sums the
       // ks partials in kc order, so the result does not depend on scheduling.
@@ -407,9 +542,21 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
                                   __float_as_uint(s[4 * c + 6]), __float_as_uint(s[4 * c + 7])));
       }
       named_bar_sync(1 + set, 128);
-      if (set_tid == 0) R.s_last[set] = (atom_add_acq_rel_gpu(&m.counters[tile], 1) == ks - 1);
-      named_bar_sync(1 + set, 128);
-      finisher = R.s_last[set] != 0;
+      if (dist) {
+        if (set_tid == 0) {
+          atom_add_acq_rel_gpu(&m.counters[tile], 1);
+          while (ld_acquire_gpu(&m.counters[tile]) < ks) nanosleep_ns(32);
+          // second arrival: the last CTA past the wait resets the counter for the next launch
+          if (atom_add_acq_rel_gpu(&m.counters[tile], 1) == 2 * ks - 1) m.counters[tile] = 0;
+        }
+        named_bar_sync(1 + set, 128);
+        if constexpr (RP >= 32) dist_finish<RP>(m, tile, kc, ks, rpc, set_tid, t0, t1);
+        finisher = false;                          // rows done above; every CTA publishes below
+      } else {
+        if (set_tid == 0) R.s_last[set] = (atom_add_acq_rel_gpu(&m.counters[tile], 1) == ks - 1);
+        named_bar_sync(1 + set, 128);
+        finisher = R.s_last[set] != 0;
+      }
       if (set_tid == 0 && finisher) CTS_STAMP(12);         // last arrival known
       if (finisher) {
         if (rvalid) {
@@ -447,7 +594,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
             }
           }
         }
-        if (set_tid == 0) m.counters[tile] = 0;       // ready for the next launch
+        if (set_tid == 0 && !dist) m.counters[tile] = 0;   // ready for the next launch
         if (set_tid == 0) CTS_STAMP(13);                // partials summed
       }
     }
@@ -513,15 +660,21 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
         for (int oo = 0; oo < 8; ++oo) {
           const int o = o0 + oo;
           float acc = 0.f;
+          // 32-byte loads: every lane reads a different Sigma_i (one L1 wavefront per lane and
+          // load), so the access width sets the wavefront count
 #pragma unroll
-          for (int v8 = 0; v8 < RP / 8; ++v8) {
-            const uint4 w = __ldg(srow + (o * RP) / 8 + v8);
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+          for (int v8 = 0; v8 < RP / 8; v8 += 2) {
+            uint4 w[2];
+            ld_global_nc_v8(srow + (o * RP) / 8 + v8, w[0], w[1]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(h[e]);
-              acc = fmaf(f.x, s[v8 * 8 + 2 * e], acc);
-              acc = fmaf(f.y, s[v8 * 8 + 2 * e + 1], acc);
+            for (int hh = 0; hh < 2; ++hh) {
+              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[hh]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                acc = fmaf(f.x, s[(v8 + hh) * 8 + 2 * e], acc);
+                acc = fmaf(f.y, s[(v8 + hh) * 8 + 2 * e + 1], acc);
+              }
             }
           }
           t8[oo] = acc * m.scale;
@@ -547,12 +700,15 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
         *reinterpret_cast<uint4*>(dst + RP + o0) = lo;
       }
     }
-    if (finisher && m.ready != nullptr) {
+    if ((finisher || dist) && m.ready != nullptr) {   // set-uniform (dist: every CTA of the slot)
       // fused kernel: make the slot's t visible to other CTAs' TMA (async proxy), then publish
       if (set_tid == 0) CTS_STAMP(14);                  // t stored
       fence_proxy_async_global();
       named_bar_sync(1 + set, 128);
-      if (set_tid == 0) st_release_gpu(&m.ready[tile], 1);
+      if (set_tid == 0) {
+        if (dist) red_release_add_gpu(&m.ready[tile], 1);   // the expand waits for ks arrivals
+        else st_release_gpu(&m.ready[tile], 1);
+      }
       if (set_tid == 0) CTS_STAMP(15);                  // flag published
     }
   }

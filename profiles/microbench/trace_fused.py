@@ -11,9 +11,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import paper_2407_00066_b200 as cts  # noqa: E402
 from workloads.gen_torch import direct_bank_torch, tokens_torch  # noqa: E402
 
-T, N, C, r = int(os.environ.get("T", 1024)), int(os.environ.get("N", 1000)), int(os.environ.get("C", 25)), 16
+T, N, C, r = int(os.environ.get("T", 1024)), int(os.environ.get("N", 1000)), int(os.environ.get("C", 25)), int(os.environ.get("R", 16))
 dev = torch.device("cuda")
 mods = [(4096, 4096), (4096, 1024), (4096, 1024), (4096, 14336), (4096, 14336)]
+if os.environ.get("QONLY"):   # cfg2: one q module
+    mods = mods[:1]
 banks = [direct_bank_torch(di, do, N, C, r, seed=m, device=dev, cluster_seed=50 + m) for m, (di, do) in enumerate(mods)]
 bank = cts.Bank([b["in_basis"] for b in banks], [b["out_basis"] for b in banks], [b["sigma"] for b in banks],
                 [b["cluster_of"] for b in banks])
@@ -31,7 +33,7 @@ names = {0: "start", 1: "prologue+wait", 2: "shrink first TMA", 3: "shrink produ
          15: "finisher: flag published", 16: "shrink: first item mapped", 17: "shrink: expect_tx armed",
          18: "shrink: first gathers issued", 19: "shrink: first acc ready", 20: "-",
          21: "-", 22: "-"}
-for grp in ([0, 1, 2], [3, 4]):
+for grp in (([0],) if os.environ.get("QONLY") else ([0, 1, 2], [3, 4])):
     for rep in range(3):
         big.zero_()
         plan.apply_group(grp, [x] * len(grp), [ys[m] for m in grp], 2.0)
@@ -39,6 +41,7 @@ for grp in ([0, 1, 2], [3, 4]):
     buf = (ctypes.c_ulonglong * (160 * 24))()
     L.cts_debug_trace(buf, 160 * 24)
     a = np.array(buf, dtype=np.int64).reshape(160, 24)[:148].astype(np.float64)
+    a = a[a[:, 0] > 0]                                 # CTAs of this launch (grid may be < 148)
     t0 = a[:, 0].min()
     rel = (a - t0) / 1e3
     print(f"fused group {grp} (T={T}, N={N}, C={C}): us after first CTA start: min / median / max over CTAs")
