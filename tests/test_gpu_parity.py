@@ -144,6 +144,22 @@ def test_config2_q_proj_r64(cts):
     check_delta(ta, got, f64, x, 2.0)
 
 
+@pytest.mark.parametrize("r,C,T", [(24, 6, 90), (24, 30, 500), (64, 6, 90), (64, 30, 500), (64, 2, 1000)])
+def test_distributed_finisher(cts, r, C, T):
+    """r_pad 32 / 64 with a K split (d_in 2048 = 32 K blocks, few slots): every CTA of a slot
+    finishes 1/ks of its rows (shrink_sigma.cuh dist_finish).  Packed two-cluster slots, ragged
+    lengths, unbound tokens, several tiles per cluster (C=2, T=1000); every row vs the oracle."""
+    bits, f64 = quantized_bank(2048, 512, 40, C, r, seed=r * 100 + C)
+    bank = make_bank(cts, [bits])
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, 40, T + C, frac_none=0.1)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(T, 2048, 3))
+    for rep in range(2):                        # the slot counters reset themselves between launches
+        got = run_apply(cts, plan, 0, x, np.zeros((T, 512), np.uint16), 1.5)
+        check_delta(ta, got, f64, x, 1.5)
+
+
 @pytest.mark.slow
 def test_config2_jd_built_bank(cts):
     """Config 2 with the bank from the oracle's JD-Full of 64 trained-like rank-16 LoRAs."""
@@ -343,15 +359,16 @@ def test_launch_count_and_split_path_agree(cts):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("G", [2, 4])
-def test_tensor_parallel_dsplit(cts, G):
+@pytest.mark.parametrize("G,r,d_in", [(2, 16, 512), (4, 16, 512), (2, 64, 2048)])
+def test_tensor_parallel_dsplit(cts, G, r, d_in):
     """TP d-split through the ABI, G shards simulated in one process: each shard's bank holds its
     d_in / d_out slices, cts_shrink_partial_group writes its fp32 partial, the partials are summed
     (the all-reduce), cts_expand_reduced_group adds each shard's slice of y.  The assembled y must
-    meet the per-row 5e-3 bound against the unsharded fp64 oracle."""
+    meet the per-row 5e-3 bound against the unsharded fp64 oracle.  r = 64 with 1024 columns per
+    shard splits K, so the partials come from the distributed finisher."""
     from paper_2407_00066_b200.tp import shard_bank, shard_cols
-    N, C, r, T = 120, 5, 16, 333
-    shapes = [(512, 256), (512, 1024)]
+    N, C, T = 120, 5, 333
+    shapes = [(d_in, 256), (d_in, 1024)]
     banks, f64s = [], []
     for m, (di, do) in enumerate(shapes):
         b, f = quantized_bank(di, do, N, C, r, seed=900 + m, cluster_of=cluster_map(N, C, 910 + m))
@@ -363,7 +380,7 @@ def test_tensor_parallel_dsplit(cts, G):
     cmaps = [torch.from_numpy(b["cluster_of"]).cuda() for b in banks]
     ta = decode_tokens(T, N, 51, frac_none=0.05)
     tok = torch.from_numpy(ta).cuda()
-    xb = bf16_round(activations(T, 512, 52))
+    xb = bf16_round(activations(T, d_in, 52))
     x = dev_bf16(xb)
     ys = [torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes]
     shards = []
