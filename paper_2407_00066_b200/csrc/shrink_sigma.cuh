@@ -54,6 +54,9 @@ constexpr int kShrinkAccSlots = 4;
 #ifndef CTS_DIST_FINISH
 #define CTS_DIST_FINISH 1     // r_pad >= 32: every CTA of a split slot finishes 1/ks of its rows
 #endif
+#ifndef CTS_DIST_MIN_RP
+#define CTS_DIST_MIN_RP 32    // smallest r_pad that uses distributed finishing
+#endif
 #ifndef CTS_SHRINK_STAGES
 #define CTS_SHRINK_STAGES 8   // x / in_basis ring depth cap (the fused kernel shares its arena with the expand)
 #endif
@@ -169,7 +172,7 @@ struct ShrinkWork {
 // floor K split guarantees it when items <= grid) -- the wait is on co-resident CTAs only.
 template <int RP>
 __device__ __forceinline__ bool shrink_dist_finish(const ShrinkWork& W) {
-  return CTS_DIST_FINISH && RP >= 32 && W.ks > 1 && W.M.total <= static_cast<int>(gridDim.x);
+  return CTS_DIST_FINISH && RP >= CTS_DIST_MIN_RP && W.ks > 1 && W.M.total <= static_cast<int>(gridDim.x);
 }
 
 // item -> (module g, index within the module); warp-uniform item, all lanes participate
@@ -345,16 +348,16 @@ __device__ void shrink_mma(const ShrinkParams& p, const ShrinkRing& R, const Shr
 }
 
 // Distributed finishing of rows [kc*rpc, (kc+1)*rpc) of a slot (shrink_dist_finish), by the 128
-// threads of one epilogue set: kTpr = 16 threads per row, 8 rows per pass.  Thread `sub` of a row
-// sums the ks partials of its kCols = r_pad/16 columns of s (kc order, as the single finisher),
+// threads of one epilogue set: kTpr = r_pad/4 threads per row, 128/kTpr rows per pass.  Thread
+// `sub` of a row sums the ks partials of its kCols = 4 columns of s (kc order, as the single finisher),
 // forms partial dot products Sigma_i[o][cols] . s[cols] for every output o (the 16 threads of a
-// row read each Sigma_i row as one contiguous 128-byte line), then a recursive-halving
-// reduce-scatter over the 16 threads leaves it kCols consecutive outputs of t.
+// row read each Sigma_i row as one contiguous line), then a recursive-halving reduce-scatter
+// over the kTpr threads leaves it kCols consecutive outputs of t.
 template <int RP>
 __device__ __forceinline__ void dist_finish(const ShrinkMod& m, int tile, int kc, int ks, int rpc, int set_tid,
                                             int4 t0, int4 t1) {
-  constexpr int kTpr = 16, kCols = RP / kTpr;
-  static_assert(kCols == 2 || kCols == 4, "dist_finish: r_pad 32 or 64");
+  constexpr int kCols = 4, kTpr = RP / kCols;                     // 4 / 8 / 16 threads per row
+  static_assert(kTpr >= 4 && kTpr <= 16, "dist_finish: r_pad 16, 32 or 64");
   const int sub = set_tid & (kTpr - 1);
   const int r_end = min((kc + 1) * rpc, kTileM);
   const float* const wtile = m.ws + static_cast<size_t>(tile) * ks * kTileM * RP;
@@ -492,7 +495,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
     const bool rvalid = row - sub * (kTileM / 2) < slen4;
     const int adapter = rvalid ? m.tile_adapters[tile * kTileM + row] : 0;
     const uint32_t tsig = R.tmem + (static_cast<uint32_t>(quarter * 32) << 16) + L::kSigmaCol0 + set * L::kSigmaCols;
-    if constexpr (L::kSigmaTmem) {
+    if (L::kSigmaTmem && !dist) {
       // this row's Sigma_i -> TMEM lane `row`, 64 columns (8 rows of Sigma_i) per global round trip
       const uint4* sg = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
 #pragma unroll 1
@@ -550,7 +553,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
           if (atom_add_acq_rel_gpu(&m.counters[tile], 1) == 2 * ks - 1) m.counters[tile] = 0;
         }
         named_bar_sync(1 + set, 128);
-        if constexpr (RP >= 32) dist_finish<RP>(m, tile, kc, ks, rpc, set_tid, t0, t1);
+        dist_finish<RP>(m, tile, kc, ks, rpc, set_tid, t0, t1);
         finisher = false;                          // rows done above; every CTA publishes below
       } else {
         if (set_tid == 0) R.s_last[set] = (atom_add_acq_rel_gpu(&m.counters[tile], 1) == ks - 1);
