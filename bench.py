@@ -254,7 +254,7 @@ def run_reference(args, cfg):
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": oracle_cores(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
@@ -379,7 +379,7 @@ def run_tp(args, cfg):
         "clocks": clocks.result(),
     }
     if rank == 0:
-        print(json.dumps(line))
+        emit(line)
     dist.barrier()
     dist.destroy_process_group()
     plan.close()
@@ -488,7 +488,7 @@ def run_proj(args, cfg):
                     "note": "torch.mm over the same x and W0 (no LoRA): the library GEMM the fused kernel competes with"},
         "gpu_launches": args.steps * launches, "launches_per_step": launches, "clocks": clocks.result(),
     }
-    print(json.dumps(line))
+    emit(line)
     plan.close()
     bank.close()
     return 0
@@ -743,7 +743,7 @@ def run_gpu(args, cfg):
             tok_s, info = oracle_sample(cfg, budget_s=args.cpu_budget)
             line["cpu_baseline"] = {"value": tok_s, "unit": "tokens/s", "cores": info["cores"], "kind": "oracle",
                                     "sample": info["sample"]}
-        print(json.dumps(line))
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -752,7 +752,20 @@ def run_gpu(args, cfg):
     return 0
 
 
+_JSON_FD = None
+
+
+def emit(line):
+    """The one JSON line of this run, on the ORIGINAL stdout (main() points fd 1 at stderr, so
+    library chatter such as NCCL's version banner cannot end up in the driver's stdout)."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
