@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
     if (threadIdx.x == 0) CTS_STAMP(3);               // producers done issuing
     mbar_wait(arena_free, 0);
     if (threadIdx.x == 0) CTS_STAMP(7);
-    expand_producer<RP>(p.e, RE, nt_lane, warp, lane, shrink_dist_finish<RP>(W) ? W.ks : 1);
+    expand_producer<RP>(p.e, RE, nt_lane, warp, lane, shrink_dist_finish<RP>(p.s, W) ? W.ks : 1);
   } else if (warp == kMmaWarp) {
     shrink_mma<RP>(p.s, RS, W, lane);
     if (lane == 0) { umma_commit(arena_free); CTS_STAMP(4); }

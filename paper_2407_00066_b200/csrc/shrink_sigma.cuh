@@ -169,10 +169,13 @@ struct ShrinkWork {
 // CTA of the slot waits until all ks partials are published and finishes rows [kc*128/ks, ...),
 // so the Sigma traffic spreads over ks SMs; the slot's "t ready" flag then counts ks arrivals.
 // Needs every CTA to hold at most one shrink item (all chunks of a slot in flight at once: the
-// floor K split guarantees it when items <= grid) -- the wait is on co-resident CTAs only.
+// floor K split guarantees it when items <= grid) and all CTAs co-resident -- so only the fused
+// kernel (ready flags set), which already relies on co-residency, uses it; the standalone shrink
+// kernel (CTS_FUSED=0, TP partials) keeps the wait-free last-arriver finisher.
 template <int RP>
-__device__ __forceinline__ bool shrink_dist_finish(const ShrinkWork& W) {
-  return CTS_DIST_FINISH && RP >= CTS_DIST_MIN_RP && W.ks > 1 && W.M.total <= static_cast<int>(gridDim.x);
+__device__ __forceinline__ bool shrink_dist_finish(const ShrinkParams& p, const ShrinkWork& W) {
+  return CTS_DIST_FINISH && RP >= CTS_DIST_MIN_RP && p.mod[0].ready != nullptr && W.ks > 1 &&
+         W.M.total <= static_cast<int>(gridDim.x);
 }
 
 // item -> (module g, index within the module); warp-uniform item, all lanes participate
@@ -475,7 +478,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
   const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
   const int row = quarter * 32 + lane;
   const int set_tid = (ew & 3) * 32 + lane;      // 0..127 within the set
-  const bool dist = shrink_dist_finish<RP>(W);   // launch-uniform
+  const bool dist = shrink_dist_finish<RP>(p, W);   // launch-uniform
   const int rpc = (kTileM + ks - 1) / ks;        // dist: rows finished per CTA of a slot
   int li = 0;                                    // index over this CTA's items
   for (int item = blockIdx.x; item < M.total; item += gridDim.x) {

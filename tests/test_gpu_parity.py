@@ -365,7 +365,7 @@ def test_tensor_parallel_dsplit(cts, G, r, d_in):
     d_in / d_out slices, cts_shrink_partial_group writes its fp32 partial, the partials are summed
     (the all-reduce), cts_expand_reduced_group adds each shard's slice of y.  The assembled y must
     meet the per-row 5e-3 bound against the unsharded fp64 oracle.  r = 64 with 1024 columns per
-    shard splits K, so the partials come from the distributed finisher."""
+    shard splits K (the standalone shrink kernel: last-arriver finisher at r_pad 64)."""
     from paper_2407_00066_b200.tp import shard_bank, shard_cols
     N, C, T = 120, 5, 333
     shapes = [(d_in, 256), (d_in, 1024)]
