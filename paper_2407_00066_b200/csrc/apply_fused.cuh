@@ -133,7 +133,10 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   if (*s_last_exit) {
     for (int g = 0; g < p.s.n_mod; ++g)
       for (int i = threadIdx.x; i < p.s.tiles_bound; i += blockDim.x) p.s.mod[g].ready[i] = 0;
-    if (threadIdx.x == 0) *p.exit_count = 0;
+    if (threadIdx.x == 0) {
+      *p.exit_count = 0;
+      if (p.e.dyn_next != nullptr) *p.e.dyn_next = 0;   // expand dynamic-tail counter
+    }
   }
   if (warp == kMmaWarp) tmem_dealloc<S::kTmemCols>(RS.tmem);
 }

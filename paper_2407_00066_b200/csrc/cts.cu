@@ -401,6 +401,7 @@ cts_status_t launch_fused(cts_plan_t p, int n, const int32_t* modules, const voi
   prm.e.poll_first = poll_first_default(p->T, p->bank->C);
   prm.e.early_items = early_items_default();
   prm.exit_count = p->exit_count;
+  prm.e.dyn_next = p->exit_count + 1;            // zeroed with the flags; reset by the last CTA
   CTS_CUDA(launch_pdl(apply_fused_kernel<RP, STORE>, std::min(sm_count(), std::max(items_s, items_e)), kApplyThreads,
                       FusedSmem<RP>::kBytes, stream, prm));
   return CTS_OK;

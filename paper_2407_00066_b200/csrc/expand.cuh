@@ -45,6 +45,15 @@ constexpr int kStoreScatter = 0, kStoreDirect = 1, kStoreCoalesced = 2;   // exp
 #ifndef CTS_Y_STORE_HINT
 #define CTS_Y_STORE_HINT ""       // e.g. ".cs" (evict-first) -- tuning aid
 #endif
+#ifndef CTS_DYN_TAIL
+#define CTS_DYN_TAIL 0            // fused kernel, many items per CTA: claim the last items at run time (measured: no gain)
+#endif
+#ifndef CTS_DYN_MIN_ROUNDS
+#define CTS_DYN_MIN_ROUNDS 48     // ... only when a launch has at least this many expand items per CTA
+#endif
+#ifndef CTS_DYN_STATIC_PCT
+#define CTS_DYN_STATIC_PCT 90     // share of the items dealt statically (whole rounds)
+#endif
 #ifndef CTS_EXPAND_BOXES
 #define CTS_EXPAND_BOXES 1   // runs of consecutive tokens as box loads / stores (row_boxes)
 #endif
@@ -81,6 +90,7 @@ struct ExpandParams {
   int poll_first;                        // fused: 1 = wait for t before issuing the item's loads
   int early_items;                       // fused, poll_first = 0: only this CTA's first early_items items
                                          // issue their y / out_basis loads before their t is ready
+  int* dyn_next;                         // fused: dynamic-tail claim counter (self-resetting), else null
 };
 
 template <int RP>
@@ -138,6 +148,23 @@ __device__ __forceinline__ ItemMap expand_map(const ExpandParams& p, int nt_lane
   return make_item_map(p.n_mod, nt_lane, lane < p.n_mod ? p.mod[lane].nblk : 0, lane);
 }
 
+// Dynamic tail.  Items [0, S) are dealt round-robin (S whole rounds of the grid); items [S, total)
+// are claimed at run time from a launch-wide counter by producer warp 0, in ring order, so CTAs
+// that started their expand late (longer shrink share) take fewer of them.  After the last item a
+// sentinel stage (module -1) tells the MMA warp and the epilogue to stop.  Only with the split
+// epilogue (both sets see every stage) and many items per CTA (prefill).
+__device__ __forceinline__ int expand_static_items(const ExpandParams& p, const ItemMap& M) {
+  if (!CTS_DYN_TAIL || !kEpiSplit || p.dyn_next == nullptr ||
+      M.total < CTS_DYN_MIN_ROUNDS * static_cast<int>(gridDim.x))
+    return M.total;
+  return (M.total / 100 * CTS_DYN_STATIC_PCT / static_cast<int>(gridDim.x)) * static_cast<int>(gridDim.x);
+}
+
+// this CTA's statically dealt items: blockIdx.x + j * grid < S
+__device__ __forceinline__ int expand_static_local(int S) {
+  return S > static_cast<int>(blockIdx.x) ? (S - static_cast<int>(blockIdx.x) + gridDim.x - 1) / gridDim.x : 0;
+}
+
 template <int RP> __device__ __forceinline__ uint8_t* stage_y(const ExpandRing& R, int s) {
   return R.arena + s * ExpandCfg<RP>::kStage;
 }
@@ -156,18 +183,54 @@ template <int RP> __device__ __forceinline__ int4* stage_info(const ExpandRing& 
 
 // ------------------------------------------------------------------ TMA producers (warps 0-3)
 template <int RP>
+__device__ __forceinline__ void expand_produce(const ExpandParams& p, const ExpandRing& R, const ItemMap& M, int item,
+                                               int my, int lane, int ready_target);
+
+template <int RP>
 __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane,
                                 int ready_target = 1) {   // fused: arrivals on a slot's "t ready" flag
   using L = ExpandCfg<RP>;
   const ItemMap M = expand_map(p, nt_lane, lane);
+  const int S = expand_static_items(p, M);
   int li = 0;                                     // index over this CTA's items
-  for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
+  for (int item = blockIdx.x; item < S; item += gridDim.x) {
+    const int my = li++;
+    if (my % kProducerWarps != warp) continue;
+    expand_produce<RP>(p, R, M, item, my, lane, ready_target);
+  }
+  if (S < M.total && warp == 0) {                 // dynamic tail, claimed in ring order
+    for (;;) {
+      const int my = li++;
+      const int stage = my % L::kStages;
+      const uint32_t phase = (my / L::kStages) & 1;
+      int item = 0;
+      if (lane == 0) item = S + atomicAdd(p.dyn_next, 1);
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= M.total) {                      // sentinel stage: consumers stop here
+        mbar_wait(&R.empty[stage], phase ^ 1);
+        if (lane == 0) {
+          stage_info<RP>(R, stage)[0] = make_int4(-1, 0, 0, 0);
+          stage_info<RP>(R, stage)[1] = make_int4(0, 0, 0, 0);
+          mbar_arrive(&R.full[stage]);
+        }
+        __syncwarp();
+        break;
+      }
+      expand_produce<RP>(p, R, M, item, my, lane, ready_target);
+    }
+  }
+}
+
+// One work item's loads into ring stage my % kStages (one producer warp, all lanes).
+template <int RP>
+__device__ __forceinline__ void expand_produce(const ExpandParams& p, const ExpandRing& R, const ItemMap& M, int item,
+                                               int my, int lane, int ready_target) {
+  using L = ExpandCfg<RP>;
+  {
     int local;
     const int g = map_item(M, p.n_mod, item, lane, &local);
     const ExpandMod& m = p.mod[g];
     const int tile = local / m.nblk, nb = local % m.nblk;
-    const int my = li++;
-    if (my % kProducerWarps != warp) continue;
     const int4 t0 = m.tiles[2 * tile], t1 = m.tiles[2 * tile + 1];
     const int4 r4 = *reinterpret_cast<const int4*>(m.tile_rows + tile * kTileM + 4 * lane);
     const int stage = my % L::kStages;
@@ -242,12 +305,19 @@ __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_la
   // unshared slot the second block is stale and D1 is never read.
   constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * kBN);
   const ItemMap M = expand_map(p, nt_lane, lane);
+  const int S = expand_static_items(p, M);
+  const int n_static = expand_static_local(S);
   int stage = 0, slot = 0;
   uint32_t phase = 0, aphase = 0;
-  for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
+  for (int li = 0; S < M.total || li < n_static; ++li) {
     mbar_wait(&R.acc_empty[slot], aphase ^ 1);
     mbar_wait(&R.full[stage], phase);
     tc_fence_after();
+    if (li >= n_static && stage_info<RP>(R, stage)[0].x < 0) {   // dynamic tail: sentinel
+      if (lane == 0) mbar_arrive(&R.acc_full[slot]);
+      __syncwarp();
+      break;
+    }
     if (lane == 0) {
       const uint32_t acc = R.tmem + slot * L::kSlotCols;
       const uint32_t hi = smem_u32(stage_a<RP>(R, stage)), lo = hi + L::kA, b = smem_u32(stage_b<RP>(R, stage));
@@ -274,9 +344,9 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
   const int set = ew >> 2;
   const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
   const int row = quarter * 32 + lane;
-  int li = 0;
-  for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
-    const int my = li++;
+  const int S = expand_static_items(p, M);
+  const int n_static = expand_static_local(S);
+  for (int my = 0; S < M.total || my < n_static; ++my) {
     if (!kEpiSplit && my % kEpiSets != set) continue;
     static_assert(!kEpiSplit || kEpiSets == kBN / 64, "split epilogue: one 64-column segment per set");
     const int seg0 = kEpiSplit ? set : 0, seg1 = kEpiSplit ? set + 1 : kBN / 64;   // this warp's segments
@@ -287,6 +357,7 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
     tc_fence_after();
     const int4 info = stage_info<RP>(R, stage)[0];    // (g, cluster0, nb, len0)
     const int4 info1 = stage_info<RP>(R, stage)[1];   // (cluster1, len1, -, -)
+    if (my >= n_static && info.x < 0) break;          // dynamic tail: sentinel
     const int sub = (info1.y > 0 && quarter >= 2) ? 1 : 0;   // which half's tile these rows hold
     const int sbase = sub * (kTileM / 2);                    // first slot row of that tile
     const int slen = sub ? info1.y : info.w;
