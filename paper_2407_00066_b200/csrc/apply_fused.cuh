@@ -100,19 +100,25 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
 //              accumulators and the staged Sigma_i, tmem_free);
   //   epilogue:  nothing -- it takes expand items after its own split-K / Sigma work, so expand
   //              loads and MMAs of this CTA overlap its shrink finisher chain.
+  // weighted expand deal: r0 = CTAs holding one more shrink item than the rest, K = expand items
+  // (128 x kBN y read + written) worth one shrink item (128 rows x its K chunk of x)
+  const int deal_r0 = (CTS_WEIGHTED_DEAL && W.M.total > static_cast<int>(gridDim.x))
+                          ? W.M.total % static_cast<int>(gridDim.x) : 0;
+  const int deal_k = p.s.mod[0].kblocks * kBK / (W.ks * CTS_DEAL_DIV * kBN);
   if (warp < kProducerWarps) {
     shrink_producer<RP>(p.s, RS, W, warp, lane, first);
     if (threadIdx.x == 0) CTS_STAMP(3);               // producers done issuing
     mbar_wait(arena_free, 0);
     if (threadIdx.x == 0) CTS_STAMP(7);
-    expand_producer<RP>(p.e, RE, nt_lane, warp, lane, shrink_dist_finish<RP>(p.s, W) ? W.ks : 1);
+    expand_producer<RP>(p.e, RE, nt_lane, warp, lane, shrink_dist_finish<RP>(p.s, W) ? W.ks : 1, deal_r0,
+                        deal_k);
   } else if (warp == kMmaWarp) {
     shrink_mma<RP>(p.s, RS, W, lane);
     if (lane == 0) { umma_commit(arena_free); CTS_STAMP(4); }
     __syncwarp();
     mbar_wait(tmem_free, 0);                  // shrink accumulators and staged Sigma all read
     tc_fence_after();
-    expand_mma<RP>(p.e, RE, nt_lane, lane);
+    expand_mma<RP>(p.e, RE, nt_lane, lane, deal_r0, deal_k);
   } else {
     shrink_epilogue<RP>(p.s, RS, W, warp, lane);
     tc_fence_before();
@@ -120,7 +126,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
     if (lane == 0) mbar_arrive(tmem_free);
     if (threadIdx.x == 32 * kEpiWarp0) CTS_STAMP(5);        // epilogue set 0 done
     if (threadIdx.x == 32 * (kEpiWarp0 + 4)) CTS_STAMP(6);  // epilogue set 1 done
-    expand_epilogue<RP, STORE>(p.e, RE, nt_lane, warp, lane);
+    expand_epilogue<RP, STORE>(p.e, RE, nt_lane, warp, lane, deal_r0, deal_k);
   }
 
   // ---------------------------------------------------------------- exit: last CTA clears flags

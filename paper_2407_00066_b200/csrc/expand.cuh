@@ -54,6 +54,12 @@ constexpr int kStoreScatter = 0, kStoreDirect = 1, kStoreCoalesced = 2;   // exp
 #ifndef CTS_DYN_STATIC_PCT
 #define CTS_DYN_STATIC_PCT 90     // share of the items dealt statically (whole rounds)
 #endif
+#ifndef CTS_WEIGHTED_DEAL
+#define CTS_WEIGHTED_DEAL 1       // fused: CTAs with an extra shrink item get fewer expand items
+#endif
+#ifndef CTS_DEAL_DIV
+#define CTS_DEAL_DIV 2            // K = d_in / (ks * CTS_DEAL_DIV * kBN): x bytes of a shrink item / y bytes of an expand item
+#endif
 #ifndef CTS_EXPAND_BOXES
 #define CTS_EXPAND_BOXES 1   // runs of consecutive tokens as box loads / stores (row_boxes)
 #endif
@@ -160,9 +166,38 @@ __device__ __forceinline__ int expand_static_items(const ExpandParams& p, const 
   return (M.total / 100 * CTS_DYN_STATIC_PCT / static_cast<int>(gridDim.x)) * static_cast<int>(gridDim.x);
 }
 
-// this CTA's statically dealt items: blockIdx.x + j * grid < S
-__device__ __forceinline__ int expand_static_local(int S) {
-  return S > static_cast<int>(blockIdx.x) ? (S - static_cast<int>(blockIdx.x) + gridDim.x - 1) / gridDim.x : 0;
+// Weighted static deal (fused kernel).  When the shrink has more items than CTAs, CTAs
+// b < r0 = shrink_items % grid run one more shrink item than the rest and would start (and end)
+// their expand that much later.  Items [0, A) go round-robin to every CTA, the last nB = K * (grid -
+// r0) only to CTAs b >= r0, K = expand items worth one shrink item.  r0 = 0: plain round-robin.
+struct ExpandDeal {
+  int A, r0, nB;
+};
+
+__device__ __forceinline__ ExpandDeal expand_deal(int S, int r0, int K) {
+  ExpandDeal d{S, 0, 0};
+  if (r0 > 0 && K > 0) {
+    d.r0 = r0;
+    d.nB = min(K * (static_cast<int>(gridDim.x) - r0), S);
+    d.A = S - d.nB;
+  }
+  return d;
+}
+
+__device__ __forceinline__ int expand_deal_count(const ExpandDeal& d) {
+  const int G = gridDim.x, b = blockIdx.x;
+  int n = d.A > b ? (d.A - b + G - 1) / G : 0;
+  if (d.nB > 0 && b >= d.r0) {
+    const int GB = G - d.r0, bb = b - d.r0;
+    n += d.nB > bb ? (d.nB - bb + GB - 1) / GB : 0;
+  }
+  return n;
+}
+
+__device__ __forceinline__ int expand_deal_item(const ExpandDeal& d, int j) {   // this CTA's j-th item
+  const int G = gridDim.x, b = blockIdx.x;
+  const int nA = d.A > b ? (d.A - b + G - 1) / G : 0;
+  return j < nA ? b + j * G : d.A + (b - d.r0) + (j - nA) * (G - d.r0);
 }
 
 template <int RP> __device__ __forceinline__ uint8_t* stage_y(const ExpandRing& R, int s) {
@@ -188,15 +223,18 @@ __device__ __forceinline__ void expand_produce(const ExpandParams& p, const Expa
 
 template <int RP>
 __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane,
-                                int ready_target = 1) {   // fused: arrivals on a slot's "t ready" flag
+                                int ready_target = 1,       // fused: arrivals on a slot's "t ready" flag
+                                int deal_r0 = 0, int deal_k = 0) {   // fused: weighted deal
   using L = ExpandCfg<RP>;
   const ItemMap M = expand_map(p, nt_lane, lane);
   const int S = expand_static_items(p, M);
+  const ExpandDeal D = expand_deal(S, deal_r0, deal_k);
+  const int n_static = expand_deal_count(D);
   int li = 0;                                     // index over this CTA's items
-  for (int item = blockIdx.x; item < S; item += gridDim.x) {
+  for (int j = 0; j < n_static; ++j) {
     const int my = li++;
     if (my % kProducerWarps != warp) continue;
-    expand_produce<RP>(p, R, M, item, my, lane, ready_target);
+    expand_produce<RP>(p, R, M, expand_deal_item(D, j), my, lane, ready_target);
   }
   if (S < M.total && warp == 0) {                 // dynamic tail, claimed in ring order
     for (;;) {
@@ -298,7 +336,8 @@ __device__ __forceinline__ void expand_produce(const ExpandParams& p, const Expa
 
 // ------------------------------------------------------------------ MMA issuer (warp 4)
 template <int RP>
-__device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_lane, int lane) {
+__device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_lane, int lane, int deal_r0 = 0,
+                           int deal_k = 0) {
   using L = ExpandCfg<RP>;
   // N = 2 kBN: the two halves' out_basis blocks are contiguous in the B stage (256 rows), so one
   // MMA per K step gives D0 = t U_c0^T (cols [0,128)) and D1 = t U_c1^T (cols [128,256)); for an
@@ -306,7 +345,7 @@ __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_la
   constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * kBN);
   const ItemMap M = expand_map(p, nt_lane, lane);
   const int S = expand_static_items(p, M);
-  const int n_static = expand_static_local(S);
+  const int n_static = expand_deal_count(expand_deal(S, deal_r0, deal_k));
   int stage = 0, slot = 0;
   uint32_t phase = 0, aphase = 0;
   for (int li = 0; S < M.total || li < n_static; ++li) {
@@ -337,7 +376,8 @@ __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_la
 
 // ------------------------------------------------------------------ epilogue (warps 5-12)
 template <int RP, int STORE>
-__device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane) {
+__device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane,
+                                int deal_r0 = 0, int deal_k = 0) {
   using L = ExpandCfg<RP>;
   const ItemMap M = expand_map(p, nt_lane, lane);
   const int ew = warp - kEpiWarp0;               // 0..7
@@ -345,7 +385,7 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
   const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
   const int row = quarter * 32 + lane;
   const int S = expand_static_items(p, M);
-  const int n_static = expand_static_local(S);
+  const int n_static = expand_deal_count(expand_deal(S, deal_r0, deal_k));
   for (int my = 0; S < M.total || my < n_static; ++my) {
     if (!kEpiSplit && my % kEpiSets != set) continue;
     static_assert(!kEpiSplit || kEpiSets == kBN / 64, "split epilogue: one 64-column segment per set");

@@ -1,0 +1,14 @@
+set -u
+NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -shared"
+cp paper_2407_00066_b200/libcts.so /tmp/lib_k2.so
+$NV -DCTS_WEIGHTED_DEAL=0 -o /tmp/lib_off.so paper_2407_00066_b200/csrc/cts.cu
+$NV -DCTS_DEAL_DIV=4 -o /tmp/lib_k4.so paper_2407_00066_b200/csrc/cts.cu
+$NV -DCTS_DEAL_DIV=1 -o /tmp/lib_k1.so paper_2407_00066_b200/csrc/cts.cu
+timeout 600 python -m pytest tests -m gpu -x -q --timeout 200 2>&1 | tail -3 > gpurun_out/deal_pytest.txt
+for rep in 1 2; do for v in off k2 k4 k1; do
+cp /tmp/lib_$v.so paper_2407_00066_b200/libcts.so
+timeout 200 python bench.py --config prefill --steps 30 --no-cpu-baseline > gpurun_out/deal_prefill_${v}_r$rep.json 2>> gpurun_out/deal.err
+timeout 200 python bench.py --config multi --steps 30 --no-cpu-baseline > gpurun_out/deal_multi_${v}_r$rep.json 2>> gpurun_out/deal.err
+done; done
+cp /tmp/lib_k2.so paper_2407_00066_b200/libcts.so
+timeout 200 python bench.py --config decode --steps 100 --no-cpu-baseline > gpurun_out/deal_decode_k2.json 2>> gpurun_out/deal.err
