@@ -194,9 +194,13 @@ __device__ __forceinline__ int expand_deal_count(const ExpandDeal& d) {
   return n;
 }
 
-__device__ __forceinline__ int expand_deal_item(const ExpandDeal& d, int j) {   // this CTA's j-th item
+__device__ __forceinline__ int expand_deal_count_a(const ExpandDeal& d) {     // round-robin part
   const int G = gridDim.x, b = blockIdx.x;
-  const int nA = d.A > b ? (d.A - b + G - 1) / G : 0;
+  return d.A > b ? (d.A - b + G - 1) / G : 0;
+}
+
+__device__ __forceinline__ int expand_deal_item(const ExpandDeal& d, int j, int nA) {   // this CTA's j-th item
+  const int G = gridDim.x, b = blockIdx.x;
   return j < nA ? b + j * G : d.A + (b - d.r0) + (j - nA) * (G - d.r0);
 }
 
@@ -229,12 +233,18 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
   const ItemMap M = expand_map(p, nt_lane, lane);
   const int S = expand_static_items(p, M);
   const ExpandDeal D = expand_deal(S, deal_r0, deal_k);
-  const int n_static = expand_deal_count(D);
   int li = 0;                                     // index over this CTA's items
-  for (int j = 0; j < n_static; ++j) {
-    const int my = li++;
-    if (my % kProducerWarps != warp) continue;
-    expand_produce<RP>(p, R, M, expand_deal_item(D, j), my, lane, ready_target);
+  if (D.nB == 0) {                                // plain round-robin (decode: always)
+    for (int item = blockIdx.x; item < S; item += gridDim.x) {
+      const int my = li++;
+      if (my % kProducerWarps != warp) continue;
+      expand_produce<RP>(p, R, M, item, my, lane, ready_target);
+    }
+  } else {
+    const int n_static = expand_deal_count(D), n_a = expand_deal_count_a(D);
+    for (int j = warp; j < n_static; j += kProducerWarps)   // local item j -> producer warp j % 4
+      expand_produce<RP>(p, R, M, expand_deal_item(D, j, n_a), j, lane, ready_target);
+    li = n_static;
   }
   if (S < M.total && warp == 0) {                 // dynamic tail, claimed in ring order
     for (;;) {
