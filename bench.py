@@ -216,43 +216,72 @@ def oracle_cores():
         return len(os.sched_getaffinity(0))
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_one_thread(ol):
+    """One layer of the oracle with the BLAS pool limited to one thread (tokens/s of the whole
+    model, extrapolated like the multi-threaded figure)."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:
+        return None
+    with threadpool_limits(limits=1):
+        t = sum(ol.run_module(m) for m in range(len(ol.mods)))
+    return ol.cfg["T"] / (t * ol.cfg["layers"])
+
+
 def oracle_sample(cfg, budget_s=20.0):
     """Time the oracle on full layers (all 7 modules) repeatedly within ~budget_s; tokens/s
-    extrapolated to the whole step (x layers)."""
+    extrapolated to the whole step (x layers).  Also one 1-thread layer and the host CPU model."""
     ol = OracleLayer(cfg)
     reps, t_start = [], time.perf_counter()
     while not reps or time.perf_counter() - t_start + reps[-1] < budget_s:
         reps.append(sum(ol.run_module(m) for m in range(len(ol.mods))))
     per_layer = statistics.median(reps)
-    info = {"cores": oracle_cores(), "kind": "oracle",
+    info = {"cores": oracle_cores(), "kind": "oracle", "cpu_model": cpu_model(),
+            "value_1thread": oracle_one_thread(ol),
             "sample": f"1 of {cfg['layers']} layers ({len(ol.mods)} modules, T={cfg['T']}), {len(reps)} rep(s), "
-                      f"median {per_layer:.3f} s/layer, extrapolated x{cfg['layers']}"}
+                      f"median {per_layer:.3f} s/layer, extrapolated x{cfg['layers']}; value_1thread: one layer "
+                      f"with the BLAS pool limited to 1 thread"}
     return cfg["T"] / (per_layer * cfg["layers"]), info
 
 
 def run_reference(args, cfg):
-    """Reference arm: the fp64 oracle as it stands on the host cores.  Step i = module (i mod 7) of
-    one layer, so K+W steps stay within minutes; a layer's time = sum of its modules' medians."""
+    """Reference arm: the fp64 oracle as it stands on the host cores.  One step = one full layer of
+    the workload (segment_ref + apply_ref of its 7 modules, T tokens): a bounded sample, so K+W
+    steps stay within minutes.  ms_per_step is that measured layer time; value (tokens/s of the
+    whole 32-layer model) divides T by the median layer time x layers, stated in the line."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     ol = OracleLayer(cfg)
     nm = len(ol.mods)
-    per_mod = {m: [] for m in range(nm)}
-    for i in range(args.warmup):
-        ol.run_module(i % nm)
-    for i in range(max(args.steps, nm)):
-        per_mod[i % nm].append(ol.run_module(i % nm))
-    per_layer = sum(statistics.median(v) for v in per_mod.values())
+    for _ in range(args.warmup):
+        for m in range(nm):
+            ol.run_module(m)
+    steps = []
+    for _ in range(args.steps):
+        steps.append(sum(ol.run_module(m) for m in range(nm)))
+    per_layer = statistics.median(steps)
     value = cfg["T"] / (per_layer * cfg["layers"])
-    sample = (f"each step = one module of layer 0 (segment_ref + apply_ref, T={cfg['T']}); layer time = sum of "
-              f"the {nm} modules' medians = {per_layer:.3f} s, extrapolated x{cfg['layers']} layers")
+    sample = (f"each step = one full layer ({nm} modules: segment_ref + apply_ref, T={cfg['T']}); value = T / "
+              f"(median layer time {per_layer:.3f} s x {cfg['layers']} layers)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_layer * cfg["layers"] * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(steps) * 1e3,
+            "full_model_step_ms_extrapolated": per_layer * cfg["layers"] * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_dict(cfg, args.gpus),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": oracle_cores(), "kind": "oracle",
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
     return 0
@@ -713,6 +742,11 @@ def run_gpu(args, cfg):
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     traffic, traffic_alg = ncu_traffic(cfg["workload"], dom)
     path_gbs = (b_shrink.sum() + b_expand.sum()) / (per_step / 1e3) / 1e9
+    # tensor-pipe share: the path's algorithmic FLOPs, T_b (2 d_in r + 2 r^2 + 2 r d_out)
+    # per module, over the step time, against the dense bf16 peak (a diagnostic: the path is HBM-bound)
+    nb = int((tokens >= 0).sum().item())
+    flops = sum(2.0 * nb * (di * r + r * r + r * do) for (_, _, di, do) in mods)
+    tflops = flops / (per_step / 1e3) / 1e12 * world
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "weak",
@@ -726,6 +760,11 @@ def run_gpu(args, cfg):
                      "path": {"algorithmic_bytes_per_step": b_shrink.sum() + b_expand.sum(),
                               "achieved_gbs": path_gbs, "frac": path_gbs / hbm},
                      "step_share": dom_ms / per_step,
+                     "frac_of_spec_8tbs": achieved / 8000.0,
+                     "tensor_pipe": {"algorithmic_flops_per_step": flops, "achieved_tflops": tflops,
+                                     "peak_tflops": bf16_peak, "pct": 100.0 * tflops / bf16_peak / world,
+                                     "note": "algorithmic FLOPs of the path (the MMAs also run padded rows / "
+                                             "columns and the hi+lo expand); ncu's tensor-pipe % is in profiles/"},
                      "kernels": {k: {"algorithmic_bytes_per_launch": v[0] / NL, "avg_launch_us": v[1] / NL * 1e3,
                                      "achieved_gbs": v[0] / (v[1] / 1e3) / 1e9,
                                      "frac": v[0] / (v[1] / 1e3) / 1e9 / hbm} for k, v in kern.items()}},
@@ -742,6 +781,7 @@ def run_gpu(args, cfg):
         if not args.no_cpu_baseline and not cfg.get("uncompressed"):
             tok_s, info = oracle_sample(cfg, budget_s=args.cpu_budget)
             line["cpu_baseline"] = {"value": tok_s, "unit": "tokens/s", "cores": info["cores"], "kind": "oracle",
+                                    "cpu_model": info["cpu_model"], "value_1thread": info["value_1thread"],
                                     "sample": info["sample"]}
         emit(line)
     if world > 1:

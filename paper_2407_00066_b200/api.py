@@ -161,6 +161,9 @@ def cts_jd_eigen_iteration(problems, r, iters, stream=None):
 def cts_route(token_adapter, owner, world, self_rank, stream=None):
     """Cluster-affinity routing: (perm [T], counts [world]) int32 CUDA tensors; perm = token indices
     stably partitioned by the rank that owns each token's adapter (owner [N] int32)."""
+    for t, nm in ((token_adapter, "token_adapter"), (owner, "owner")):
+        if t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous() or t.dim() != 1:
+            raise TypeError(f"{nm} must be a contiguous 1-D int32 CUDA tensor")
     T = token_adapter.shape[0]
     perm = torch.empty(max(T, 1), dtype=torch.int32, device=token_adapter.device)
     counts = torch.empty(world, dtype=torch.int32, device=token_adapter.device)
@@ -177,6 +180,8 @@ def cts_rows_move(src, dst, idx, scatter, stream=None):
     for t, nm in ((src, "src"), (dst, "dst")):
         if not t.is_cuda or t.dim() != 2 or t.stride(1) != 1 or t.dtype != src.dtype:
             raise TypeError(f"{nm} must be a 2-D CUDA tensor with unit inner stride and src's dtype")
+    if idx.dtype != torch.int32 or not idx.is_cuda or not idx.is_contiguous() or idx.dim() != 1:
+        raise TypeError("idx must be a contiguous 1-D int32 CUDA tensor")
     es = src.element_size()
     n = idx.shape[0]
     check("cts_rows_move", lib().cts_rows_move(ctypes.c_void_p(src.data_ptr()), src.stride(0) * es,

@@ -665,8 +665,10 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
   std::vector<int> map_id(M);
   std::vector<int32_t> tmp(N);
   for (int m = 0; m < M; ++m) {
-    if (d->sources_on_device)
-      CTS_CUDA(cudaMemcpy(tmp.data(), d->cluster_of[m], N * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (d->sources_on_device) {   // ordered after the caller's pending writes on `stream`
+      CTS_CUDA(cudaMemcpyAsync(tmp.data(), d->cluster_of[m], N * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+      CTS_CUDA(cudaStreamSynchronize(stream));
+    }
     else
       std::memcpy(tmp.data(), d->cluster_of[m], N * sizeof(int32_t));
     for (int i = 0; i < N; ++i)

@@ -291,6 +291,17 @@ __global__ void __launch_bounds__(256) jd_gram(const __grid_constant__ JdBatch b
   }
 }
 
+// Rank collapse.  Column j of X is (numerically) in the span of columns 0..j-1 when its Cholesky
+// pivot -- the squared norm of its residual after projecting out those columns -- falls below
+// kJdCollapse of its squared norm: a cluster whose stacked LoRA rank n*r_i is below r, duplicate
+// adapters, or an exactly rank-deficient iterate.  Plain Cholesky-QR would divide by ~0 and return
+// Inf/NaN.  Instead that column of X is REPLACED by the first standard basis vector e_k (k in index
+// order) whose residual is at least half its average, and the factorization continues: the result
+// is a deterministic orthonormal completion with standard basis vectors in index order, as the
+// oracle's _complete does for a span smaller than r (oracle/jd.py).  fp32 cancellation makes a
+// residual below ~3e-3 of the column norm meaningless, hence the threshold.
+constexpr float kJdCollapse = 1e-5f;
+
 template <int R>
 __global__ void __launch_bounds__(256) jd_chol(const __grid_constant__ JdBatch b, int pass) {
   const JdProblem& p = b.pr[blockIdx.y];
@@ -299,12 +310,16 @@ __global__ void __launch_bounds__(256) jd_chol(const __grid_constant__ JdBatch b
   int d;
   float* gram;
   jd_orth_mats<R>(p, blockIdx.z, pass, src, dst, d, gram);
+  float* X = const_cast<float*>(src);               // a workspace iterate (U0/V0 or U/V): writable
   __shared__ float G[R][R + 1];
+  __shared__ float diag0[R];
+  __shared__ int sub_k;
   const int nb = (d + kJdGramRows - 1) / kJdGramRows;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     float s = 0.f;
     for (int k = 0; k < nb; ++k) s += gram[static_cast<size_t>(k) * R * R + e];   // block order
     G[e / R][e % R] = s;
+    if (e / R == e % R) diag0[e / R] = s;
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -314,12 +329,41 @@ __global__ void __launch_bounds__(256) jd_chol(const __grid_constant__ JdBatch b
       if (lane == 0) {
         float s = G[j][j];
         for (int k = 0; k < j; ++k) s -= G[j][k] * G[j][k];
+        sub_k = -1;
+        if (!(s > kJdCollapse * diag0[j])) {
+          // column j collapsed: candidate e_k has Gram entries G[j][m] = X[k][m]; row j of L is
+          // the forward substitution of those, its pivot 1 - |L[j][0..j-1]|^2
+          const float need = 0.5f * static_cast<float>(d - j) / static_cast<float>(d);
+          for (int k = 0; k < d; ++k) {
+            float ss = 1.f;
+            for (int m = 0; m < j; ++m) {
+              float t = X[static_cast<size_t>(k) * R + m];
+              for (int q = 0; q < m; ++q) t -= G[j][q] * G[m][q];
+              t /= G[m][m];
+              G[j][m] = t;
+              ss -= t * t;
+            }
+            if (ss > need || k == d - 1) {
+              sub_k = k;
+              s = ss;
+              break;
+            }
+          }
+        }
         G[j][j] = sqrtf(fmaxf(s, 1e-30f));
+      }
+      __syncwarp();
+      const int k = sub_k;
+      if (k >= 0) {
+        // X[:, j] := e_k; later columns' Gram entries with it are X[k][i]
+        for (int i = j + 1 + lane; i < R; i += 32) G[i][j] = X[static_cast<size_t>(k) * R + i];
+        __syncwarp();
+        for (int row = lane; row < d; row += 32) X[static_cast<size_t>(row) * R + j] = row == k ? 1.f : 0.f;
       }
       __syncwarp();
       for (int i = j + 1 + lane; i < R; i += 32) {
         float t = G[i][j];
-        for (int k = 0; k < j; ++k) t -= G[i][k] * G[j][k];
+        for (int k2 = 0; k2 < j; ++k2) t -= G[i][k2] * G[j][k2];
         G[i][j] = t / G[j][j];
       }
       __syncwarp();

@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) route_kernel(RouteArgs a) {
       if (t < a.T) {
         const int id = a.token_adapter[t];
         dst = (id >= 0 && id < a.N) ? a.owner[id] : a.self;
+        if (dst < 0 || dst >= a.world) dst = a.self;   // an out-of-range owner keeps the token local
       }
       const int f = dst == r ? 1 : 0;
       int total;

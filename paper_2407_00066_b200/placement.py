@@ -29,7 +29,11 @@ def owned_clusters(C, rank, world):
 def shard_bank_by_cluster(in_basis, out_basis, cluster_of, rank, world):
     """This rank's share of one module's bank: the owned clusters' bases and a LOCAL adapter ->
     cluster map (c // world for owned adapters; 0 for the others, whose tokens never arrive here).
-    in_basis [C][d_in][r], out_basis [C][d_out][r], cluster_of [N] (torch tensors)."""
+    in_basis [C][d_in][r], out_basis [C][d_out][r], cluster_of [N] (torch tensors).  Needs
+    C >= world: a rank owning no cluster would hold an empty bank (cts_bank_load rejects C < 1)."""
+    if in_basis.shape[0] < world:
+        raise ValueError(f"cluster-affinity placement needs at least one cluster per rank (C={in_basis.shape[0]} "
+                         f"< world={world}); use data-parallel replication instead")
     own = owned_clusters(in_basis.shape[0], rank, world)
     local = (cluster_of // world).clone()
     local[(cluster_of % world) != rank] = 0

@@ -1,0 +1,61 @@
+"""compute-sanitizer driver: small applies through every kernel path of libcts (the fused
+single-launch kernel with its inter-CTA flags, the split shrink/expand launches, the r_pad 64
+distributed finisher, segmentation with invalid ids, the TP partial path), each followed by a
+stream sync so the tool reports per launch.  Run as
+    compute-sanitizer --tool memcheck|racecheck|synccheck python profiles/microbench/sanitize_apply.py
+Shapes are small (the tools serialize and instrument every access) but keep the decode structure:
+several packed slots, a K split > 1, a ragged tail.  No oracle: the parity suite checks values."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import paper_2407_00066_b200 as cts  # noqa: E402
+from workloads.gen_torch import direct_bank_torch, tokens_torch  # noqa: E402
+
+dev = torch.device("cuda", 0)
+torch.cuda.set_device(dev)
+
+
+def run(tag, mods, N, C, r, T, prefill=False, groups=None):
+    banks = [direct_bank_torch(di, do, N, C, r, seed=m, device=dev, cluster_seed=50 + m)
+             for m, (di, do) in enumerate(mods)]
+    bank = cts.Bank([b["in_basis"] for b in banks], [b["out_basis"] for b in banks],
+                    [b["sigma"] for b in banks], [b["cluster_of"] for b in banks])
+    plan = cts.Plan(bank, T)
+    tok = tokens_torch(T, N, 1, prefill, dev)
+    tok[::7] = -1
+    plan.segment(tok)
+    x = torch.randn(T, max(di for di, _ in mods), device=dev).to(torch.bfloat16)
+    ys = [torch.randn(T, do, device=dev).to(torch.bfloat16) for (_, do) in mods]
+    for grp in groups or [[m] for m in range(len(mods))]:
+        xs = [x[:, :mods[m][0]] for m in grp]
+        plan.apply_group(grp, xs, [ys[m] for m in grp], 2.0)
+        torch.cuda.synchronize()
+        plan.shrink_group(grp, xs, 2.0)
+        plan.expand_group(grp, [ys[m] for m in grp])
+        torch.cuda.synchronize()
+        parts = plan.new_partials(len(grp))
+        plan.shrink_partial_group(grp, xs, parts, 2.0)
+        plan.expand_reduced_group(grp, parts, [ys[m] for m in grp])
+        torch.cuda.synchronize()
+    assert plan.error() == (0, -1)
+    bad = tok.clone()
+    bad[3] = N + 5
+    plan.segment(bad)
+    plan.apply(0, x[:, :mods[0][0]], ys[0], 1.0)
+    torch.cuda.synchronize()
+    assert plan.error()[0] == 3
+    plan.close()
+    bank.close()
+    print(f"{tag}: ok", flush=True)
+
+
+run("tiny r=4 (r_pad 16)", [(64, 64)], N=4, C=1, r=4, T=32)
+run("decode-like r=16, 3 modules grouped", [(1024, 1024), (1024, 256), (1024, 256)], N=100, C=5, r=16, T=200,
+    groups=[[0, 1, 2]])
+run("cfg2-like r=64 (distributed finisher)", [(2048, 2048)], N=16, C=1, r=64, T=96)
+run("r=32", [(1024, 512)], N=32, C=3, r=32, T=150)
+run("prefill-like r=16", [(512, 1024)], N=20, C=4, r=16, T=900, prefill=True)
+print("sanitize_apply: all paths ran")

@@ -207,3 +207,15 @@ def test_two_rank_cluster_affinity_placement():
         assert err < 1e-10, (rank, err)
         assert owned_ok
         assert n_clusters == 3                                     # 6 clusters over 2 ranks
+
+
+def test_affinity_needs_a_cluster_per_rank():
+    """with C < world a rank would own no cluster and an empty bank; refuse up front."""
+    import pytest
+    import torch
+    from paper_2407_00066_b200.placement import shard_bank_by_cluster
+    ib, ob = torch.zeros(2, 64, 4), torch.zeros(2, 64, 4)
+    with pytest.raises(ValueError):
+        shard_bank_by_cluster(ib, ob, torch.zeros(8, dtype=torch.int32), 3, 4)
+    s = shard_bank_by_cluster(ib, ob, torch.zeros(8, dtype=torch.int32), 1, 2)
+    assert s[0].shape[0] == 1

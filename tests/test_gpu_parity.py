@@ -453,17 +453,22 @@ def test_diagonal_sigma_jd_diag(cts):
 
 
 # ---------------------------------------------------------------- fused base + LoRA projection
+@pytest.mark.parametrize("w_zero", [False, True])
 @pytest.mark.parametrize("d_in,d_out,T,prefill,frac_none", [(512, 512, 300, False, 0.1), (256, 768, 700, True, 0.0),
                                                             (1024, 256, 130, False, 1.0), (256, 512, 5, False, 0.0)])
-def test_fused_projection(cts, d_in, d_out, T, prefill, frac_none):
+def test_fused_projection(cts, d_in, d_out, T, prefill, frac_none, w_zero):
     """cts_project: y = W0 x + scale U_c Sigma_i V_c^T x for EVERY token
     (unbound ones get W0 x) vs the fp64 oracle on the same bf16 bits; packed and whole slots,
-    several 256-column blocks, all-unbound and tiny batches."""
+    several 256-column blocks, all-unbound and tiny batches.  With W0 = 0 the output IS the LoRA
+    term, so the per-row 5e-3 bound holds on Delta y alone (with W0 != 0 the row norm is dominated
+    by W0 x and a wrong Delta y could hide inside the tolerance)."""
     from oracle import project_ref
     N, C = 40, 5
     bits, f64 = quantized_bank(d_in, d_out, N, C, 16, seed=d_in + T)
     g = np.random.default_rng(T)
     w_bits = bf16_round(g.standard_normal((d_out, d_in)) / np.sqrt(d_in))
+    if w_zero:
+        w_bits = np.zeros_like(w_bits)
     bank = make_bank(cts, [bits])
     plan = cts.Plan(bank, T)
     if frac_none >= 1.0:
@@ -480,7 +485,10 @@ def test_fused_projection(cts, d_in, d_out, T, prefill, frac_none):
                       f64["sigma"], 2.0)
     assert np.all(np.isfinite(got)), "some rows of y were not written"
     err = row_rel_err(got, ref)
-    assert err.max() <= PARITY_TOL, f"max per-row rel err {err.max():.3e}"
+    assert err.size == 0 or err.max() <= PARITY_TOL, f"max per-row rel err {err.max():.3e}"
+    if w_zero:
+        assert np.all(got[ta < 0] == 0), "unbound rows must be exactly W0 x = 0"
+        assert err.size == np.count_nonzero(ta >= 0), "every bound row carries a nonzero Delta y"
     plan.close()
     bank.close()
 
@@ -522,6 +530,7 @@ def test_layer_grouped_bench_configuration(cts, N, C, T, prefill, sample):
     plan.segment(torch.from_numpy(ta).cuda())
     slots = {"attn": [0, 1, 2], "o": [3], "mlp": [4, 5], "down": [6]}
     rows = np.arange(T) if sample is None else np.sort(np.random.default_rng(8).choice(T, sample, replace=False))
+    dys = {}
     for si, (slot, mods) in enumerate(slots.items()):
         di = MISTRAL_MODULES[mods[0]][1]
         x = bf16_round(activations(T, di, 10 + si))
@@ -537,13 +546,28 @@ def test_layer_grouped_bench_configuration(cts, N, C, T, prefill, sample):
             ygot = bf16_to_f64(host_bits(y))[rows]
             bound = np.abs(ygot - yref) <= bf16_ulp(yref) + 1e-3 * np.abs(dy).max(axis=1, keepdims=True)
             assert bound.all(), f"module {m}: {np.count_nonzero(~bound)} elements off"
+            dys[m] = dy
+        # the same launches with y_base = 0: y IS bf16(Delta y), so north_star's per-row 5e-3 bound
+        # is checked on every row (decode) / every sampled row (prefill) of every module in the
+        # timed launch configuration (with y_base ~ N(0,1) the residual contract above dominates)
+        yz = [torch.zeros(T, MISTRAL_MODULES[m][2], dtype=torch.bfloat16, device="cuda") for m in mods]
+        plan.apply_group(mods, [dev_bf16(x)] * len(mods), yz, 2.0)
+        torch.cuda.synchronize()
+        for m, y in zip(mods, yz):
+            got = bf16_to_f64(host_bits(y))[rows]
+            err = row_rel_err(got, dys[m])
+            assert err.size == np.count_nonzero(ta[rows] >= 0)
+            assert err.max() <= PARITY_TOL, f"module {m}: max per-row rel err {err.max():.3e}"
+            assert np.all(got[ta[rows] < 0] == 0)
     plan.close()
     bank.close()
 
 
-def test_fused_projection_full_size_sampled(cts):
+@pytest.mark.parametrize("w_zero", [False, True])
+def test_fused_projection_full_size_sampled(cts, w_zero):
     """cts_project at config 4 size for q (4096 -> 4096, T=16384 prefill) and at decode size for
-    down (14336 -> 4096, T=1024), sampled rows vs the oracle."""
+    down (14336 -> 4096, T=1024), sampled rows vs the oracle.  w_zero: W0 = 0, so the per-row
+    bound is held by the LoRA term alone (the timed GEMM's K = 16 expand stage)."""
     from oracle import project_ref
     N, C, r = 1000, 25, 16
     for (di, do, T, prefill, seed) in ((4096, 4096, 16384, True, 61), (14336, 4096, 1024, False, 62)):
@@ -553,15 +577,21 @@ def test_fused_projection_full_size_sampled(cts):
         ta = prefill_tokens(T, N, seed) if prefill else decode_tokens(T, N, seed, frac_none=0.05)
         plan.segment(torch.from_numpy(ta).cuda())
         x = bf16_round(activations(T, di, seed + 1))
-        w = bf16_round(np.random.default_rng(seed).standard_normal((do, di)) / np.sqrt(di))
+        if w_zero:
+            w = np.zeros((do, di), np.uint16)
+        else:
+            w = bf16_round(np.random.default_rng(seed).standard_normal((do, di)) / np.sqrt(di))
         y = torch.empty(T, do, dtype=torch.bfloat16, device="cuda")
         plan.project(0, dev_bf16(x), dev_bf16(w), y, 2.0)
         torch.cuda.synchronize()
         rows = np.sort(np.random.default_rng(seed).choice(T, 256, replace=False))
         ref = project_ref(bf16_to_f64(x[rows]), bf16_to_f64(w), ta[rows], f64["cluster_of"], f64["in_basis"],
                           f64["out_basis"], f64["sigma"], 2.0)
-        err = row_rel_err(bf16_to_f64(host_bits(y))[rows], ref)
+        got = bf16_to_f64(host_bits(y))[rows]
+        err = row_rel_err(got, ref)
         assert err.max() <= PARITY_TOL, f"{di}->{do}: max per-row rel err {err.max():.3e}"
+        if w_zero:
+            assert np.all(got[ta[rows] < 0] == 0)
         plan.close()
         bank.close()
 
@@ -716,3 +746,34 @@ def test_cluster_affinity_single_rank(cts):
     bank.close()
     if own_pg:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["singleton", "duplicates", "ill_conditioned"])
+def test_gpu_jd_rank_deficient_cluster(cts, case):
+    """App A.2 on clusters whose stacked rank n*r_i is below r (a singleton or duplicated adapters)
+    or nearly so (one adapter a 1e-4 perturbation of another): Cholesky-QR alone would return
+    Inf/NaN; the kernel completes the basis deterministically (jd_eigen.cuh kJdCollapse).  U, V
+    must come back finite and orthonormal, and since r covers the whole span, the compressed
+    adapters must reconstruct B_i A_i (Prop. 1) up to fp32 rounding."""
+    from oracle import orthogonalize
+    r, d_in, d_out = 32, 384, 256
+    g = np.random.default_rng(5)
+    if case == "singleton":
+        Bs, As, _ = gen_loras("random", d_in, d_out, 1, 16, seed=3)
+    else:
+        Bs, As, _ = gen_loras("random", d_in, d_out, 1, 16, seed=4)
+        B2 = Bs[0] + (1e-4 * g.standard_normal(Bs[0].shape) if case == "ill_conditioned" else 0)
+        Bs, As = [Bs[0], B2], [As[0], As[0].copy()]
+    U0 = orthogonalize(g.standard_normal((d_out, r)))
+    V0 = orthogonalize(g.standard_normal((d_in, r)))
+    q = _jd_problem(Bs, As, U0, V0)
+    ws = cts.cts_jd_eigen_iteration([q], r, 5)
+    torch.cuda.synchronize()
+    del ws
+    U, V, S = (q[k].cpu().numpy().astype(np.float64) for k in ("U", "V", "sigma"))
+    assert np.all(np.isfinite(U)) and np.all(np.isfinite(V)) and np.all(np.isfinite(S))
+    assert np.allclose(U.T @ U, np.eye(r), atol=1e-4) and np.allclose(V.T @ V, np.eye(r), atol=1e-4)
+    for i, (B, A) in enumerate(zip(Bs, As)):
+        BA = B.astype(np.float32).astype(np.float64) @ A.astype(np.float32).astype(np.float64)
+        rel = np.linalg.norm(U @ S[i] @ V.T - BA) / np.linalg.norm(BA)
+        assert rel < (1e-3 if case == "ill_conditioned" else 2e-4), (case, i, rel)

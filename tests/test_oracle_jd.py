@@ -189,3 +189,19 @@ def test_eigen_iteration_exact_span_is_lossless():
                              orthogonalize(g.standard_normal((48, 4))), iters=100)
     for B, A, S in zip(Bs, As, out["sigma"]):
         assert np.allclose(out["U"] @ S @ out["V"].T, B @ A, atol=1e-8 * np.abs(B @ A).max())
+
+
+def test_mean_relative_error_hand_computed():
+    """Pin of the Sec. 6.2 metric ("mean relative reconstruction error"), hand-computed on a
+    2-adapter, d = 2, r = 1 example (no call into the method's solver):
+        B_1 A_1 = [[1, 0], [0, 0]], B_2 A_2 = [[0, 0], [0, 2]], U = V = e_1, Sigma_1 = 0.5, Sigma_2 = 1
+        adapter 1: ||[[0.5,0],[0,0]] - [[1,0],[0,0]]||_F / 1 = 0.5
+        adapter 2: ||[[1,0],[0,0]] - [[0,0],[0,2]]||_F / 2 = sqrt(5) / 2
+        mean = (0.5 + sqrt(5)/2) / 2 = 0.80901699...
+    A squared norm in the denominator (0.25 + sqrt(5)/4)/2, a squared ratio (0.25 + 5/4)/2, or a sum
+    instead of the mean (1.618...) all miss this value."""
+    Bs = [np.array([[1.0], [0.0]]), np.array([[0.0], [2.0]])]
+    As = [np.array([[1.0, 0.0]]), np.array([[0.0, 1.0]])]
+    U = V = np.array([[1.0], [0.0]])
+    sigma = np.array([[[0.5]], [[1.0]]])
+    assert abs(mean_relative_error(Bs, As, U, V, sigma) - (0.5 + np.sqrt(5) / 2) / 2) < 1e-15
