@@ -40,11 +40,13 @@ typedef enum {
   CTS_ERR_INDEX_OUT_OF_RANGE = 3, /* token adapter id outside [-1, N) or cluster id >= C  */
   CTS_ERR_UNSUPPORTED = 4,        /* not an sm_100 device, r > 64, C > 1024               */
   CTS_ERR_OUT_OF_MEMORY = 5,
-  CTS_ERR_CUDA = 6                /* a CUDA runtime/driver call failed                    */
+  CTS_ERR_CUDA = 6,               /* a CUDA runtime/driver call failed                    */
+  CTS_ERR_NCCL = 7                /* NCCL missing (libnccl.so.2 not loadable) or a call failed */
 } cts_status_t;
 
 typedef struct cts_bank_s* cts_bank_t;   /* owns all device copies of a compressed collection */
 typedef struct cts_plan_s* cts_plan_t;   /* per-batch segmentation + scratch, reusable        */
+typedef struct cts_comm_s* cts_comm_t;   /* NCCL communicator of a tensor-parallel group     */
 
 /*
  * A compressed collection for n_modules projections (e.g. 224 = 32 layers x q,k,v,o,gate,up,
@@ -188,6 +190,33 @@ cts_status_t cts_shrink_partial_group(cts_plan_t plan, int32_t n, const int32_t*
                                       const int64_t* ld_x, float scale, float* const* parts, cudaStream_t stream);
 cts_status_t cts_expand_reduced_group(cts_plan_t plan, int32_t n, const int32_t* modules, const float* const* parts,
                                       void* const* ys, const int64_t* ld_y, cudaStream_t stream);
+
+/*
+ * Tensor-parallel apply with the collective inside the library (cts_comm_create,
+ * cts_apply_tp; north_star: "the rank-r intermediate is all-reduced with NCCL over NVLink").
+ * NCCL is loaded at run time (dlopen of libnccl.so.2 -- the copy torch already loaded, if any), so
+ * libcts itself has no link-time NCCL dependency; without NCCL these calls return CTS_ERR_NCCL.
+ * cts_comm_unique_id: id_out = 128 host bytes (ncclGetUniqueId); one rank calls it and the caller
+ *   distributes the bytes to every rank (e.g. a torch.distributed broadcast).
+ * cts_comm_create: every rank of the group, with the same id, nranks >= 1 and its rank in
+ *   [0, nranks); binds to the current CUDA device (ncclCommInitRank, blocking until all ranks join).
+ *   Errors: CTS_ERR_INVALID_ARGUMENT (null, bad rank), CTS_ERR_NCCL.
+ * cts_apply_tp: the TP d-split of cts_apply_group for this rank's shard (bank holding d_in / d_out
+ *   slice `rank`, see cts_shrink_partial_group), the same segmented batch on every rank:
+ *     1. shrink on the d_in shard -> fp32 partial t_g in plan-owned buffers (one launch)
+ *     2. ncclAllReduce(sum, fp32, T * r_pad) of each module's partial, in one NCCL group, on `stream`
+ *     3. hi / lo split + expand + residual add into this rank's d_out slice of y (two launches)
+ *   Sums the ranks' partials, so the result equals the unsharded apply up to fp32 reassociation
+ *   (Sigma linear, Eq. 1).  Stream-ordered and CUDA-graph capturable (NCCL supports
+ *   capture).  Errors as cts_apply_group plus CTS_ERR_NCCL; every rank must pass the same modules.
+ * cts_comm_free: destroys the communicator (no apply may still use it).
+ */
+cts_status_t cts_comm_unique_id(void* id_out);
+cts_status_t cts_comm_create(const void* nccl_unique_id, int32_t nranks, int32_t rank, cts_comm_t* out);
+cts_status_t cts_comm_free(cts_comm_t comm);
+cts_status_t cts_apply_tp(cts_plan_t plan, int32_t n, const int32_t* modules, const void* const* xs,
+                          const int64_t* ld_x, void* const* ys, const int64_t* ld_y, float scale, cts_comm_t comm,
+                          cudaStream_t stream);
 
 /*
  * Fused base + compressed-LoRA projection: for every token t of the batch

@@ -17,6 +17,7 @@ STATUS = {
     4: "CTS_ERR_UNSUPPORTED",
     5: "CTS_ERR_OUT_OF_MEMORY",
     6: "CTS_ERR_CUDA",
+    7: "CTS_ERR_NCCL",
 }
 
 # Every symbol include/cts.h declares (tests check the .so exports all of them).
@@ -27,6 +28,7 @@ EXPORTS = (
     "cts_apply_group", "cts_shrink_group", "cts_expand_group", "cts_plan_error", "cts_status_string",
     "cts_launch_count", "cts_plan_partial_elems", "cts_shrink_partial_group", "cts_expand_reduced_group",
     "cts_project", "cts_jd_workspace_bytes", "cts_jd_eigen_iteration", "cts_route", "cts_rows_move",
+    "cts_comm_unique_id", "cts_comm_create", "cts_comm_free", "cts_apply_tp",
 )
 
 
@@ -112,6 +114,10 @@ def lib():
         "cts_jd_eigen_iteration": ([ctypes.POINTER(JdProblem), I32, I32, I32, VP, ctypes.c_size_t, P], I32),
         "cts_route": ([VP, I32, VP, I32, I32, I32, VP, VP, P], I32),
         "cts_rows_move": ([VP, I64, VP, I64, VP, I32, I32, I32, P], I32),
+        "cts_comm_unique_id": ([VP], I32),
+        "cts_comm_create": ([VP, I32, I32, ctypes.POINTER(P)], I32),
+        "cts_comm_free": ([P], I32),
+        "cts_apply_tp": ([P, I32, VP, VP, VP, VP, VP, F, P, P], I32),
     }
     for name, (argt, rest) in sig.items():
         f = getattr(L, name)

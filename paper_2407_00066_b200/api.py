@@ -275,6 +275,36 @@ def cts_expand_reduced_group(plan, modules, parts, ys, stream=None):
                                                                      _stream_handle(stream)))
 
 
+def cts_comm_unique_id():
+    """128-byte NCCL unique id (bytes) for cts_comm_create; one rank creates it, all ranks use it."""
+    buf = ctypes.create_string_buffer(128)
+    check("cts_comm_unique_id", lib().cts_comm_unique_id(buf))
+    return buf.raw
+
+
+def cts_comm_create(unique_id, nranks, rank):
+    """NCCL communicator inside libcts for the tensor-parallel apply (current CUDA device)."""
+    if len(unique_id) != 128:
+        raise ValueError("unique_id must be the 128 bytes of cts_comm_unique_id")
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    h = ctypes.c_void_p()
+    check("cts_comm_create", lib().cts_comm_create(buf, int(nranks), int(rank), ctypes.byref(h)))
+    return h
+
+
+def cts_comm_free(comm):
+    check("cts_comm_free", lib().cts_comm_free(comm))
+
+
+def cts_apply_tp(plan, modules, xs, ys, comm, scale=1.0, stream=None):
+    """TP d-split apply of one module group on this rank's shard: shrink partial, NCCL all-reduce of
+    the rank-r partials and the expand, all issued by libcts on `stream`."""
+    n, mods, xp, xl = _group_args(modules, xs, "x")
+    _, _, yp, yl = _group_args(modules, ys, "y")
+    check("cts_apply_tp", lib().cts_apply_tp(plan, n, mods, xp, xl, yp, yl, ctypes.c_float(scale), comm,
+                                             _stream_handle(stream)))
+
+
 def cts_launch_count():
     """Kernels libcts has enqueued since load (graph captures count once, at capture)."""
     return int(lib().cts_launch_count())
@@ -348,6 +378,9 @@ class Plan:
     def expand_group(self, modules, ys, stream=None):
         cts_expand_group(self.handle, modules, ys, stream)
 
+    def apply_tp(self, modules, xs, ys, comm, scale=1.0, stream=None):
+        cts_apply_tp(self.handle, modules, xs, ys, comm.handle, scale, stream)
+
     def partial_elems(self):
         return cts_plan_partial_elems(self.handle)
 
@@ -372,6 +405,25 @@ class Plan:
     def close(self):
         if self.handle is not None:
             cts_plan_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Comm:
+    """Owner of a libcts NCCL communicator (cts_comm_create / cts_comm_free)."""
+
+    def __init__(self, unique_id, nranks, rank):
+        self.handle = cts_comm_create(unique_id, nranks, rank)
+        self.nranks, self.rank = nranks, rank
+
+    def close(self):
+        if self.handle is not None:
+            cts_comm_free(self.handle)
             self.handle = None
 
     def __del__(self):

@@ -3,6 +3,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <atomic>
@@ -14,6 +16,7 @@
 
 #include "../../include/cts.h"
 #include "apply_fused.cuh"
+#include "apply_local.cuh"
 #include "expand.cuh"
 #include "proj_fused.cuh"
 #include "jd_eigen.cuh"
@@ -138,6 +141,8 @@ struct cts_bank_s {
   int32_t* maps;          // [n_maps][N]
   CUtensorMap* d_tm_in;   // [n_modules] device copies (TMA descriptors in global memory)
   CUtensorMap* d_tm_out;  // [n_modules]
+  CUtensorMap* d_tm_in3;  // [n_modules] in_basis as {64, C*rp, d_in/64}, box {64, rp, kLocKB} (apply_local)
+  CUtensorMap* d_tm_out256;  // [n_modules] out_basis, box {rp, 256} (apply_local)
   void* arena;
   size_t bytes;
 };
@@ -154,6 +159,7 @@ struct cts_plan_s {
   int32_t* n_tiles;       // [n_maps]
   int32_t* tile_rows;     // [n_maps][max_tiles*128]
   int32_t* tile_adapters; // [n_maps][max_tiles*128]
+  int32_t* sadapter;      // [n_maps][T_max] adapter of each cluster-sorted position
   int32_t* err;           // [2]
   int32_t* unbound_rows;  // [T_max + 128] tokens with id -1 (fused projection)
   int32_t* n_unbound;     // [1]
@@ -164,6 +170,7 @@ struct cts_plan_s {
   int32_t* counters;      // [kMaxGroup][max_tiles]
   int32_t* ready;         // [kMaxGroup][max_tiles] per-slot "t ready" flags (fused kernel)
   int32_t* exit_count;    // fused kernel: CTAs exited (last one clears the flags)
+  float* tp_parts;        // [kMaxGroup][T_max][rp] fp32 TP partials (cts_apply_tp)
   int launches_since_segment;  // host view, for meta_ready (see next_meta_ready)
 };
 
@@ -407,6 +414,99 @@ cts_status_t launch_fused(cts_plan_t p, int n, const int32_t* modules, const voi
   return CTS_OK;
 }
 
+// apply_local (exchange-free, decode regime) vs apply_fused (split-K + flags): CTS_LOCAL=0 forces the
+// latter (tuning aid).
+bool use_local() {
+  static bool v = [] {
+    const char* e = std::getenv("CTS_LOCAL");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
+constexpr int kLocSmemMax = 232448 - 512;   // dynamic shared memory cap (227 KB minus static)
+
+// Host half of apply_local's work map and shared-memory plan.  Rows per piece target u_g: every CTA
+// should move about the same bytes, a token row of module g costs d_in + 2 d_out elements, so
+// u_g = round((T * sum_h (d_in_h + 2 d_out_h) / grid) / (d_in_g + 2 d_out_g)).  A piece holds at
+// most ~1.5 u_g rows (device rounding), capped by lcap.  Returns false when the batch is not in the
+// kernel's regime (r_pad != 16, pieces above kLocMaxRows rows -- prefill -- or shapes it does not
+// tile); apply_fused then runs.
+bool local_plan(cts_plan_t p, int n, const int32_t* modules, LocParams& prm, int& smem) {
+  const cts_bank_t b = p->bank;
+  if (!use_local() || b->rp != kLocRP || n * (b->C + 1) + 1 > kLocTable) return false;
+  const int G = sm_count();
+  double per_row = 0;
+  for (int i = 0; i < n; ++i) {
+    const Module& m = b->mods[modules[i]];
+    if (m.d_in % (64 * kLocKB) || m.d_out < kLocBN) return false;
+    per_row += m.d_in + 2.0 * m.d_out;
+  }
+  const double cstar = per_row * p->T / G;
+  int lcap = 8;
+  for (int i = 0; i < n; ++i) {
+    const Module& m = b->mods[modules[i]];
+    const int u = std::max(1, static_cast<int>(cstar / (m.d_in + 2.0 * m.d_out) + 0.5));
+    prm.mod[i].unit_rows = u;
+    lcap = std::max(lcap, (3 * u + 1) / 2 + 1);
+  }
+  lcap = (lcap + 7) / 8 * 8;
+  if (lcap > kLocMaxRows) return false;
+  const int npad = (lcap + 15) / 16 * 16;
+  const int n_acc = std::min(8, (512 - kLocE0) / (2 * npad));
+  const LocLayout L0 = loc_layout(n, b->C, lcap, npad, 0, 0, n_acc);
+  const int avail = kLocSmemMax - L0.total - (2 * 16 + 2 * 16) * 8;
+  const int S = std::max(2, std::min(16, static_cast<int>(CTS_LOC_SFRAC / 100.0 * avail) / L0.s_bytes));
+  const int E = std::max(2, std::min(16, (avail - S * L0.s_bytes) / L0.e_bytes));
+  const LocLayout L = loc_layout(n, b->C, lcap, npad, S, E, n_acc);
+  // the shrink MMA reads 128 rows (16 KB) from every K block's A base: stay inside the allocation
+  if (L.total > kLocSmemMax || L.sring + S * L.s_bytes + 16384 > L.total) return false;
+  prm.n_mod = n;
+  prm.C = b->C;
+  prm.lcap = lcap;
+  prm.npad = npad;
+  prm.s_stages = S;
+  prm.e_stages = E;
+  prm.n_acc = n_acc;
+  smem = L.total;
+  return true;
+}
+
+cts_status_t launch_local(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
+                          void* const* ys, const int64_t* ld_y, float scale, cudaStream_t stream, bool& done) {
+  done = false;
+  LocParams prm;
+  std::memset(&prm, 0, sizeof(prm));
+  int smem = 0;
+  if (!local_plan(p, n, modules, prm, smem)) return CTS_OK;
+  static const cudaError_t attr = set_smem(apply_local_kernel, kLocSmemMax);
+  CTS_CUDA(attr);
+  const cts_bank_t b = p->bank;
+  for (int i = 0; i < n; ++i) {
+    const Module& m = b->mods[modules[i]];
+    LocMod& lm = prm.mod[i];
+    if (!make_tmap(&lm.tm_x, xs[i], m.d_in, p->T, ld_x[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap(&lm.tm_y, ys[i], m.d_out, p->T, ld_y[i] * 2, kLocBN, 1, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return CTS_ERR_CUDA;
+    lm.tm_in3 = b->d_tm_in3 + modules[i];
+    lm.tm_out = b->d_tm_out256 + modules[i];
+    const size_t mid = m.map_id;
+    lm.offsets = p->offsets + mid * (b->C + 1);
+    lm.perm = p->perm + mid * p->T_max;
+    lm.sadapter = p->sadapter + mid * p->T_max;
+    lm.sigma = m.sigma;
+    lm.y = static_cast<__nv_bfloat16*>(ys[i]);
+    lm.ld_y = ld_y[i];
+    lm.d_in = m.d_in;
+    lm.d_out = m.d_out;
+    lm.scale = scale;
+  }
+  prm.meta_ready = next_meta_ready(p);
+  CTS_CUDA(launch_pdl(apply_local_kernel, sm_count(), kLocThreads, smem, stream, prm));
+  done = true;
+  return CTS_OK;
+}
+
 cts_status_t check_group(cts_plan_t p, int32_t n, const int32_t* modules, const void* const* ptrs, const int64_t* lds,
                          bool is_x) {
   if (!p || n < 1 || !modules || !ptrs || !lds) return CTS_ERR_INVALID_ARGUMENT;
@@ -492,6 +592,9 @@ cts_status_t do_expand(cts_plan_t p, int n, const int32_t* mods, void* const* ys
 
 cts_status_t do_fused(cts_plan_t p, int n, const int32_t* mods, const void* const* xs, const int64_t* ldx,
                       void* const* ys, const int64_t* ldy, float scale, cudaStream_t s) {
+  bool done = false;
+  const cts_status_t st = launch_local(p, n, mods, xs, ldx, ys, ldy, scale, s, done);
+  if (st != CTS_OK || done) return st;
   return dispatch_rp_store<FusedLaunch>(p->bank->rp, expand_store_mode(p->T, p->bank->C), p, n, mods, xs, ldx, ys,
                                         ldy, scale, s);
 }
@@ -624,7 +727,47 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   return x < y + nb && y < x + na;
 }
 
+// ------------------------------------------------------------------ NCCL (loaded at run time)
+// Only the handful of entry points cts_apply_tp needs; ABI types restated from nccl.h (stable since
+// NCCL 2.0): ncclUniqueId is 128 opaque bytes, ncclFloat32 = 7, ncclSum = 0, ncclSuccess = 0.
+struct NcclId { char internal[128]; };
+using ncclComm_p = void*;
+struct NcclApi {
+  int (*get_unique_id)(NcclId*) = nullptr;
+  int (*comm_init_rank)(ncclComm_p*, int, NcclId, int) = nullptr;
+  int (*comm_destroy)(ncclComm_p) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, ncclComm_p, cudaStream_t) = nullptr;
+  int (*group_start)() = nullptr;
+  int (*group_end)() = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.get_unique_id = reinterpret_cast<int (*)(NcclId*)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<int (*)(ncclComm_p*, int, NcclId, int)>(dlsym(h, "ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<int (*)(ncclComm_p)>(dlsym(h, "ncclCommDestroy"));
+    api.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, ncclComm_p, cudaStream_t)>(
+        dlsym(h, "ncclAllReduce"));
+    api.group_start = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupStart"));
+    api.group_end = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupEnd"));
+    api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.all_reduce && api.group_start &&
+             api.group_end;
+  });
+  return api;
+}
+
 }  // namespace
+
+struct cts_comm_s {
+  ncclComm_p comm;
+  int nranks, rank;
+};
 
 extern "C" {
 
@@ -637,6 +780,7 @@ const char* cts_status_string(cts_status_t s) {
     case CTS_ERR_UNSUPPORTED: return "unsupported device or configuration";
     case CTS_ERR_OUT_OF_MEMORY: return "out of device memory";
     case CTS_ERR_CUDA: return "CUDA error";
+    case CTS_ERR_NCCL: return "NCCL unavailable or failed";
   }
   return "unknown status";
 }
@@ -692,7 +836,7 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
   const size_t off_maps = total;
   total = align_up(total + uniq.size() * N * sizeof(int32_t), 1024);
   const size_t off_tm = total;
-  total = align_up(total + 2 * size_t(M) * sizeof(CUtensorMap), 1024);
+  total = align_up(total + 4 * size_t(M) * sizeof(CUtensorMap), 1024);
 
   auto* b = new (std::nothrow) cts_bank_s();
   if (!b) return CTS_ERR_OUT_OF_MEMORY;
@@ -709,9 +853,11 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
   b->maps = reinterpret_cast<int32_t*>(base + off_maps);
   b->d_tm_in = reinterpret_cast<CUtensorMap*>(base + off_tm);
   b->d_tm_out = b->d_tm_in + M;
+  b->d_tm_in3 = b->d_tm_in + 2 * M;
+  b->d_tm_out256 = b->d_tm_in + 3 * M;
   for (size_t u = 0; u < uniq.size(); ++u)
     if (cudaMemcpyAsync(b->maps + u * N, uniq[u].data(), N * 4, cudaMemcpyHostToDevice, stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
-  std::vector<CUtensorMap> h_tm(2 * size_t(M));
+  std::vector<CUtensorMap> h_tm(4 * size_t(M));
   b->mods.resize(M);
   for (int m = 0; m < M; ++m) {
     Module& mod = b->mods[m];
@@ -736,8 +882,17 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
     }
     if (!make_tmap(&h_tm[m], mod.in_t, mod.d_in, uint64_t(C) * rp, uint64_t(mod.d_in) * 2, 64, rp,
                    CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap(&h_tm[M + m], mod.out, rp, uint64_t(C) * mod.d_out, uint64_t(rp) * 2, rp, 64, swizzle_for(rp * 2)))
+        !make_tmap(&h_tm[M + m], mod.out, rp, uint64_t(C) * mod.d_out, uint64_t(rp) * 2, rp, 64, swizzle_for(rp * 2)) ||
+        !make_tmap(&h_tm[3 * M + m], mod.out, rp, uint64_t(C) * mod.d_out, uint64_t(rp) * 2, rp, kLocBN,
+                   swizzle_for(rp * 2)))
       return fail(CTS_ERR_CUDA);
+    {   // the same in_basis viewed as {64 columns, C*rp rows, d_in/64 K blocks}: one box = kLocKB slabs
+      const uint64_t dims[3] = {64, uint64_t(C) * rp, uint64_t(mod.d_in / 64)};
+      const uint64_t strides[2] = {uint64_t(mod.d_in) * 2, 128};
+      const uint32_t box[3] = {64, uint32_t(rp), uint32_t(kLocKB)};
+      if (!make_tmap3(&h_tm[2 * M + m], mod.in_t, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+        return fail(CTS_ERR_CUDA);
+    }
   }
   if (cudaMemcpyAsync(b->d_tm_in, h_tm.data(), h_tm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, stream) != cudaSuccess)
     return fail(CTS_ERR_CUDA);
@@ -795,6 +950,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   const size_t o_nt = off; off = align_up(off + nm * 4, 256);
   const size_t o_trows = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
   const size_t o_tads = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
+  const size_t o_sad = off; off = align_up(off + nm * T_max * 4, 256);
   const size_t o_err = off; off = align_up(off + 16, 256);
   const size_t o_unb = off; off = align_up(off + (size_t(T_max) + kTileM + 4) * 4, 256);
   const size_t o_cnt = off; off = align_up(off + size_t(kMaxGroup) * p->max_tiles * 4, 1024);
@@ -802,6 +958,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   const size_t o_tm = off; off = align_up(off + size_t(b->n_modules) * sizeof(CUtensorMap), 1024);
   const size_t o_ws = off; off = align_up(off + size_t(kMaxGroup) * p->ws_cap_rows * b->rp * 4, 1024);
   const size_t o_t = off; off = align_up(off + size_t(b->n_modules) * p->max_tiles * kTileM * 2 * b->rp * 2, 1024);
+  const size_t o_tp = off; off = align_up(off + size_t(kMaxGroup) * T_max * b->rp * 4, 1024);
   if (cudaMalloc(&p->arena, off) != cudaSuccess) { (void)cudaGetLastError(); delete p; return CTS_ERR_OUT_OF_MEMORY; }
   uint8_t* base = static_cast<uint8_t*>(p->arena);
   p->tok_adapter = reinterpret_cast<int32_t*>(base + o_tok);
@@ -811,6 +968,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->n_tiles = reinterpret_cast<int32_t*>(base + o_nt);
   p->tile_rows = reinterpret_cast<int32_t*>(base + o_trows);
   p->tile_adapters = reinterpret_cast<int32_t*>(base + o_tads);
+  p->sadapter = reinterpret_cast<int32_t*>(base + o_sad);
   p->err = reinterpret_cast<int32_t*>(base + o_err);
   p->n_unbound = reinterpret_cast<int32_t*>(base + o_unb);
   p->unbound_rows = p->n_unbound + 4;
@@ -820,6 +978,7 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->d_tm_t = reinterpret_cast<CUtensorMap*>(base + o_tm);
   p->ws = reinterpret_cast<float*>(base + o_ws);
   p->tbuf = reinterpret_cast<__nv_bfloat16*>(base + o_t);
+  p->tp_parts = reinterpret_cast<float*>(base + o_tp);
   const int32_t init_err[2] = {0, -1};
   bool ok = cudaMemset(p->n_tiles, 0, nm * 4) == cudaSuccess && cudaMemset(p->n_unbound, 0, 16) == cudaSuccess &&
             cudaMemset(p->tiles, 0, nm * p->max_tiles * 32) == cudaSuccess &&
@@ -862,6 +1021,7 @@ cts_status_t cts_segment(cts_plan_t p, const int32_t* token_adapter, int32_t T, 
   a.n_tiles = p->n_tiles;
   a.tile_rows = p->tile_rows;
   a.tile_adapters = p->tile_adapters;
+  a.sadapter = p->sadapter;
   a.err = p->err;
   a.unbound_rows = p->unbound_rows;
   a.n_unbound = p->n_unbound;
@@ -983,6 +1143,68 @@ cts_status_t cts_expand_reduced_group(cts_plan_t p, int32_t n, const int32_t* mo
   return do_expand(p, n, modules, ys, ld_y, stream);
 }
 
+cts_status_t cts_comm_unique_id(void* id_out) {
+  if (!id_out) return CTS_ERR_INVALID_ARGUMENT;
+  const NcclApi& api = nccl();
+  if (!api.ok) return CTS_ERR_NCCL;
+  NcclId id;
+  if (api.get_unique_id(&id) != 0) return CTS_ERR_NCCL;
+  std::memcpy(id_out, &id, sizeof(id));
+  return CTS_OK;
+}
+
+cts_status_t cts_comm_create(const void* nccl_unique_id, int32_t nranks, int32_t rank, cts_comm_t* out) {
+  if (!out) return CTS_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (!nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks) return CTS_ERR_INVALID_ARGUMENT;
+  const NcclApi& api = nccl();
+  if (!api.ok) return CTS_ERR_NCCL;
+  NcclId id;
+  std::memcpy(&id, nccl_unique_id, sizeof(id));
+  auto* c = new (std::nothrow) cts_comm_s();
+  if (!c) return CTS_ERR_OUT_OF_MEMORY;
+  c->nranks = nranks;
+  c->rank = rank;
+  if (api.comm_init_rank(&c->comm, nranks, id, rank) != 0) {
+    delete c;
+    return CTS_ERR_NCCL;
+  }
+  *out = c;
+  return CTS_OK;
+}
+
+cts_status_t cts_comm_free(cts_comm_t c) {
+  if (!c) return CTS_ERR_INVALID_ARGUMENT;
+  const NcclApi& api = nccl();
+  const int rc = api.ok ? api.comm_destroy(c->comm) : 1;
+  delete c;
+  return rc == 0 ? CTS_OK : CTS_ERR_NCCL;
+}
+
+cts_status_t cts_apply_tp(cts_plan_t p, int32_t n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
+                          void* const* ys, const int64_t* ld_y, float scale, cts_comm_t comm, cudaStream_t stream) {
+  if (!comm) return CTS_ERR_INVALID_ARGUMENT;
+  cts_status_t st = check_group(p, n, modules, xs, ld_x, true);
+  if (st != CTS_OK) return st;
+  if ((st = check_group(p, n, modules, ys, ld_y, false)) != CTS_OK) return st;
+  if (p->T == 0) return CTS_OK;
+  const NcclApi& api = nccl();
+  if (!api.ok) return CTS_ERR_NCCL;
+  const int rp = p->bank->rp;
+  float* parts[kMaxGroup];
+  for (int i = 0; i < n; ++i) parts[i] = p->tp_parts + size_t(i) * p->T_max * rp;
+  if ((st = do_shrink(p, n, modules, xs, ld_x, scale, stream, parts)) != CTS_OK) return st;
+  if (api.group_start() != 0) return CTS_ERR_NCCL;
+  for (int i = 0; i < n; ++i)
+    if (api.all_reduce(parts[i], parts[i], size_t(p->T) * rp, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm->comm, stream) != 0) {
+      api.group_end();
+      return CTS_ERR_NCCL;
+    }
+  if (api.group_end() != 0) return CTS_ERR_NCCL;
+  if ((st = do_split(p, n, modules, parts, stream)) != CTS_OK) return st;
+  return do_expand(p, n, modules, ys, ld_y, stream);
+}
+
 cts_status_t cts_shrink(cts_plan_t p, int32_t module, const void* x, int64_t ld_x, float scale, cudaStream_t stream) {
   return cts_shrink_group(p, 1, &module, &x, &ld_x, scale, stream);
 }
@@ -1077,6 +1299,9 @@ cts_status_t cts_rows_move(const void* src, int64_t ld_src, void* dst, int64_t l
 
 #ifdef CTS_TRACE
 // debug-only (not part of cts.h): copy the per-CTA timeline of the last traced launch
+int cts_debug_jobtrace(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_cts_jobtrace, std::min<size_t>(n, sizeof(g_cts_jobtrace) / 8) * 8) == cudaSuccess ? 0 : 1;
+}
 int cts_debug_trace(unsigned long long* host, int n) {
   return cudaMemcpyFromSymbol(host, g_cts_trace, std::min<size_t>(n, sizeof(g_cts_trace) / 8) * 8) == cudaSuccess ? 0 : 1;
 }

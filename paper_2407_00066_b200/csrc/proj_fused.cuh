@@ -76,15 +76,6 @@ struct ProjCfg {
   static constexpr uint32_t kTmemCols = kProjBN * kProjAccSlots;   // 512
 };
 
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
-                                            int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
 __global__ void __launch_bounds__(kApplyThreads, 1) proj_fused_kernel(const __grid_constant__ ProjParams p) {
   using L = ProjCfg;
   extern __shared__ uint8_t smem_raw[];

@@ -40,6 +40,7 @@ struct SegArgs {
   int32_t* n_tiles;              // [n_maps] number of slots
   int32_t* tile_rows;            // [n_maps][max_tiles*128] token of each tile row (dup of last past len)
   int32_t* tile_adapters;        // [n_maps][max_tiles*128] adapter of that token
+  int32_t* sadapter;             // [n_maps][T_max] adapter of each sorted position (apply_local)
   int32_t* err;                  // [2] code, first bad token
   int32_t* unbound_rows;         // [T_max + 128] tokens with id -1 in order, padded to a multiple of 128
   int32_t* n_unbound;            // [1] (0 if the batch is invalid)
@@ -134,8 +135,9 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
     if (map_id == 0) a.tok_adapter_copy[t] = id;
   }
   __syncthreads();
-  if (s_bad != 0x7fffffff) {                       // poison: no tiles for any module
+  if (s_bad != 0x7fffffff) {                       // poison: no tiles / no bound rows for any module
     for (int i = threadIdx.x; i < 2 * a.max_tiles; i += kSegThreads) tiles[i] = make_int4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i <= a.C; i += kSegThreads) offsets[i] = 0;
     if (threadIdx.x == 0) {
       a.n_tiles[map_id] = 0;
       if (map_id == 0) {
@@ -225,6 +227,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
     if (key >= 0) {
       const int rank = __popc(peers & ((1u << lane) - 1u));
       perm[my_hist[key] + rank] = t;
+      a.sadapter[static_cast<size_t>(map_id) * a.T_max + my_hist[key] + rank] = a.token_adapter[t];
     }
     __syncwarp();
     if (key >= 0 && lane == 31 - __clz(peers)) my_hist[key] += __popc(peers);

@@ -64,6 +64,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uin
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// 3-D tile load: box at (c0, c1, c2), innermost first.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 // Gather four rows (r0..r3) of box width starting at column c0 (box = {width, 1}).
 __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
                                             int r0, int r1, int r2, int r3) {
@@ -313,6 +321,20 @@ __device__ __forceinline__ void ld_global_nc_v8(const void* p, uint4& a, uint4& 
   asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
                : "l"(p));
+}
+// Shared-memory loads through explicit ld.shared (no generic-pointer aliasing with global stores).
+__device__ __forceinline__ __nv_bfloat16 ld_shared_bf16(const void* p) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(smem_u32(p)));
+  return __ushort_as_bfloat16(v);
+}
+__device__ __forceinline__ void st_shared_bf16(void* p, __nv_bfloat16 v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(smem_u32(p)), "h"(__bfloat16_as_ushort(v)) : "memory");
+}
+__device__ __forceinline__ int ld_shared_s32(const void* p) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)));
+  return v;
 }
 __device__ __forceinline__ void nanosleep_ns(uint32_t ns) { asm volatile("nanosleep.u32 %0;" ::"r"(ns)); }
 

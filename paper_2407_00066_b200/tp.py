@@ -49,6 +49,32 @@ def tp_apply_group(modules, x_shards, y_shards, parts, live, scale, shrink_parti
     expand_reduced(modules, parts, y_shards)
 
 
+def create_comm(rank, world, group=None, device=None):
+    """libcts NCCL communicator for the TP group: rank 0 draws the NCCL unique id through libcts,
+    torch.distributed broadcasts the 128 bytes, every rank calls cts_comm_create (plumbing only)."""
+    import torch
+    import torch.distributed as dist
+
+    from .api import Comm, cts_comm_unique_id
+    buf = torch.zeros(128, dtype=torch.uint8, device=device if device is not None else "cpu")
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(cts_comm_unique_id()), dtype=torch.uint8))
+    if world > 1:
+        dist.broadcast(buf, 0, group=group)
+    return Comm(bytes(buf.cpu().tolist()), world, rank)
+
+
+class LibTensorParallelApply:
+    """The TP d-split with the all-reduce issued INSIDE libcts (cts_apply_tp: shrink partial ->
+    ncclAllReduce -> split + expand on one stream, graph-capturable)."""
+
+    def __init__(self, plan, comm):
+        self.plan, self.comm = plan, comm
+
+    def apply_group(self, modules, x_shards, y_shards, scale=1.0):
+        self.plan.apply_tp(modules, x_shards, y_shards, self.comm, scale)
+
+
 class TensorParallelApply:
     """Rank-local driver over a Plan of this rank's bank shard; partial buffers are allocated once
     per group size (fixed pointers: the sequence is CUDA-graph capturable)."""

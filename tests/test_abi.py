@@ -76,3 +76,19 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(_lib.CtsLibraryError):
         _lib.lib()
+
+
+def test_comm_validation_before_nccl(lib):
+    """cts_comm_* / cts_apply_tp reject bad arguments before touching NCCL or the GPU."""
+    L = lib.lib()
+    out = ctypes.c_void_p()
+    uid = ctypes.create_string_buffer(128)
+    assert L.cts_comm_create(None, 2, 0, ctypes.byref(out)) == 1            # no id
+    assert L.cts_comm_create(uid, 0, 0, ctypes.byref(out)) == 1             # nranks < 1
+    assert L.cts_comm_create(uid, 2, 2, ctypes.byref(out)) == 1             # rank outside [0, nranks)
+    assert L.cts_comm_create(uid, 2, 0, None) == 1
+    assert out.value is None
+    assert L.cts_comm_free(None) == 1
+    assert L.cts_comm_unique_id(None) == 1
+    assert L.cts_apply_tp(None, 1, None, None, None, None, None, 1.0, None, None) == 1
+    assert L.cts_status_string(7) == b"NCCL unavailable or failed"

@@ -777,3 +777,127 @@ def test_gpu_jd_rank_deficient_cluster(cts, case):
         BA = B.astype(np.float32).astype(np.float64) @ A.astype(np.float32).astype(np.float64)
         rel = np.linalg.norm(U @ S[i] @ V.T - BA) / np.linalg.norm(BA)
         assert rel < (1e-3 if case == "ill_conditioned" else 2e-4), (case, i, rel)
+
+
+@pytest.mark.parametrize("shapes,N,C,T,frac_none", [
+    ([(1024, 1024), (1024, 256), (1024, 256)], 300, 12, 1024, 0.0),   # q,k,v-like group, decode
+    ([(512, 320)], 40, 5, 257, 0.1),                                 # ragged last 256-column job
+    ([(768, 512), (768, 512)], 500, 200, 333, 0.05),                 # many clusters, tiny pieces
+    ([(256, 256)], 8, 3, 5, 0.0),                                    # a handful of rows
+])
+def test_exchange_free_decode_kernel(cts, shapes, N, C, T, frac_none):
+    """apply_local.cuh (the decode-regime kernel: pieces of one cluster's rows, shrink, Sigma and the
+    transposed expand all in one CTA, no inter-CTA exchange): every row of every module of a grouped
+    launch vs the fp64 oracle, unbound rows untouched, residual contract with a random y_base."""
+    banks, f64s = [], []
+    for m, (di, do) in enumerate(shapes):
+        b, f = quantized_bank(di, do, N, C, 16, seed=500 + m, cluster_of=cluster_map(N, C, 510 + m))
+        banks.append(b)
+        f64s.append(f)
+    bank = make_bank(cts, banks)
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, N, 521, frac_none=frac_none)
+    plan.segment(torch.from_numpy(ta).cuda())
+    x = bf16_round(activations(T, shapes[0][0], 522))
+    ybits = [bf16_round(activations(T, do, 523 + m)) for m, (_, do) in enumerate(shapes)]
+    ys = [dev_bf16(b) for b in ybits]
+    yz = [torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes]
+    mods = list(range(len(shapes)))
+    plan.apply_group(mods, [dev_bf16(x)] * len(mods), ys, 1.5)
+    plan.apply_group(mods, [dev_bf16(x)] * len(mods), yz, 1.5)
+    torch.cuda.synchronize()
+    for m in mods:
+        check_delta(ta, host_bits(yz[m]), f64s[m], x, 1.5)
+        dy, yref = apply_ref(bf16_to_f64(x), ta, f64s[m]["cluster_of"], f64s[m]["in_basis"], f64s[m]["out_basis"],
+                             f64s[m]["sigma"], 1.5, y_base=bf16_to_f64(ybits[m]))
+        got = host_bits(ys[m])
+        assert np.array_equal(got[ta < 0], ybits[m][ta < 0])
+        g = bf16_to_f64(got)
+        assert np.all(np.abs(g - yref) <= bf16_ulp(yref) + 1e-3 * np.abs(dy).max(axis=1, keepdims=True))
+    plan.close()
+    bank.close()
+
+
+def test_two_streams_concurrent_applies(cts):
+    """cts.h allows several plans / streams to apply the same bank concurrently: two plans on two
+    streams, 40 grouped launches each, interleaved; both results vs the oracle (a deadlock would hang
+    the test under its timeout)."""
+    N, C, T = 400, 16, 512
+    shapes = [(1024, 1024), (1024, 512)]
+    banks, f64s = [], []
+    for m, (di, do) in enumerate(shapes):
+        b, f = quantized_bank(di, do, N, C, 16, seed=600 + m, cluster_of=cluster_map(N, C, 610 + m))
+        banks.append(b)
+        f64s.append(f)
+    bank = make_bank(cts, banks)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    plans, tas, xs, ys = [], [], [], []
+    for k in range(2):
+        plan = cts.Plan(bank, T)
+        ta = decode_tokens(T, N, 620 + k)
+        with torch.cuda.stream(streams[k]):
+            plan.segment(torch.from_numpy(ta).cuda())
+        plans.append(plan)
+        tas.append(ta)
+        xs.append(bf16_round(activations(T, 1024, 630 + k)))
+        ys.append([torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes])
+    torch.cuda.synchronize()
+    xd = [dev_bf16(x) for x in xs]
+    for rep in range(40):
+        for k in range(2):
+            with torch.cuda.stream(streams[k]):
+                if rep == 39:
+                    for y in ys[k]:
+                        y.zero_()
+                plans[k].apply_group([0, 1], [xd[k], xd[k]], ys[k], 1.0)
+    torch.cuda.synchronize()
+    for k in range(2):
+        for m in range(2):
+            check_delta(tas[k], host_bits(ys[k][m]), f64s[m], xs[k], 1.0)
+    for pl in plans:
+        pl.close()
+    bank.close()
+
+
+def test_apply_tp_nccl_inside_library_world1(cts):
+    """cts_comm_create + cts_apply_tp: the TP d-split with the NCCL all-reduce issued
+    by libcts.  One rank (the box has one GPU): shrink partial -> ncclAllReduce over a 1-rank
+    communicator -> split + expand; every row vs the oracle, then the same sequence captured in a
+    CUDA graph and replayed (NCCL is graph-capturable) gives identical bits."""
+    N, C, T = 120, 5, 333
+    shapes = [(1024, 512), (1024, 1024)]
+    banks, f64s = [], []
+    for m, (di, do) in enumerate(shapes):
+        b, f = quantized_bank(di, do, N, C, 16, seed=940 + m, cluster_of=cluster_map(N, C, 950 + m))
+        banks.append(b)
+        f64s.append(f)
+    bank = make_bank(cts, banks)
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, N, 961, frac_none=0.05)
+    plan.segment(torch.from_numpy(ta).cuda())
+    comm = cts.Comm(cts.cts_comm_unique_id(), 1, 0)
+    xb = bf16_round(activations(T, 1024, 962))
+    x = dev_bf16(xb)
+    ys = [torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes]
+    plan.apply_tp([0, 1], [x, x], ys, comm, 2.0)
+    torch.cuda.synchronize()
+    for m in range(2):
+        check_delta(ta, host_bits(ys[m]), f64s[m], xb, 2.0)
+    first = [host_bits(y) for y in ys]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        for y in ys:
+            y.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            plan.apply_tp([0, 1], [x, x], ys, comm, 2.0)
+        for y in ys:
+            y.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    for m in range(2):
+        assert np.array_equal(host_bits(ys[m]), first[m])
+    comm.close()
+    plan.close()
+    bank.close()
