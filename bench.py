@@ -304,7 +304,9 @@ def config_dict(cfg, world):
             "n_adapters": cfg["N"], "n_clusters": cfg["C"], "rank": cfg["r"], "tokens_per_gpu": cfg["T"],
             "cluster_maps": "per module", "parallelism": f"dp{world} (replicated bank, request sharding)",
             "l2": "inputs larger than L2: every module reads its own x/y/bases (>= 10 GB per step vs 126 MB L2)",
-            "timing": "one CUDA graph per step (segment + all applies), CUDA events, max over ranks"}
+            "timing": "one CUDA graph per step (segment + all applies), CUDA events, max over ranks",
+            "device_mode": "exclusive (cts_set_exclusive_device): the process owns the GPU, fused applies launch "
+                           "non-cooperatively; the library default is cooperative (~4% slower at decode)"}
 
 
 # ----------------------------------------------------------------------------- GPU leg, TP d-split
@@ -538,6 +540,8 @@ def run_gpu(args, cfg):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    # the bench process owns its GPU and issues every apply on one stream (cts.h contract)
+    cts.cts_set_exclusive_device(True)
 
     T, N, C, r = cfg["T"], cfg["N"], cfg["C"], cfg["r"]
     mods = module_list(cfg)

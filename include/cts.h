@@ -48,6 +48,13 @@ typedef struct cts_bank_s* cts_bank_t;   /* owns all device copies of a compress
 typedef struct cts_plan_s* cts_plan_t;   /* per-batch segmentation + scratch, reusable        */
 typedef struct cts_comm_s* cts_comm_t;   /* NCCL communicator of a tensor-parallel group     */
 
+/* Storage kind of the per-adapter matrices Sigma_i.
+ *   CTS_SIGMA_FULL: JD-Full (Eq. 2), Sigma_i an arbitrary r x r matrix.
+ *   CTS_SIGMA_DIAG: JD-Diag (Eq. 3), Sigma_i diagonal; only its r diagonal entries are
+ *                   stored and applied ("batched matrix multiplications can be completely
+ *                   circumvented", App D): t = scale * sigma_i (elementwise) * (V_c^T x). */
+typedef enum { CTS_SIGMA_FULL = 0, CTS_SIGMA_DIAG = 1 } cts_sigma_kind_t;
+
 /*
  * A compressed collection for n_modules projections (e.g. 224 = 32 layers x q,k,v,o,gate,up,
  * down of Mistral-7B).  Every module shares N adapters, C clusters and one rank r (one r for all
@@ -63,17 +70,20 @@ typedef struct {
   const int32_t* d_out;          /* host [n_modules]; each a positive multiple of 64           */
   const void* const* in_basis;   /* host array [n_modules] of -> bf16 [C][d_in][r] row-major   */
   const void* const* out_basis;  /* host array [n_modules] of -> bf16 [C][d_out][r] row-major  */
-  const void* const* sigma;      /* host array [n_modules] of -> bf16 [N][r][r], row = out idx */
+  const void* const* sigma;      /* host array [n_modules] of -> bf16 [N][r][r], row = out idx;
+                                    CTS_SIGMA_DIAG: bf16 [N][r], the diagonals                 */
   const int32_t* const* cluster_of; /* host array [n_modules] of -> int32 [N], values in [0,C) */
   int32_t sources_on_device;     /* 0: the four pointer arrays point to host memory;
                                     1: they point to device memory                             */
+  int32_t sigma_kind;            /* cts_sigma_kind_t; 0 (zero-initialised descriptor) = full    */
 } cts_bank_desc_t;
 
 /* Copy and re-lay-out a compressed collection into device memory (the resident bank that lets
  * "U and V be pre-loaded onto the GPU").  SYNCHRONOUS: when it returns the sources may be
  * freed.  Layout on device: in_basis [C][r_pad][d_in] (K-major operand of the shrink GEMM),
- * out_basis [C][d_out][r_pad], sigma [N][r_pad][r_pad], one int32 map per distinct cluster map.
- * Errors: CTS_ERR_INVALID_ARGUMENT (null), CTS_ERR_SHAPE (dims), CTS_ERR_INDEX_OUT_OF_RANGE
+ * out_basis [C][d_out][r_pad], sigma [N][r_pad][r_pad] (CTS_SIGMA_DIAG: [N][r_pad]), one int32 map
+ * per distinct cluster map.
+ * Errors: CTS_ERR_INVALID_ARGUMENT (null, unknown sigma_kind), CTS_ERR_SHAPE (dims), CTS_ERR_INDEX_OUT_OF_RANGE
  * (cluster id), CTS_ERR_UNSUPPORTED (device is not sm_100, r > 64, C > 1024), CTS_ERR_OUT_OF_MEMORY.
  * On error *out is set to NULL and nothing stays allocated. */
 cts_status_t cts_bank_load(const cts_bank_desc_t* desc, cudaStream_t stream, cts_bank_t* out);
@@ -82,7 +92,8 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* desc, cudaStream_t stream, cts
 cts_status_t cts_bank_bytes(cts_bank_t bank, size_t* device_bytes);
 
 /* Parameter count of the bank as App F counts it for module m:
- * sum over clusters of (d_in + d_out) * r  +  N * (r^2 + (C > 1 ? 1 : 0)).  Unpadded. */
+ * sum over clusters of (d_in + d_out) * r  +  N * (r^2 + (C > 1 ? 1 : 0)).  Unpadded.
+ * CTS_SIGMA_DIAG banks count r instead of r^2 per adapter (JD-Diag, Eq. 3). */
 cts_status_t cts_bank_params(cts_bank_t bank, int32_t module, int64_t* params);
 
 /* Release all device memory of the bank.  The caller must ensure no apply still uses it. */
@@ -130,9 +141,9 @@ cts_status_t cts_segment_readback(cts_plan_t plan, int32_t module, int32_t* perm
  * per-token Sigma_i matvec in its epilogue), then expand + residual (tcgen05, y rows moved by TMA)
  * as each slot's rank-r intermediate is published (CTS_FUSED=0: the two as separate launches).
  * Progress of the single launch relies on its CTAs (at most one per SM) being co-resident: expand
- * work waits on flags that other CTAs' shrink work publishes.  With exclusive use of the GPU that
- * always holds; when other kernels may occupy SMs for long (another stream, MPS), run with
- * CTS_FUSED=0 -- the two-launch path has no inter-CTA waits.
+ * work waits on flags that other CTAs' shrink work publishes.  The launch is therefore COOPERATIVE
+ * (the runtime starts it only when every CTA can be resident), so concurrent applies on other
+ * streams cannot deadlock it; see cts_set_exclusive_device for the non-cooperative variant.
  * Deterministic (no float atomics; the reduction order does not depend on scheduling).
  * Host validation: CTS_ERR_INVALID_ARGUMENT (null, x/y overlap), CTS_ERR_SHAPE (module index,
  * ld_x < d_in, ld_y < d_out, ld or pointer not 16-byte aligned). */
@@ -290,6 +301,16 @@ cts_status_t cts_plan_error(cts_plan_t plan, int32_t* code, int32_t* first_bad_t
 
 /* Static description of a status code. */
 const char* cts_status_string(cts_status_t status);
+
+/* Declare (1) or revoke (0, the default) exclusive use of the current process's device by libcts
+ * launches: the caller guarantees that no other kernel (another stream of this process, another
+ * process under MPS) runs while a fused apply is in flight -- e.g. a serving process that owns the
+ * GPU and issues its applies on one stream.  Fused applies then launch NON-cooperatively, which
+ * lets their prologue overlap the previous kernel's tail under programmatic dependent launch
+ * (~1.3 us per launch at decode, measured); under sharing that variant can deadlock (its CTAs wait
+ * on flags of CTAs that are not resident), so leave the default when unsure.  Process-wide; takes
+ * effect for launches enqueued (or captured) afterwards.  Errors: CTS_ERR_INVALID_ARGUMENT. */
+cts_status_t cts_set_exclusive_device(int32_t exclusive);
 
 /* Number of kernels this library has enqueued since it was loaded (process-wide, all banks and
  * plans; launches recorded into a CUDA graph under stream capture count once, at capture).  The

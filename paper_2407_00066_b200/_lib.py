@@ -28,7 +28,7 @@ EXPORTS = (
     "cts_apply_group", "cts_shrink_group", "cts_expand_group", "cts_plan_error", "cts_status_string",
     "cts_launch_count", "cts_plan_partial_elems", "cts_shrink_partial_group", "cts_expand_reduced_group",
     "cts_project", "cts_jd_workspace_bytes", "cts_jd_eigen_iteration", "cts_route", "cts_rows_move",
-    "cts_comm_unique_id", "cts_comm_create", "cts_comm_free", "cts_apply_tp",
+    "cts_comm_unique_id", "cts_comm_create", "cts_comm_free", "cts_apply_tp", "cts_set_exclusive_device",
 )
 
 
@@ -69,6 +69,7 @@ class BankDesc(ctypes.Structure):
         ("sigma", ctypes.POINTER(ctypes.c_void_p)),
         ("cluster_of", ctypes.POINTER(ctypes.c_void_p)),
         ("sources_on_device", ctypes.c_int32),
+        ("sigma_kind", ctypes.c_int32),
     ]
 
 
@@ -106,6 +107,7 @@ def lib():
         "cts_plan_error": ([P, ctypes.POINTER(I32), ctypes.POINTER(I32)], I32),
         "cts_status_string": ([I32], ctypes.c_char_p),
         "cts_launch_count": ([], ctypes.c_uint64),
+        "cts_set_exclusive_device": ([I32], I32),
         "cts_plan_partial_elems": ([P, ctypes.POINTER(I64)], I32),
         "cts_shrink_partial_group": ([P, I32, VP, VP, VP, F, VP, P], I32),
         "cts_expand_reduced_group": ([P, I32, VP, VP, VP, VP, P], I32),

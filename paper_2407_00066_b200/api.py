@@ -21,15 +21,20 @@ def _bf16(t, name):
     return t
 
 
+SIGMA_FULL, SIGMA_DIAG = 0, 1          # cts_sigma_kind_t
+
+
 def cts_bank_load(in_basis, out_basis, sigma, cluster_of, stream=None):
     """in_basis[m]: [C][d_in][r] bf16 (paper V_c), out_basis[m]: [C][d_out][r] bf16 (paper U_c),
-    sigma[m]: [N][r][r] bf16 (row = out index), cluster_of[m]: [N] int32.  All on the GPU or all
-    on the host.  Returns an opaque bank handle (ctypes.c_void_p)."""
+    sigma[m]: [N][r][r] bf16 (row = out index; JD-Full) or [N][r] bf16 (the diagonals; JD-Diag,
+    Eq. 3 -> CTS_SIGMA_DIAG), cluster_of[m]: [N] int32.  All on the GPU or all on the host.
+    Returns an opaque bank handle (ctypes.c_void_p)."""
     M = len(in_basis)
     if not (len(out_basis) == len(sigma) == len(cluster_of) == M) or M == 0:
         raise ValueError("per-module lists must have the same non-zero length")
     C, _, r = in_basis[0].shape
     N = sigma[0].shape[0]
+    diag = sigma[0].dim() == 2
     on_dev = in_basis[0].is_cuda
     keep = []
     for m in range(M):
@@ -40,15 +45,16 @@ def cts_bank_load(in_basis, out_basis, sigma, cluster_of, stream=None):
         cm = cluster_of[m]
         if cm.dtype != torch.int32 or not cm.is_contiguous() or cm.is_cuda != on_dev:
             raise TypeError("cluster_of must be contiguous int32 on the same device as the bases")
+        sig_shape = (N, r) if diag else (N, r, r)
         if in_basis[m].shape[0] != C or in_basis[m].shape[2] != r or out_basis[m].shape[0] != C \
-                or out_basis[m].shape[2] != r or tuple(sigma[m].shape) != (N, r, r) or cm.shape[0] != N:
+                or out_basis[m].shape[2] != r or tuple(sigma[m].shape) != sig_shape or cm.shape[0] != N:
             raise ValueError(f"module {m}: inconsistent bank shapes")
         keep += [in_basis[m], out_basis[m], sigma[m], cm]
     d_in = (ctypes.c_int32 * M)(*[int(t.shape[1]) for t in in_basis])
     d_out = (ctypes.c_int32 * M)(*[int(t.shape[1]) for t in out_basis])
     ptrs = lambda ts: (ctypes.c_void_p * M)(*[t.data_ptr() for t in ts])  # noqa: E731
     desc = BankDesc(M, N, C, r, d_in, d_out, ptrs(in_basis), ptrs(out_basis), ptrs(sigma), ptrs(cluster_of),
-                    1 if on_dev else 0)
+                    1 if on_dev else 0, SIGMA_DIAG if diag else SIGMA_FULL)
     h = ctypes.c_void_p()
     check("cts_bank_load", lib().cts_bank_load(ctypes.byref(desc), _stream_handle(stream), ctypes.byref(h)))
     del keep
@@ -305,6 +311,12 @@ def cts_apply_tp(plan, modules, xs, ys, comm, scale=1.0, stream=None):
                                              _stream_handle(stream)))
 
 
+def cts_set_exclusive_device(exclusive):
+    """Declare (True) or revoke (False, default) exclusive use of the GPU by libcts launches: fused
+    applies then launch non-cooperatively (cts.h: only safe when no other kernel runs concurrently)."""
+    check("cts_set_exclusive_device", lib().cts_set_exclusive_device(1 if exclusive else 0))
+
+
 def cts_launch_count():
     """Kernels libcts has enqueued since load (graph captures count once, at capture)."""
     return int(lib().cts_launch_count())
@@ -318,6 +330,7 @@ class Bank:
         self.n_modules = len(in_basis)
         self.C = int(in_basis[0].shape[0])
         self.N = int(sigma[0].shape[0])
+        self.sigma_diag = sigma[0].dim() == 2
         self.r = int(in_basis[0].shape[2])
         self.d_in = [int(t.shape[1]) for t in in_basis]
         self.d_out = [int(t.shape[1]) for t in out_basis]

@@ -42,7 +42,7 @@ struct FusedSmem {
   static_assert(ShrinkCfg<RP>::kTmemCols <= kTmemCols && ExpandCfg<RP>::kTmemCols <= kTmemCols, "TMEM");
 };
 
-template <int RP, int STORE>
+template <int RP, int STORE, bool DIAG>
 __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __grid_constant__ FusedParams p) {
   using S = FusedSmem<RP>;
   extern __shared__ uint8_t smem_raw[];
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
     tc_fence_after();
     expand_mma<RP>(p.e, RE, nt_lane, lane, deal_r0, deal_k);
   } else {
-    shrink_epilogue<RP>(p.s, RS, W, warp, lane);
+    shrink_epilogue<RP, DIAG>(p.s, RS, W, warp, lane);
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(tmem_free);
@@ -141,7 +141,6 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
       for (int i = threadIdx.x; i < p.s.tiles_bound; i += blockDim.x) p.s.mod[g].ready[i] = 0;
     if (threadIdx.x == 0) {
       *p.exit_count = 0;
-      if (p.e.dyn_next != nullptr) *p.e.dyn_next = 0;   // expand dynamic-tail counter
     }
   }
   if (warp == kMmaWarp) tmem_dealloc<S::kTmemCols>(RS.tmem);

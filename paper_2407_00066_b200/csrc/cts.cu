@@ -16,7 +16,6 @@
 
 #include "../../include/cts.h"
 #include "apply_fused.cuh"
-#include "apply_local.cuh"
 #include "expand.cuh"
 #include "proj_fused.cuh"
 #include "jd_eigen.cuh"
@@ -129,20 +128,19 @@ struct Module {
   int d_in, d_out, map_id;
   __nv_bfloat16* in_t;    // [C][rp][d_in]
   __nv_bfloat16* out;     // [C][d_out][rp]
-  __nv_bfloat16* sigma;   // [N][rp][rp]
+  __nv_bfloat16* sigma;   // [N][rp][rp], or [N][rp] (diagonal kind)
 };
 
 }  // namespace
 
 struct cts_bank_s {
   int n_modules, N, C, r, rp;
+  int sigma_diag;         // CTS_SIGMA_DIAG: Sigma_i stored as its diagonal (JD-Diag, Eq. 3)
   std::vector<Module> mods;
   int n_maps;
   int32_t* maps;          // [n_maps][N]
   CUtensorMap* d_tm_in;   // [n_modules] device copies (TMA descriptors in global memory)
   CUtensorMap* d_tm_out;  // [n_modules]
-  CUtensorMap* d_tm_in3;  // [n_modules] in_basis as {64, C*rp, d_in/64}, box {64, rp, kLocKB} (apply_local)
-  CUtensorMap* d_tm_out256;  // [n_modules] out_basis, box {rp, 256} (apply_local)
   void* arena;
   size_t bytes;
 };
@@ -159,7 +157,6 @@ struct cts_plan_s {
   int32_t* n_tiles;       // [n_maps]
   int32_t* tile_rows;     // [n_maps][max_tiles*128]
   int32_t* tile_adapters; // [n_maps][max_tiles*128]
-  int32_t* sadapter;      // [n_maps][T_max] adapter of each cluster-sorted position
   int32_t* err;           // [2]
   int32_t* unbound_rows;  // [T_max + 128] tokens with id -1 (fused projection)
   int32_t* n_unbound;     // [1]
@@ -208,15 +205,15 @@ cudaError_t set_smem(Kern kernel, int bytes) {
 // expand store path (expand.cuh STORE modes): register-direct stores when tiles are small
 // (latency-bound decode: the stage is freed right after the y_base reads), TMA scatter when tiles
 // are full (bandwidth-bound prefill).  Measured on B200 (expand us per launch, decode / prefill):
-// scatter 21.4 / 150.7, direct 19.4 / 179.1, coalesced row copies out of the stage 23.7 / 160.9
-// (the extra shared-memory round trip costs more than the 8x fewer store wavefronts save).
-// CTS_EXPAND_STORE = 0 / 1 / 2 forces scatter / direct / coalesced (tuning aid).
+// scatter 21.4 / 150.7, direct 19.4 / 179.1 (row copies out of the stage, 23.7 / 160.9, were
+// removed: the extra shared-memory round trip cost more than the fewer store wavefronts saved).
+// CTS_EXPAND_STORE = 0 / 1 forces scatter / direct (tuning aid).
 int expand_store_mode(int T, int C) {
   static int v = [] {
     const char* e = std::getenv("CTS_EXPAND_STORE");
     return e ? std::atoi(e) : -1;
   }();
-  if (v >= 0 && v <= 2) return v;
+  if (v == 0 || v == 1) return v;
   return T < 96 * C ? kStoreDirect : kStoreScatter;   // mean tokens per cluster < 96
 }
 
@@ -251,25 +248,42 @@ bool use_fused() {
   return v;
 }
 
+// The fused kernel launches cooperatively unless the caller declared exclusive use of the device
+// (cts_set_exclusive_device): a cooperative launch cannot start before every CTA fits, so it loses
+// the PDL overlap of its prologue with the previous kernel's tail (measured ~1.3 us per launch).
+std::atomic<int> g_exclusive{0};
+bool use_cooperative() { return g_exclusive.load(std::memory_order_relaxed) == 0; }
+
 // Launch with programmatic stream serialization (PDL): the kernel may start while the previous
 // kernel in the stream drains; every kernel calls griddep_wait() before touching dependent data.
 std::atomic<uint64_t> g_launches{0};          // kernels this library enqueued (cts_launch_count)
 
+// cooperative = 1: the launch is cooperative, i.e. the runtime only starts it when every CTA can be
+// resident at once -- the fused kernel's inter-CTA waits (expand producers polling t-ready flags
+// published by other CTAs) rely on that, also when other streams run kernels concurrently.
 template <typename Kern, typename... Args>
-cudaError_t launch_pdl(Kern kernel, int grid, int block, size_t smem, cudaStream_t stream, Args... args) {
+cudaError_t launch_pdl_ex(Kern kernel, int grid, int block, size_t smem, cudaStream_t stream, bool cooperative,
+                          Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(block, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = cooperative ? 2 : 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
   if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
   return e;
+}
+
+template <typename Kern, typename... Args>
+cudaError_t launch_pdl(Kern kernel, int grid, int block, size_t smem, cudaStream_t stream, Args... args) {
+  return launch_pdl_ex(kernel, grid, block, smem, stream, false, args...);
 }
 
 __nv_bfloat16* module_tbuf(cts_plan_t p, int module) {
@@ -306,6 +320,7 @@ cts_status_t fill_shrink(cts_plan_t p, int n, const int32_t* modules, const void
   prm.tiles_bound = tiles_bound;
   prm.ks_max = ks_max;
   prm.target_items = target_items_per_sm();
+  prm.sigma_diag = b->sigma_diag;
   for (int i = 0; i < n; ++i) {
     const Module& m = b->mods[modules[i]];
     ShrinkMod& sm = prm.mod[i];
@@ -367,14 +382,17 @@ cts_status_t fill_expand(cts_plan_t p, int n, const int32_t* modules, void* cons
 template <int RP>
 cts_status_t launch_shrink(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
                            float scale, cudaStream_t stream, float* const* parts = nullptr) {
-  static const cudaError_t attr = set_smem(shrink_sigma_kernel<RP>, ShrinkKernelSmem<RP>::kBytes);
+  static const cudaError_t attr = set_smem(shrink_sigma_kernel<RP, false>, ShrinkKernelSmem<RP>::kBytes);
+  static const cudaError_t attr_d = set_smem(shrink_sigma_kernel<RP, true>, ShrinkKernelSmem<RP>::kBytes);
   CTS_CUDA(attr);
+  CTS_CUDA(attr_d);
   ShrinkParams prm;
   int items = 0;
   cts_status_t st = fill_shrink(p, n, modules, xs, ld_x, scale, false, prm, items, parts);
   if (st != CTS_OK) return st;
   prm.meta_ready = next_meta_ready(p);
-  CTS_CUDA(launch_pdl(shrink_sigma_kernel<RP>, std::min(sm_count(), items), kApplyThreads,
+  CTS_CUDA(launch_pdl(prm.sigma_diag ? shrink_sigma_kernel<RP, true> : shrink_sigma_kernel<RP, false>,
+                      std::min(sm_count(), items), kApplyThreads,
                       ShrinkKernelSmem<RP>::kBytes, stream, prm));
   return CTS_OK;
 }
@@ -397,8 +415,10 @@ cts_status_t launch_expand(cts_plan_t p, int n, const int32_t* modules, void* co
 template <int RP, int STORE>
 cts_status_t launch_fused(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
                           void* const* ys, const int64_t* ld_y, float scale, cudaStream_t stream) {
-  static const cudaError_t attr = set_smem(apply_fused_kernel<RP, STORE>, FusedSmem<RP>::kBytes);
+  static const cudaError_t attr = set_smem(apply_fused_kernel<RP, STORE, false>, FusedSmem<RP>::kBytes);
+  static const cudaError_t attr_d = set_smem(apply_fused_kernel<RP, STORE, true>, FusedSmem<RP>::kBytes);
   CTS_CUDA(attr);
+  CTS_CUDA(attr_d);
   FusedParams prm;
   int items_s = 0, items_e = 0;
   cts_status_t st = fill_shrink(p, n, modules, xs, ld_x, scale, true, prm.s, items_s);
@@ -408,102 +428,9 @@ cts_status_t launch_fused(cts_plan_t p, int n, const int32_t* modules, const voi
   prm.e.poll_first = poll_first_default(p->T, p->bank->C);
   prm.e.early_items = early_items_default();
   prm.exit_count = p->exit_count;
-  prm.e.dyn_next = p->exit_count + 1;            // zeroed with the flags; reset by the last CTA
-  CTS_CUDA(launch_pdl(apply_fused_kernel<RP, STORE>, std::min(sm_count(), std::max(items_s, items_e)), kApplyThreads,
-                      FusedSmem<RP>::kBytes, stream, prm));
-  return CTS_OK;
-}
-
-// apply_local (exchange-free, decode regime) vs apply_fused (split-K + flags): CTS_LOCAL=0 forces the
-// latter (tuning aid).
-bool use_local() {
-  static bool v = [] {
-    const char* e = std::getenv("CTS_LOCAL");
-    return e ? std::atoi(e) != 0 : true;
-  }();
-  return v;
-}
-
-constexpr int kLocSmemMax = 232448 - 512;   // dynamic shared memory cap (227 KB minus static)
-
-// Host half of apply_local's work map and shared-memory plan.  Rows per piece target u_g: every CTA
-// should move about the same bytes, a token row of module g costs d_in + 2 d_out elements, so
-// u_g = round((T * sum_h (d_in_h + 2 d_out_h) / grid) / (d_in_g + 2 d_out_g)).  A piece holds at
-// most ~1.5 u_g rows (device rounding), capped by lcap.  Returns false when the batch is not in the
-// kernel's regime (r_pad != 16, pieces above kLocMaxRows rows -- prefill -- or shapes it does not
-// tile); apply_fused then runs.
-bool local_plan(cts_plan_t p, int n, const int32_t* modules, LocParams& prm, int& smem) {
-  const cts_bank_t b = p->bank;
-  if (!use_local() || b->rp != kLocRP || n * (b->C + 1) + 1 > kLocTable) return false;
-  const int G = sm_count();
-  double per_row = 0;
-  for (int i = 0; i < n; ++i) {
-    const Module& m = b->mods[modules[i]];
-    if (m.d_in % (64 * kLocKB) || m.d_out < kLocBN) return false;
-    per_row += m.d_in + 2.0 * m.d_out;
-  }
-  const double cstar = per_row * p->T / G;
-  int lcap = 8;
-  for (int i = 0; i < n; ++i) {
-    const Module& m = b->mods[modules[i]];
-    const int u = std::max(1, static_cast<int>(cstar / (m.d_in + 2.0 * m.d_out) + 0.5));
-    prm.mod[i].unit_rows = u;
-    lcap = std::max(lcap, (3 * u + 1) / 2 + 1);
-  }
-  lcap = (lcap + 7) / 8 * 8;
-  if (lcap > kLocMaxRows) return false;
-  const int npad = (lcap + 15) / 16 * 16;
-  const int n_acc = std::min(8, (512 - kLocE0) / (2 * npad));
-  const LocLayout L0 = loc_layout(n, b->C, lcap, npad, 0, 0, n_acc);
-  const int avail = kLocSmemMax - L0.total - (2 * 16 + 2 * 16) * 8;
-  const int S = std::max(2, std::min(16, static_cast<int>(CTS_LOC_SFRAC / 100.0 * avail) / L0.s_bytes));
-  const int E = std::max(2, std::min(16, (avail - S * L0.s_bytes) / L0.e_bytes));
-  const LocLayout L = loc_layout(n, b->C, lcap, npad, S, E, n_acc);
-  // the shrink MMA reads 128 rows (16 KB) from every K block's A base: stay inside the allocation
-  if (L.total > kLocSmemMax || L.sring + S * L.s_bytes + 16384 > L.total) return false;
-  prm.n_mod = n;
-  prm.C = b->C;
-  prm.lcap = lcap;
-  prm.npad = npad;
-  prm.s_stages = S;
-  prm.e_stages = E;
-  prm.n_acc = n_acc;
-  smem = L.total;
-  return true;
-}
-
-cts_status_t launch_local(cts_plan_t p, int n, const int32_t* modules, const void* const* xs, const int64_t* ld_x,
-                          void* const* ys, const int64_t* ld_y, float scale, cudaStream_t stream, bool& done) {
-  done = false;
-  LocParams prm;
-  std::memset(&prm, 0, sizeof(prm));
-  int smem = 0;
-  if (!local_plan(p, n, modules, prm, smem)) return CTS_OK;
-  static const cudaError_t attr = set_smem(apply_local_kernel, kLocSmemMax);
-  CTS_CUDA(attr);
-  const cts_bank_t b = p->bank;
-  for (int i = 0; i < n; ++i) {
-    const Module& m = b->mods[modules[i]];
-    LocMod& lm = prm.mod[i];
-    if (!make_tmap(&lm.tm_x, xs[i], m.d_in, p->T, ld_x[i] * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap(&lm.tm_y, ys[i], m.d_out, p->T, ld_y[i] * 2, kLocBN, 1, CU_TENSOR_MAP_SWIZZLE_NONE))
-      return CTS_ERR_CUDA;
-    lm.tm_in3 = b->d_tm_in3 + modules[i];
-    lm.tm_out = b->d_tm_out256 + modules[i];
-    const size_t mid = m.map_id;
-    lm.offsets = p->offsets + mid * (b->C + 1);
-    lm.perm = p->perm + mid * p->T_max;
-    lm.sadapter = p->sadapter + mid * p->T_max;
-    lm.sigma = m.sigma;
-    lm.y = static_cast<__nv_bfloat16*>(ys[i]);
-    lm.ld_y = ld_y[i];
-    lm.d_in = m.d_in;
-    lm.d_out = m.d_out;
-    lm.scale = scale;
-  }
-  prm.meta_ready = next_meta_ready(p);
-  CTS_CUDA(launch_pdl(apply_local_kernel, sm_count(), kLocThreads, smem, stream, prm));
-  done = true;
+  CTS_CUDA(launch_pdl_ex(prm.s.sigma_diag ? apply_fused_kernel<RP, STORE, true> : apply_fused_kernel<RP, STORE, false>,
+                         std::min(sm_count(), std::max(items_s, items_e)),
+                         kApplyThreads, FusedSmem<RP>::kBytes, stream, use_cooperative(), prm));
   return CTS_OK;
 }
 
@@ -563,13 +490,10 @@ cts_status_t dispatch_rp_store(int rp, int store, A... a) {
   switch (rp * 4 + store) {
     case 16 * 4 + kStoreScatter: return F<16, kStoreScatter>::run(a...);
     case 16 * 4 + kStoreDirect: return F<16, kStoreDirect>::run(a...);
-    case 16 * 4 + kStoreCoalesced: return F<16, kStoreCoalesced>::run(a...);
     case 32 * 4 + kStoreScatter: return F<32, kStoreScatter>::run(a...);
     case 32 * 4 + kStoreDirect: return F<32, kStoreDirect>::run(a...);
-    case 32 * 4 + kStoreCoalesced: return F<32, kStoreCoalesced>::run(a...);
     case 64 * 4 + kStoreScatter: return F<64, kStoreScatter>::run(a...);
-    case 64 * 4 + kStoreDirect: return F<64, kStoreDirect>::run(a...);
-    default: return F<64, kStoreCoalesced>::run(a...);
+    default: return F<64, kStoreDirect>::run(a...);
   }
 }
 template <int RP, int STORE>
@@ -592,9 +516,6 @@ cts_status_t do_expand(cts_plan_t p, int n, const int32_t* mods, void* const* ys
 
 cts_status_t do_fused(cts_plan_t p, int n, const int32_t* mods, const void* const* xs, const int64_t* ldx,
                       void* const* ys, const int64_t* ldy, float scale, cudaStream_t s) {
-  bool done = false;
-  const cts_status_t st = launch_local(p, n, mods, xs, ldx, ys, ldy, scale, s, done);
-  if (st != CTS_OK || done) return st;
   return dispatch_rp_store<FusedLaunch>(p->bank->rp, expand_store_mode(p->T, p->bank->C), p, n, mods, xs, ldx, ys,
                                         ldy, scale, s);
 }
@@ -787,6 +708,12 @@ const char* cts_status_string(cts_status_t s) {
 
 uint64_t cts_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+cts_status_t cts_set_exclusive_device(int32_t exclusive) {
+  if (exclusive != 0 && exclusive != 1) return CTS_ERR_INVALID_ARGUMENT;
+  g_exclusive.store(exclusive, std::memory_order_relaxed);
+  return CTS_OK;
+}
+
 cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_bank_t* out) {
   if (!out) return CTS_ERR_INVALID_ARGUMENT;
   *out = nullptr;
@@ -794,6 +721,8 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
     return CTS_ERR_INVALID_ARGUMENT;
   if (d->n_modules < 1 || d->n_adapters < 1 || d->n_clusters < 1 || d->rank < 1) return CTS_ERR_SHAPE;
   if (d->rank > 64 || d->n_clusters > 1024) return CTS_ERR_UNSUPPORTED;
+  if (d->sigma_kind != CTS_SIGMA_FULL && d->sigma_kind != CTS_SIGMA_DIAG) return CTS_ERR_INVALID_ARGUMENT;
+  const bool diag = d->sigma_kind == CTS_SIGMA_DIAG;
   int dev = 0, major = 0;
   CTS_CUDA(cudaGetDevice(&dev));
   CTS_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
@@ -827,20 +756,21 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
   std::vector<size_t> off_in(M), off_out(M), off_sig(M);
   size_t total = 0, stage = 0;
   for (int m = 0; m < M; ++m) {
-    const size_t n_in = size_t(C) * rp * d->d_in[m], n_out = size_t(C) * d->d_out[m] * rp, n_sig = size_t(N) * rp * rp;
+    const size_t n_in = size_t(C) * rp * d->d_in[m], n_out = size_t(C) * d->d_out[m] * rp, n_sig = size_t(N) * rp * (diag ? 1 : rp);
     off_in[m] = total;  total = align_up(total + n_in * 2, 1024);
     off_out[m] = total; total = align_up(total + n_out * 2, 1024);
     off_sig[m] = total; total = align_up(total + n_sig * 2, 1024);
-    stage = std::max(stage, std::max(size_t(C) * d->d_in[m] * r, std::max(size_t(C) * d->d_out[m] * r, size_t(N) * r * r)) * 2);
+    stage = std::max(stage, std::max(size_t(C) * d->d_in[m] * r, std::max(size_t(C) * d->d_out[m] * r, size_t(N) * r * (diag ? 1 : r))) * 2);
   }
   const size_t off_maps = total;
   total = align_up(total + uniq.size() * N * sizeof(int32_t), 1024);
   const size_t off_tm = total;
-  total = align_up(total + 4 * size_t(M) * sizeof(CUtensorMap), 1024);
+  total = align_up(total + 2 * size_t(M) * sizeof(CUtensorMap), 1024);
 
   auto* b = new (std::nothrow) cts_bank_s();
   if (!b) return CTS_ERR_OUT_OF_MEMORY;
   b->n_modules = M; b->N = N; b->C = C; b->r = r; b->rp = rp;
+  b->sigma_diag = diag ? 1 : 0;
   b->n_maps = int(uniq.size());
   b->bytes = total;
   if (cudaMalloc(&b->arena, total) != cudaSuccess) { (void)cudaGetLastError(); delete b; return CTS_ERR_OUT_OF_MEMORY; }
@@ -853,11 +783,9 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
   b->maps = reinterpret_cast<int32_t*>(base + off_maps);
   b->d_tm_in = reinterpret_cast<CUtensorMap*>(base + off_tm);
   b->d_tm_out = b->d_tm_in + M;
-  b->d_tm_in3 = b->d_tm_in + 2 * M;
-  b->d_tm_out256 = b->d_tm_in + 3 * M;
   for (size_t u = 0; u < uniq.size(); ++u)
     if (cudaMemcpyAsync(b->maps + u * N, uniq[u].data(), N * 4, cudaMemcpyHostToDevice, stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
-  std::vector<CUtensorMap> h_tm(4 * size_t(M));
+  std::vector<CUtensorMap> h_tm(2 * size_t(M));
   b->mods.resize(M);
   for (int m = 0; m < M; ++m) {
     Module& mod = b->mods[m];
@@ -866,7 +794,7 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
     mod.out = reinterpret_cast<__nv_bfloat16*>(base + off_out[m]);
     mod.sigma = reinterpret_cast<__nv_bfloat16*>(base + off_sig[m]);
     const void* srcs[3] = {d->in_basis[m], d->out_basis[m], d->sigma[m]};
-    const size_t nbytes[3] = {size_t(C) * mod.d_in * r * 2, size_t(C) * mod.d_out * r * 2, size_t(N) * r * r * 2};
+    const size_t nbytes[3] = {size_t(C) * mod.d_in * r * 2, size_t(C) * mod.d_out * r * 2, size_t(N) * r * (diag ? 1 : r) * 2};
     for (int k = 0; k < 3; ++k) {
       const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(srcs[k]);
       if (!d->sources_on_device) {
@@ -875,24 +803,16 @@ cts_status_t cts_bank_load(const cts_bank_desc_t* d, cudaStream_t stream, cts_ba
       }
       if (k == 0) relayout_in_kernel<<<1184, 256, 0, stream>>>(src, mod.in_t, C, mod.d_in, r, rp);
       if (k == 1) relayout_pad_kernel<<<1184, 256, 0, stream>>>(src, mod.out, size_t(C) * mod.d_out, r, rp);
-      if (k == 2) relayout_sigma_kernel<<<1184, 256, 0, stream>>>(src, mod.sigma, N, r, rp);
+      if (k == 2 && diag) relayout_pad_kernel<<<1184, 256, 0, stream>>>(src, mod.sigma, size_t(N), r, rp);
+      if (k == 2 && !diag) relayout_sigma_kernel<<<1184, 256, 0, stream>>>(src, mod.sigma, N, r, rp);
       if (cudaGetLastError() != cudaSuccess) return fail(CTS_ERR_CUDA);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       if (!d->sources_on_device && cudaStreamSynchronize(stream) != cudaSuccess) return fail(CTS_ERR_CUDA);
     }
     if (!make_tmap(&h_tm[m], mod.in_t, mod.d_in, uint64_t(C) * rp, uint64_t(mod.d_in) * 2, 64, rp,
                    CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap(&h_tm[M + m], mod.out, rp, uint64_t(C) * mod.d_out, uint64_t(rp) * 2, rp, 64, swizzle_for(rp * 2)) ||
-        !make_tmap(&h_tm[3 * M + m], mod.out, rp, uint64_t(C) * mod.d_out, uint64_t(rp) * 2, rp, kLocBN,
-                   swizzle_for(rp * 2)))
+        !make_tmap(&h_tm[M + m], mod.out, rp, uint64_t(C) * mod.d_out, uint64_t(rp) * 2, rp, 64, swizzle_for(rp * 2)))
       return fail(CTS_ERR_CUDA);
-    {   // the same in_basis viewed as {64 columns, C*rp rows, d_in/64 K blocks}: one box = kLocKB slabs
-      const uint64_t dims[3] = {64, uint64_t(C) * rp, uint64_t(mod.d_in / 64)};
-      const uint64_t strides[2] = {uint64_t(mod.d_in) * 2, 128};
-      const uint32_t box[3] = {64, uint32_t(rp), uint32_t(kLocKB)};
-      if (!make_tmap3(&h_tm[2 * M + m], mod.in_t, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
-        return fail(CTS_ERR_CUDA);
-    }
   }
   if (cudaMemcpyAsync(b->d_tm_in, h_tm.data(), h_tm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, stream) != cudaSuccess)
     return fail(CTS_ERR_CUDA);
@@ -912,7 +832,8 @@ cts_status_t cts_bank_params(cts_bank_t b, int32_t module, int64_t* params) {
   if (!b || !params) return CTS_ERR_INVALID_ARGUMENT;
   if (module < 0 || module >= b->n_modules) return CTS_ERR_SHAPE;
   const Module& m = b->mods[module];
-  *params = int64_t(b->C) * (m.d_in + m.d_out) * b->r + int64_t(b->N) * (int64_t(b->r) * b->r + (b->C > 1 ? 1 : 0));
+  const int64_t sig = b->sigma_diag ? int64_t(b->r) : int64_t(b->r) * b->r;   // JD-Diag: r numbers (Eq. 3)
+  *params = int64_t(b->C) * (m.d_in + m.d_out) * b->r + int64_t(b->N) * (sig + (b->C > 1 ? 1 : 0));
   return CTS_OK;
 }
 
@@ -950,7 +871,6 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   const size_t o_nt = off; off = align_up(off + nm * 4, 256);
   const size_t o_trows = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
   const size_t o_tads = off; off = align_up(off + nm * p->max_tiles * kTileM * 4, 256);
-  const size_t o_sad = off; off = align_up(off + nm * T_max * 4, 256);
   const size_t o_err = off; off = align_up(off + 16, 256);
   const size_t o_unb = off; off = align_up(off + (size_t(T_max) + kTileM + 4) * 4, 256);
   const size_t o_cnt = off; off = align_up(off + size_t(kMaxGroup) * p->max_tiles * 4, 1024);
@@ -968,7 +888,6 @@ cts_status_t cts_plan_create(cts_bank_t b, int32_t T_max, cts_plan_t* out) {
   p->n_tiles = reinterpret_cast<int32_t*>(base + o_nt);
   p->tile_rows = reinterpret_cast<int32_t*>(base + o_trows);
   p->tile_adapters = reinterpret_cast<int32_t*>(base + o_tads);
-  p->sadapter = reinterpret_cast<int32_t*>(base + o_sad);
   p->err = reinterpret_cast<int32_t*>(base + o_err);
   p->n_unbound = reinterpret_cast<int32_t*>(base + o_unb);
   p->unbound_rows = p->n_unbound + 4;
@@ -1021,7 +940,6 @@ cts_status_t cts_segment(cts_plan_t p, const int32_t* token_adapter, int32_t T, 
   a.n_tiles = p->n_tiles;
   a.tile_rows = p->tile_rows;
   a.tile_adapters = p->tile_adapters;
-  a.sadapter = p->sadapter;
   a.err = p->err;
   a.unbound_rows = p->unbound_rows;
   a.n_unbound = p->n_unbound;

@@ -21,13 +21,8 @@
 //               a time, add y_base from smem, round to bf16 (RNE), then (STORE mode)
 //                 kStoreScatter:   write back into the stage; the warp TMA-scatters its 8 four-row
 //                                  groups and releases the stage once the scatter has read it;
-//                 kStoreDirect:    store the row's 16-byte chunks straight from registers (one
-//                                  16-byte piece of 32 different rows per warp store) and release
-//                                  the stage right after the y_base reads;
-//                 kStoreCoalesced: write back into the stage, then the warp copies its rows out
-//                                  with row-contiguous stores (8 lanes per 128-byte line, 4 lines
-//                                  per instruction, 8x fewer L1 store wavefronts than direct) and
-//                                  releases the stage as soon as those shared-memory reads are done.
+//                 kStoreDirect:    store the row's 32-byte pieces straight from registers and
+//                                  release the stage right after the y_base reads.
 #pragma once
 #include "sm100.cuh"
 #include "segment.cuh"
@@ -41,18 +36,9 @@ constexpr int kExpandThreads = kApplyThreads;
 #endif
 constexpr int kBN = CTS_EXPAND_BN;       // d_out columns per work item
 constexpr int kExpandAccSlots = 512 / (2 * kBN);   // (D0 | D1) x kBN fp32 columns each: all of TMEM
-constexpr int kStoreScatter = 0, kStoreDirect = 1, kStoreCoalesced = 2;   // expand epilogue store paths
+constexpr int kStoreScatter = 0, kStoreDirect = 1;   // expand epilogue store paths
 #ifndef CTS_Y_STORE_HINT
 #define CTS_Y_STORE_HINT ""       // e.g. ".cs" (evict-first) -- tuning aid
-#endif
-#ifndef CTS_DYN_TAIL
-#define CTS_DYN_TAIL 0            // fused kernel, many items per CTA: claim the last items at run time (measured: no gain)
-#endif
-#ifndef CTS_DYN_MIN_ROUNDS
-#define CTS_DYN_MIN_ROUNDS 48     // ... only when a launch has at least this many expand items per CTA
-#endif
-#ifndef CTS_DYN_STATIC_PCT
-#define CTS_DYN_STATIC_PCT 90     // share of the items dealt statically (whole rounds)
 #endif
 #ifndef CTS_WEIGHTED_DEAL
 #define CTS_WEIGHTED_DEAL 1       // fused: CTAs with an extra shrink item get fewer expand items
@@ -96,7 +82,6 @@ struct ExpandParams {
   int poll_first;                        // fused: 1 = wait for t before issuing the item's loads
   int early_items;                       // fused, poll_first = 0: only this CTA's first early_items items
                                          // issue their y / out_basis loads before their t is ready
-  int* dyn_next;                         // fused: dynamic-tail claim counter (self-resetting), else null
 };
 
 template <int RP>
@@ -152,18 +137,6 @@ __device__ __forceinline__ void expand_init_barriers(const ExpandRing& R) {   //
 
 __device__ __forceinline__ ItemMap expand_map(const ExpandParams& p, int nt_lane, int lane) {
   return make_item_map(p.n_mod, nt_lane, lane < p.n_mod ? p.mod[lane].nblk : 0, lane);
-}
-
-// Dynamic tail.  Items [0, S) are dealt round-robin (S whole rounds of the grid); items [S, total)
-// are claimed at run time from a launch-wide counter by producer warp 0, in ring order, so CTAs
-// that started their expand late (longer shrink share) take fewer of them.  After the last item a
-// sentinel stage (module -1) tells the MMA warp and the epilogue to stop.  Only with the split
-// epilogue (both sets see every stage) and many items per CTA (prefill).
-__device__ __forceinline__ int expand_static_items(const ExpandParams& p, const ItemMap& M) {
-  if (!CTS_DYN_TAIL || !kEpiSplit || p.dyn_next == nullptr ||
-      M.total < CTS_DYN_MIN_ROUNDS * static_cast<int>(gridDim.x))
-    return M.total;
-  return (M.total / 100 * CTS_DYN_STATIC_PCT / static_cast<int>(gridDim.x)) * static_cast<int>(gridDim.x);
 }
 
 // Weighted static deal (fused kernel).  When the shrink has more items than CTAs, CTAs
@@ -231,11 +204,10 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
                                 int deal_r0 = 0, int deal_k = 0) {   // fused: weighted deal
   using L = ExpandCfg<RP>;
   const ItemMap M = expand_map(p, nt_lane, lane);
-  const int S = expand_static_items(p, M);
-  const ExpandDeal D = expand_deal(S, deal_r0, deal_k);
-  int li = 0;                                     // index over this CTA's items
+  const ExpandDeal D = expand_deal(M.total, deal_r0, deal_k);
   if (D.nB == 0) {                                // plain round-robin (decode: always)
-    for (int item = blockIdx.x; item < S; item += gridDim.x) {
+    int li = 0;                                   // index over this CTA's items
+    for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
       const int my = li++;
       if (my % kProducerWarps != warp) continue;
       expand_produce<RP>(p, R, M, item, my, lane, ready_target);
@@ -244,28 +216,6 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
     const int n_static = expand_deal_count(D), n_a = expand_deal_count_a(D);
     for (int j = warp; j < n_static; j += kProducerWarps)   // local item j -> producer warp j % 4
       expand_produce<RP>(p, R, M, expand_deal_item(D, j, n_a), j, lane, ready_target);
-    li = n_static;
-  }
-  if (S < M.total && warp == 0) {                 // dynamic tail, claimed in ring order
-    for (;;) {
-      const int my = li++;
-      const int stage = my % L::kStages;
-      const uint32_t phase = (my / L::kStages) & 1;
-      int item = 0;
-      if (lane == 0) item = S + atomicAdd(p.dyn_next, 1);
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item >= M.total) {                      // sentinel stage: consumers stop here
-        mbar_wait(&R.empty[stage], phase ^ 1);
-        if (lane == 0) {
-          stage_info<RP>(R, stage)[0] = make_int4(-1, 0, 0, 0);
-          stage_info<RP>(R, stage)[1] = make_int4(0, 0, 0, 0);
-          mbar_arrive(&R.full[stage]);
-        }
-        __syncwarp();
-        break;
-      }
-      expand_produce<RP>(p, R, M, item, my, lane, ready_target);
-    }
   }
 }
 
@@ -354,19 +304,13 @@ __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_la
   // unshared slot the second block is stale and D1 is never read.
   constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * kBN);
   const ItemMap M = expand_map(p, nt_lane, lane);
-  const int S = expand_static_items(p, M);
-  const int n_static = expand_deal_count(expand_deal(S, deal_r0, deal_k));
+  const int n_items = expand_deal_count(expand_deal(M.total, deal_r0, deal_k));
   int stage = 0, slot = 0;
   uint32_t phase = 0, aphase = 0;
-  for (int li = 0; S < M.total || li < n_static; ++li) {
+  for (int li = 0; li < n_items; ++li) {
     mbar_wait(&R.acc_empty[slot], aphase ^ 1);
     mbar_wait(&R.full[stage], phase);
     tc_fence_after();
-    if (li >= n_static && stage_info<RP>(R, stage)[0].x < 0) {   // dynamic tail: sentinel
-      if (lane == 0) mbar_arrive(&R.acc_full[slot]);
-      __syncwarp();
-      break;
-    }
     if (lane == 0) {
       const uint32_t acc = R.tmem + slot * L::kSlotCols;
       const uint32_t hi = smem_u32(stage_a<RP>(R, stage)), lo = hi + L::kA, b = smem_u32(stage_b<RP>(R, stage));
@@ -394,9 +338,8 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
   const int set = ew >> 2;
   const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
   const int row = quarter * 32 + lane;
-  const int S = expand_static_items(p, M);
-  const int n_static = expand_deal_count(expand_deal(S, deal_r0, deal_k));
-  for (int my = 0; S < M.total || my < n_static; ++my) {
+  const int n_items = expand_deal_count(expand_deal(M.total, deal_r0, deal_k));
+  for (int my = 0; my < n_items; ++my) {
     if (!kEpiSplit && my % kEpiSets != set) continue;
     static_assert(!kEpiSplit || kEpiSets == kBN / 64, "split epilogue: one 64-column segment per set");
     const int seg0 = kEpiSplit ? set : 0, seg1 = kEpiSplit ? set + 1 : kBN / 64;   // this warp's segments
@@ -407,7 +350,6 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
     tc_fence_after();
     const int4 info = stage_info<RP>(R, stage)[0];    // (g, cluster0, nb, len0)
     const int4 info1 = stage_info<RP>(R, stage)[1];   // (cluster1, len1, -, -)
-    if (my >= n_static && info.x < 0) break;          // dynamic tail: sentinel
     const int sub = (info1.y > 0 && quarter >= 2) ? 1 : 0;   // which half's tile these rows hold
     const int sbase = sub * (kTileM / 2);                    // first slot row of that tile
     const int slen = sub ? info1.y : info.w;
@@ -467,24 +409,6 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&R.acc_empty[slot]);
-    if (STORE == kStoreCoalesced && active) {
-      // lane -> (row, 64-column segment, 16-byte chunk): 8 lanes cover one 128-byte line, the two
-      // segments of a row are adjacent in y, so one instruction writes 2 rows x 256 contiguous bytes
-      const ExpandMod& mo = p.mod[info.x];
-      const int* rows = stage_rows<RP>(R, stage);
-      constexpr int nseg = kEpiSplit ? 1 : L::kSeg;
-#pragma unroll 4
-      for (int it = 0; it < nseg * 8; ++it) {
-        const int idx = it * 32 + lane;
-        const int rr = quarter * 32 + idx / (8 * nseg);
-        const int seg = seg0 + (idx >> 3) % nseg, ch = idx & 7;
-        const int col = info.z * kBN + seg * 64 + ch * 8;
-        if (rr - sbase < slen && col < mo.d_out) {
-          const uint4 w = *reinterpret_cast<const uint4*>(ys + seg * L::kY + rr * 128 + ((ch ^ (rr & 7)) << 4));
-          *reinterpret_cast<uint4*>(mo.y + static_cast<size_t>(rows[rr]) * mo.ld_y + col) = w;
-        }
-      }
-    }
     if (STORE == kStoreScatter && active) {
       // this warp's 8 four-row groups: lane -> (group, segment); TMA scatter of the rows
       fence_proxy_async_smem();

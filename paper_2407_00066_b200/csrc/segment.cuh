@@ -40,7 +40,6 @@ struct SegArgs {
   int32_t* n_tiles;              // [n_maps] number of slots
   int32_t* tile_rows;            // [n_maps][max_tiles*128] token of each tile row (dup of last past len)
   int32_t* tile_adapters;        // [n_maps][max_tiles*128] adapter of that token
-  int32_t* sadapter;             // [n_maps][T_max] adapter of each sorted position (apply_local)
   int32_t* err;                  // [2] code, first bad token
   int32_t* unbound_rows;         // [T_max + 128] tokens with id -1 in order, padded to a multiple of 128
   int32_t* n_unbound;            // [1] (0 if the batch is invalid)
@@ -227,7 +226,6 @@ __global__ void __launch_bounds__(kSegThreads, 1) segment_kernel(SegArgs a) {
     if (key >= 0) {
       const int rank = __popc(peers & ((1u << lane) - 1u));
       perm[my_hist[key] + rank] = t;
-      a.sadapter[static_cast<size_t>(map_id) * a.T_max + my_hist[key] + rank] = a.token_adapter[t];
     }
     __syncwarp();
     if (key >= 0 && lane == 31 - __clz(peers)) my_hist[key] += __popc(peers);

@@ -73,7 +73,7 @@ struct alignas(64) ShrinkMod {
   const int32_t* n_tiles;               // real slot count of this module's map
   const int32_t* tile_rows;             // [slot*128 + row] token index
   const int32_t* tile_adapters;         // [slot*128 + row] adapter id
-  const __nv_bfloat16* sigma;           // [N][rp][rp], row = out index
+  const __nv_bfloat16* sigma;           // [N][rp][rp], row = out index; sigma_diag: [N][rp]
   __nv_bfloat16* tbuf;                  // [max_tiles*128][2*rp]  (hi | lo)
   float* tpart;                         // TP partial mode: fp32 t in TOKEN order [T][rp] instead of tbuf
   float* ws;                            // [(slot*ks + kc)*128 + row][rp] split-K partials
@@ -90,6 +90,7 @@ struct ShrinkParams {
   int ks_max;                           // K chunks per slot: cap (>= 4 K blocks each, workspace fit)
   int target_items;                     // wanted items per SM (K chunks sized on the device)
   int meta_ready;                       // 1: segment outputs are complete before griddep_wait
+  int sigma_diag;                       // bank of kind CTS_SIGMA_DIAG (JD-Diag): t = scale * sigma_i .* s
 };
 
 template <int RP>
@@ -174,7 +175,7 @@ struct ShrinkWork {
 // kernel (CTS_FUSED=0, TP partials) keeps the wait-free last-arriver finisher.
 template <int RP>
 __device__ __forceinline__ bool shrink_dist_finish(const ShrinkParams& p, const ShrinkWork& W) {
-  return CTS_DIST_FINISH && RP >= CTS_DIST_MIN_RP && p.mod[0].ready != nullptr && W.ks > 1 &&
+  return CTS_DIST_FINISH && RP >= CTS_DIST_MIN_RP && !p.sigma_diag && p.mod[0].ready != nullptr && W.ks > 1 &&
          W.M.total <= static_cast<int>(gridDim.x);
 }
 
@@ -467,8 +468,35 @@ __device__ __forceinline__ void dist_finish(const ShrinkMod& m, int tile, int kc
   }
 }
 
-// ------------------------------------------------------------------ epilogue (warps 5-12)
+// Eight finished entries t[o0 .. o0+8) of a row (fp32, scale applied) out: TP partial mode -> fp32
+// in token order; else the bf16 hi + lo pair the expand MMA consumes (t ~= hi + lo to ~2^-16).
 template <int RP>
+__device__ __forceinline__ void store_t8(const ShrinkMod& m, int tile, int row, int o0, const float* t8) {
+  if (m.tpart != nullptr) {
+    float4* dp = reinterpret_cast<float4*>(m.tpart + static_cast<size_t>(m.tile_rows[tile * kTileM + row]) * RP + o0);
+    dp[0] = make_float4(t8[0], t8[1], t8[2], t8[3]);
+    dp[1] = make_float4(t8[4], t8[5], t8[6], t8[7]);
+    return;
+  }
+  __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP) + o0;
+  uint4 hi, lo;
+  __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&hi);
+  __nv_bfloat162* ll = reinterpret_cast<__nv_bfloat162*>(&lo);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const __nv_bfloat162 h2 = __floats2bfloat162_rn(t8[2 * e], t8[2 * e + 1]);
+    const float2 hf = __bfloat1622float2(h2);
+    hh[e] = h2;
+    ll[e] = __floats2bfloat162_rn(t8[2 * e] - hf.x, t8[2 * e + 1] - hf.y);
+  }
+  *reinterpret_cast<uint4*>(dst) = hi;
+  *reinterpret_cast<uint4*>(dst + RP) = lo;
+}
+
+// ------------------------------------------------------------------ epilogue (warps 5-12)
+// DIAG: the bank is of kind CTS_SIGMA_DIAG (a separate instantiation, so the diagonal path adds no
+// register pressure to the full-Sigma path).
+template <int RP, bool DIAG>
 __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, const ShrinkWork& W, int warp, int lane) {
   using L = ShrinkCfg<RP>;
   const int ks = W.ks;
@@ -479,6 +507,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
   const int row = quarter * 32 + lane;
   const int set_tid = (ew & 3) * 32 + lane;      // 0..127 within the set
   const bool dist = shrink_dist_finish<RP>(p, W);   // launch-uniform
+  constexpr bool diag = DIAG;
   const int rpc = (kTileM + ks - 1) / ks;        // dist: rows finished per CTA of a slot
   int li = 0;                                    // index over this CTA's items
   for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
@@ -498,7 +527,9 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
     const bool rvalid = row - sub * (kTileM / 2) < slen4;
     const int adapter = rvalid ? m.tile_adapters[tile * kTileM + row] : 0;
     const uint32_t tsig = R.tmem + (static_cast<uint32_t>(quarter * 32) << 16) + L::kSigmaCol0 + set * L::kSigmaCols;
-    if (L::kSigmaTmem && !dist) {
+    if (diag) {                                    // warm L2 with this row's sigma_i (RP bf16)
+      if (rvalid) prefetch_l2(m.sigma + static_cast<size_t>(adapter) * RP);
+    } else if (L::kSigmaTmem && !dist) {
       // this row's Sigma_i -> TMEM lane `row`, 64 columns (8 rows of Sigma_i) per global round trip
       const uint4* sg = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
 #pragma unroll 1
@@ -604,7 +635,24 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
         if (set_tid == 0) CTS_STAMP(13);                // partials summed
       }
     }
-    if (L::kSigmaTmem && finisher) {
+    if (diag && finisher && rvalid) {
+      // JD-Diag (Eq. 3): t = scale * sigma_i .* s -- no r x r matvec (App D)
+      const uint4* sg = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP);
+#pragma unroll
+      for (int v = 0; v < RP / 8; ++v) {
+        const uint4 q = __ldg(sg + v);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+        float t8[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+          t8[2 * e] = f.x * s[8 * v + 2 * e] * m.scale;
+          t8[2 * e + 1] = f.y * s[8 * v + 2 * e + 1] * m.scale;
+        }
+        store_t8<RP>(m, tile, row, 8 * v, t8);
+      }
+    }
+    if (L::kSigmaTmem && !diag && finisher) {
       // t = scale * Sigma_i s from the TMEM-staged Sigma_i (warp-collective loads: whole warps)
       float t[RP];
 #pragma unroll 1
@@ -654,7 +702,7 @@ __device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
         }
       }
     }
-    if (!L::kSigmaTmem && finisher && rvalid) {
+    if (!L::kSigmaTmem && !diag && finisher && rvalid) {
       // t = scale * Sigma_i s ; thread = token row
       const uint4* srow = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP * RP);
       const int tok = m.tpart != nullptr ? m.tile_rows[tile * kTileM + row] : 0;
@@ -729,7 +777,7 @@ struct ShrinkKernelSmem {
   static constexpr int kBytes = kOffMisc + 64 + 1024;
 };
 
-template <int RP>
+template <int RP, bool DIAG>
 __global__ void __launch_bounds__(kApplyThreads, 1) shrink_sigma_kernel(const __grid_constant__ ShrinkParams p) {
   using S = ShrinkKernelSmem<RP>;
   extern __shared__ uint8_t smem_raw[];
@@ -769,7 +817,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) shrink_sigma_kernel(const __
 
   if (warp < kProducerWarps) shrink_producer<RP>(p, R, W, warp, lane, first);
   else if (warp == kMmaWarp) shrink_mma<RP>(p, R, W, lane);
-  else shrink_epilogue<RP>(p, R, W, warp, lane);
+  else shrink_epilogue<RP, DIAG>(p, R, W, warp, lane);
 
   __syncthreads();
   if (warp == kMmaWarp) tmem_dealloc<ShrinkCfg<RP>::kTmemCols>(R.tmem);

@@ -62,6 +62,8 @@ def test_host_validation_before_cuda(lib):
     assert L.cts_bank_load(ctypes.byref(d), None, ctypes.byref(out)) == 4  # r > 64
     d.rank, d.n_clusters = 4, 1025
     assert L.cts_bank_load(ctypes.byref(d), None, ctypes.byref(out)) == 4  # C > 1024
+    d.n_clusters, d.sigma_kind = 1, 7
+    assert L.cts_bank_load(ctypes.byref(d), None, ctypes.byref(out)) == 1  # unknown sigma_kind
     assert out.value is None
     assert L.cts_plan_create(None, 16, ctypes.byref(out)) == 1
     assert L.cts_segment(None, None, 4, None) == 1
@@ -92,3 +94,12 @@ def test_comm_validation_before_nccl(lib):
     assert L.cts_comm_unique_id(None) == 1
     assert L.cts_apply_tp(None, 1, None, None, None, None, None, 1.0, None, None) == 1
     assert L.cts_status_string(7) == b"NCCL unavailable or failed"
+
+
+def test_exclusive_device_flag(lib):
+    """cts_set_exclusive_device takes 0 / 1 only; it never touches the GPU."""
+    L = lib.lib()
+    assert L.cts_set_exclusive_device(2) == 1
+    assert L.cts_set_exclusive_device(-1) == 1
+    assert L.cts_set_exclusive_device(1) == 0
+    assert L.cts_set_exclusive_device(0) == 0

@@ -452,6 +452,61 @@ def test_diagonal_sigma_jd_diag(cts):
     bank.close()
 
 
+@pytest.mark.parametrize("r,T,prefill", [(16, 1024, False), (4, 300, False), (16, 3000, True), (24, 257, False),
+                                         (64, 256, False), (32, 700, True)])
+def test_diag_bank_kind(cts, r, T, prefill):
+    """CTS_SIGMA_DIAG banks (JD-Diag, Eq. 3): Sigma_i stored as its r diagonal entries and
+    applied as an r-vector scale (App D).  Every row of a grouped launch vs the fp64 oracle on
+    diag(sigma_i); the same diagonals loaded as a FULL bank give bit-identical y (the full matvec only
+    adds exact zeros); the split path, the TP partial path and App F's parameter count (r, not r^2)."""
+    shapes = [(1024, 512), (1024, 256)]
+    N, C = 300, 12
+    banks, f64s, diags = [], [], []
+    for m, (di, do) in enumerate(shapes):
+        bits, f64 = quantized_bank(di, do, N, C, r, seed=1300 + m, cluster_of=cluster_map(N, C, 1310 + m))
+        dg = bf16_round(np.stack([np.diag(bf16_to_f64(s_)) for s_ in bits["sigma"]]))      # [N][r]
+        full = bf16_round(np.stack([np.diag(d_) for d_ in bf16_to_f64(dg)]))                  # [N][r][r]
+        bits["sigma"] = full
+        f64["sigma"] = bf16_to_f64(full)
+        banks.append(bits)
+        f64s.append(f64)
+        diags.append(dg)
+    bank_full = make_bank(cts, banks)
+    bank_diag = cts.Bank([dev_bf16(b["in_basis"]) for b in banks], [dev_bf16(b["out_basis"]) for b in banks],
+                         [dev_bf16(d_) for d_ in diags], [torch.from_numpy(b["cluster_of"]).cuda() for b in banks])
+    assert bank_diag.sigma_diag and not bank_full.sigma_diag
+    for m, (di, do) in enumerate(shapes):
+        assert bank_diag.params(m) == C * (di + do) * r + N * (r + 1)
+        assert bank_full.params(m) == C * (di + do) * r + N * (r * r + 1)
+    assert bank_diag.bytes < bank_full.bytes
+    ta = prefill_tokens(T, N, 1321) if prefill else decode_tokens(T, N, 1321, frac_none=0.05)
+    xb = bf16_round(activations(T, 1024, 1322))
+    x = dev_bf16(xb)
+    outs = {}
+    for name, bank in (("diag", bank_diag), ("full", bank_full)):
+        plan = cts.Plan(bank, T)
+        plan.segment(torch.from_numpy(ta).cuda())
+        ys = [torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes]
+        plan.apply_group([0, 1], [x, x], ys, 1.5)
+        ys2 = [torch.zeros_like(y) for y in ys]
+        plan.shrink_group([0, 1], [x, x], 1.5)
+        plan.expand_group([0, 1], ys2)
+        parts = plan.new_partials(2)
+        ys3 = [torch.zeros_like(y) for y in ys]
+        plan.shrink_partial_group([0, 1], [x, x], parts, 1.5)
+        plan.expand_reduced_group([0, 1], parts, ys3)
+        torch.cuda.synchronize()
+        outs[name] = [[host_bits(y) for y in v] for v in (ys, ys2, ys3)]
+        plan.close()
+    for m in range(2):
+        check_delta(ta, outs["diag"][0][m], f64s[m], xb, 1.5)
+        for v in range(3):
+            assert np.array_equal(outs["diag"][v][m], outs["full"][v][m]), (m, v)
+        assert np.array_equal(outs["diag"][1][m], outs["diag"][0][m])
+    bank_full.close()
+    bank_diag.close()
+
+
 # ---------------------------------------------------------------- fused base + LoRA projection
 @pytest.mark.parametrize("w_zero", [False, True])
 @pytest.mark.parametrize("d_in,d_out,T,prefill,frac_none", [(512, 512, 300, False, 0.1), (256, 768, 700, True, 0.0),
@@ -785,10 +840,10 @@ def test_gpu_jd_rank_deficient_cluster(cts, case):
     ([(768, 512), (768, 512)], 500, 200, 333, 0.05),                 # many clusters, tiny pieces
     ([(256, 256)], 8, 3, 5, 0.0),                                    # a handful of rows
 ])
-def test_exchange_free_decode_kernel(cts, shapes, N, C, T, frac_none):
-    """apply_local.cuh (the decode-regime kernel: pieces of one cluster's rows, shrink, Sigma and the
-    transposed expand all in one CTA, no inter-CTA exchange): every row of every module of a grouped
-    launch vs the fp64 oracle, unbound rows untouched, residual contract with a random y_base."""
+def test_grouped_decode_shapes(cts, shapes, N, C, T, frac_none):
+    """Grouped fused launches at decode-like shapes (q,k,v-like group, a ragged last column block,
+    many clusters with tiny slots, a handful of rows): every row of every module vs the fp64 oracle,
+    unbound rows untouched, residual contract with a random y_base."""
     banks, f64s = [], []
     for m, (di, do) in enumerate(shapes):
         b, f = quantized_bank(di, do, N, C, 16, seed=500 + m, cluster_of=cluster_map(N, C, 510 + m))
@@ -856,6 +911,33 @@ def test_two_streams_concurrent_applies(cts):
             check_delta(tas[k], host_bits(ys[k][m]), f64s[m], xs[k], 1.0)
     for pl in plans:
         pl.close()
+    bank.close()
+
+
+def test_exclusive_device_same_bits(cts):
+    """cts_set_exclusive_device(1) (non-cooperative fused launches) computes exactly what the default
+    cooperative launch computes: a Mistral-like grouped layer, both modes, bit-identical y."""
+    shapes = [(1024, 1024), (1024, 256), (1024, 256)]
+    N, C, T = 300, 12, 1024
+    banks = [quantized_bank(di, do, N, C, 16, seed=1400 + m, cluster_of=cluster_map(N, C, 1410 + m))[0]
+             for m, (di, do) in enumerate(shapes)]
+    bank = make_bank(cts, banks)
+    plan = cts.Plan(bank, T)
+    plan.segment(torch.from_numpy(decode_tokens(T, N, 1421, frac_none=0.05)).cuda())
+    x = dev_bf16(bf16_round(activations(T, 1024, 1422)))
+    got = []
+    try:
+        for excl in (False, True):
+            cts.cts_set_exclusive_device(excl)
+            ys = [torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes]
+            plan.apply_group([0, 1, 2], [x, x, x], ys, 2.0)
+            torch.cuda.synchronize()
+            got.append([host_bits(y) for y in ys])
+    finally:
+        cts.cts_set_exclusive_device(False)
+    for a, b in zip(*got):
+        assert np.array_equal(a, b)
+    plan.close()
     bank.close()
 
 
