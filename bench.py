@@ -41,6 +41,10 @@ CONFIGS = {
     # processes the same T tokens, one all-reduce of the rank-r partial per module (strong scaling)
     "tp_decode": dict(workload="cfg5_tp_decode", N=8192, C=128, r=16, T=1024, prefill=False, tp=True,
                       layers=MISTRAL_LAYERS, modules=MISTRAL_MODULES, steps=50, warmup=5),
+    # the JD-Diag variant (Eq. 3) served as an r-vector bank (CTS_SIGMA_DIAG),
+    # otherwise configs[2]
+    "diag_decode": dict(workload="cfg3_decode_jd_diag", N=1000, C=25, r=16, T=1024, prefill=False, diag=True,
+                        layers=MISTRAL_LAYERS, modules=MISTRAL_MODULES, steps=300, warmup=10),
     "multi": dict(workload="cfg5_multi_decode", N=8192, C=128, r=16, T=1024, prefill=False,
                   layers=MISTRAL_LAYERS, modules=MISTRAL_MODULES, steps=200, warmup=10),
     # the paper's baseline on the same box -- the same 1000 adapters served
@@ -53,6 +57,12 @@ CONFIGS = {
     # tensor-core bound: reported in TFLOP/s against the measured bf16 peak
     "proj_prefill": dict(workload="cfg4_fused_projection_prefill", N=1000, C=25, r=16, T=16384, prefill=True,
                          proj=True, layers=MISTRAL_LAYERS, modules=MISTRAL_MODULES, steps=5, warmup=3),
+    # serving 1024 LoRAs (10 generated tokens per request) at
+    # MATCHED adapter memory: the compressed bank (25 clusters, r=16) vs an uncompressed pool of 28
+    # slots (App F's max-gpu-lora for this setting) with misses paged in over PCIe
+    "lora_matched": dict(workload="app_f_matched_memory_1024_loras", N=1024, C=25, r=16, T=1024, slots=28,
+                         gen_tokens=10, prefill=False, matched=True, layers=MISTRAL_LAYERS,
+                         modules=MISTRAL_MODULES, steps=3, warmup=3),
     "lora_decode": dict(workload="uncompressed_lora_decode", N=1000, C=1000, r=16, T=1024, prefill=False,
                         uncompressed=True, layers=8, model_layers=MISTRAL_LAYERS, modules=MISTRAL_MODULES,
                         steps=100, warmup=5),
@@ -70,9 +80,70 @@ def x_slot(name):
     return {"q": "attn", "k": "attn", "v": "attn", "o": "o", "gate": "mlp", "up": "mlp", "down": "down"}[name]
 
 
-def algorithmic_bytes(tokens, cluster_maps, mods, r):
+def layer_groups(cfg, mods):
+    """Dependency groups of one decoder layer: q,k,v read one x; gate,up read one x; o and down each
+    wait for the previous sub-layer -- one grouped launch per group (4 per layer)."""
+    groups = []
+    for layer in range(cfg["layers"]):
+        by_slot = {}
+        for m, (l, name, di, do) in enumerate(mods):
+            if l == layer:
+                by_slot.setdefault(x_slot(name), []).append(m)
+        for slot in ("attn", "o", "mlp", "down"):
+            if slot in by_slot:
+                groups.append(by_slot[slot])
+    return groups
+
+
+def schedule_waves(req_adapters, slots):
+    """vLLM multi-LoRA admission at max-gpu-lora = `slots` (App F): requests in
+    arrival order; a wave admits requests while its distinct adapters fit in the slots.  Returns the
+    waves as lists of request indices."""
+    waves, cur, seen = [], [], set()
+    for i, a in enumerate(req_adapters):
+        a = int(a)
+        if a not in seen and len(seen) == slots:
+            waves.append(cur)
+            cur, seen = [], set()
+        cur.append(i)
+        seen.add(a)
+    if cur:
+        waves.append(cur)
+    return waves
+
+
+class SlotPool:
+    """LRU map adapter -> slot of a resident pool of `slots` uncompressed LoRAs."""
+
+    def __init__(self, slots):
+        self.slots = slots
+        self.where = {}                 # adapter -> slot
+        self.last = [-1] * slots        # slot -> last wave that used it
+        self.held = [None] * slots      # slot -> adapter
+
+    def admit(self, adapters, wave):
+        """Slots for the wave's distinct adapters; returns ({adapter: slot}, [(slot, adapter) to page in])."""
+        need = [a for a in dict.fromkeys(int(a) for a in adapters)]
+        assert len(need) <= self.slots
+        keep = {a for a in need if a in self.where}
+        free = sorted((s for s in range(self.slots) if self.held[s] not in keep), key=lambda s: self.last[s])
+        misses = []
+        for a in need:
+            if a not in self.where:
+                s_ = free.pop(0)
+                if self.held[s_] is not None:
+                    del self.where[self.held[s_]]
+                self.held[s_] = a
+                self.where[a] = s_
+                misses.append((s_, a))
+            self.last[self.where[a]] = wave
+        return {a: self.where[a] for a in need}, misses
+
+
+def algorithmic_bytes(tokens, cluster_maps, mods, r, sigma_diag=False):
     """Per-module algorithmic bytes: shrink = x rows + touched in_basis + touched
-    Sigma + ids; expand = y read + write + touched out_basis + perm.  Counted from the batch."""
+    Sigma (r^2, or r for a JD-Diag bank) + ids; expand = y read + write + touched out_basis + perm.
+    Counted from the batch."""
     tokens = np.asarray(tokens)
     bound = tokens >= 0
     Tb = int(bound.sum())
@@ -81,7 +152,7 @@ def algorithmic_bytes(tokens, cluster_maps, mods, r):
     shrink, expand = [], []
     for (_, _, di, do), cmap in zip(mods, cluster_maps):
         ct = len(np.unique(cmap[adapters])) if adapters.size else 0
-        shrink.append(Tb * di * 2 + ct * di * r * 2 + adapters.size * r * r * 2 + 4 * T)
+        shrink.append(Tb * di * 2 + ct * di * r * 2 + adapters.size * r * (1 if sigma_diag else r) * 2 + 4 * T)
         expand.append(2 * Tb * do * 2 + ct * do * r * 2 + 4 * T)
     return np.array(shrink, dtype=np.float64), np.array(expand, dtype=np.float64)
 
@@ -293,6 +364,8 @@ METRIC = "compressed-LoRA apply tokens/s at 1000 adapters"
 def config_dict(cfg, world):
     mods = "+".join(n for (n, _, _) in cfg["modules"])
     extra = {}
+    if cfg.get("diag"):
+        extra = {"bank": "JD-Diag (Eq. 3): Sigma_i diagonal, stored as r numbers (CTS_SIGMA_DIAG)"}
     if cfg.get("uncompressed"):
         extra = {"bank": f"UNCOMPRESSED: {cfg['N']} separate rank-{cfg['r']} LoRAs (cluster = adapter, Sigma = I)",
                  "timed_layers": cfg["layers"],
@@ -552,6 +625,9 @@ def run_gpu(args, cfg):
     else:
         srcs = [direct_bank_torch(di, do, N, C, r, seed=m % len(cfg["modules"]) + 1000 * (m // len(cfg["modules"])),
                                   device=dev, cluster_seed=50 + m) for m, (_, _, di, do) in enumerate(mods)]
+    if cfg.get("diag"):                          # JD-Diag bank: keep the diagonals only (CTS_SIGMA_DIAG)
+        for s_ in srcs:
+            s_["sigma"] = torch.diagonal(s_["sigma"], dim1=1, dim2=2).contiguous()
     bank = cts.Bank([s["in_basis"] for s in srcs], [s["out_basis"] for s in srcs], [s["sigma"] for s in srcs],
                     [s["cluster_of"] for s in srcs])
     cmaps = [s["cluster_of"].cpu().numpy() for s in srcs]
@@ -573,17 +649,7 @@ def run_gpu(args, cfg):
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
 
-    # dependency groups of one decoder layer: q,k,v read one x; gate,up read one x; o and down
-    # each wait for the previous sub-layer -- one grouped launch pair per group (4 per layer)
-    groups = []
-    for layer in range(cfg["layers"]):
-        by_slot = {}
-        for m, (l, name, di, do) in enumerate(mods):
-            if l == layer:
-                by_slot.setdefault(x_slot(name), []).append(m)
-        for slot in ("attn", "o", "mlp", "down"):
-            if slot in by_slot:
-                groups.append(by_slot[slot])
+    groups = layer_groups(cfg, mods)
 
     def step():
         plan.segment(tokens)
@@ -599,7 +665,7 @@ def run_gpu(args, cfg):
             torch.cuda.synchronize()
             # algorithmic bytes of every apply launch of the step, in launch order (for
             # profiles/make_traffic.py, which divides ncu's dram bytes of the same launches by them)
-            bs, be = algorithmic_bytes(tokens.cpu().numpy(), cmaps, mods, r)
+            bs, be = algorithmic_bytes(tokens.cpu().numpy(), cmaps, mods, r, cfg.get("diag", False))
             os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
             with open(os.path.join(ROOT, "gpurun_out", f"{cfg['workload']}_alg_bytes.json"), "w") as f:
                 json.dump({"workload": cfg["workload"], "groups": groups,
@@ -733,7 +799,7 @@ def run_gpu(args, cfg):
 
     NL = len(groups)                     # launches of each kernel per step
     tok_np = tokens.cpu().numpy()
-    b_shrink, b_expand = algorithmic_bytes(tok_np, cmaps, mods, r)
+    b_shrink, b_expand = algorithmic_bytes(tok_np, cmaps, mods, r, cfg.get("diag", False))
     hbm, bf16_peak, peak_src = measured_peaks()
     fused = launches_per_step == 1 + NL
     kern = {"shrink_sigma_kernel": (b_shrink.sum(), ms_shrink), "expand_kernel": (b_expand.sum(), ms_expand)}
@@ -796,6 +862,186 @@ def run_gpu(args, cfg):
     return 0
 
 
+# ----------------------------------------------------------------------------- GPU leg, matched memory (App F)
+def run_matched(args, cfg):
+    """App F / Fig. 1 direction on one B200, LoRA apply only (no base model): R = T requests, adapter
+    uniform over N, L = gen_tokens decode steps each.
+      compressed:   every adapter resident (bank of C clusters); the R requests decode together,
+                    L steps of segment + 224-module apply (one CUDA graph per step).
+      uncompressed: a pool of `slots` resident rank-r LoRAs (cluster = slot, Sigma = I), the App F
+                    matched-memory slot count; requests run in waves of <= slots distinct adapters
+                    (schedule_waves), a wave's missing adapters are paged in (SlotPool, LRU) -- one
+                    H2D copy per module and basis from pinned host memory, then
+                    cts_bank_write_clusters -- and the wave then decodes L steps.
+    Both arms on one stream, CUDA events around the whole run; requests/s and tokens/s of each."""
+    import torch
+
+    import paper_2407_00066_b200 as cts
+    from workloads.gen_torch import direct_bank_torch, lora_bank_torch, tokens_torch
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    cts.cts_set_exclusive_device(True)
+    N, C, r, P, L, R = cfg["N"], cfg["C"], cfg["r"], cfg["slots"], cfg["gen_tokens"], cfg["T"]
+    mods = module_list(cfg)
+    groups = layer_groups(cfg, mods)
+    req = tokens_torch(R, N, 1, False, "cpu")
+    stream = torch.cuda.Stream(device=dev)
+    g = torch.Generator(device=dev).manual_seed(2)
+
+    def activations_for(T):
+        xs, ys, xbuf = [], [], {}
+        for (layer, name, di, do) in mods:
+            key = (layer, x_slot(name))
+            if key not in xbuf:
+                xbuf[key] = torch.randn(T, di, generator=g, device=dev).to(torch.bfloat16)
+            xs.append(xbuf[key])
+            ys.append(torch.randn(T, do, generator=g, device=dev).to(torch.bfloat16))
+        return xs, ys
+
+    def capture(plan, tok, xs, ys):
+        def step():
+            plan.segment(tok)
+            for gm in groups:
+                plan.apply_group(gm, [xs[m] for m in gm], [ys[m] for m in gm], SCALE)
+        with torch.cuda.stream(stream):
+            step()
+            torch.cuda.synchronize()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=stream):
+                step()
+        return gr
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    # --- compressed arm
+    srcs = [direct_bank_torch(di, do, N, C, r, seed=m % len(cfg["modules"]) + 1000 * (m // len(cfg["modules"])),
+                              device=dev, cluster_seed=50 + m) for m, (_, _, di, do) in enumerate(mods)]
+    bank_c = cts.Bank([s_["in_basis"] for s_ in srcs], [s_["out_basis"] for s_ in srcs],
+                      [s_["sigma"] for s_ in srcs], [s_["cluster_of"] for s_ in srcs])
+    del srcs
+    xs, ys = activations_for(R)
+    plan_c = cts.Plan(bank_c, R)
+    tok_c = req.to(dev)
+    gr_c = capture(plan_c, tok_c, xs, ys)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            gr_c.replay()
+    stream.synchronize()
+    runs_c = []
+    with ClockSampler(0) as clocks:
+        for _ in range(args.steps):
+            a, b = ev(), ev()
+            a.record(stream)
+            with torch.cuda.stream(stream):
+                for _ in range(L):
+                    gr_c.replay()
+            b.record(stream)
+            b.synchronize()
+            runs_c.append(a.elapsed_time(b))
+    ms_c = statistics.median(runs_c)
+    bytes_c = bank_c.bytes
+    plan_c.close()
+    bank_c.close()
+    del xs, ys, gr_c
+    torch.cuda.empty_cache()
+
+    # --- uncompressed arm: the matched-memory slot pool
+    pool = [lora_bank_torch(di, do, P, r, seed=m, device=dev) for m, (_, _, di, do) in enumerate(mods)]
+    bank_u = cts.Bank([p_["in_basis"] for p_ in pool], [p_["out_basis"] for p_ in pool],
+                      [p_["sigma"] for p_ in pool], [p_["cluster_of"] for p_ in pool])
+    bytes_u = bank_u.bytes
+    # host LoRA store (pinned): one slice per slot position, re-sent on every page-in (contents repeat,
+    # the bytes moved over PCIe are the real ones); device staging of the same shape
+    host_in = [p_["in_basis"].cpu().pin_memory() for p_ in pool]
+    host_out = [p_["out_basis"].cpu().pin_memory() for p_ in pool]
+    stage_in = [torch.empty_like(p_["in_basis"]) for p_ in pool]
+    stage_out = [torch.empty_like(p_["out_basis"]) for p_ in pool]
+    del pool
+    waves = schedule_waves(req.numpy(), P)
+    Tw = max(len(w) for w in waves)
+    xs, ys = activations_for(Tw)
+    plan_u = cts.Plan(bank_u, Tw)
+    tok_u = torch.full((Tw,), -1, dtype=torch.int32, device=dev)
+    gr_u = capture(plan_u, tok_u, xs, ys)
+    lora_bytes = sum((di + do) * r * 2 for (_, _, di, do) in mods)
+
+    def run_waves():
+        pool_map = SlotPool(P)
+        plan_tok = torch.full((len(waves), Tw), -1, dtype=torch.int32)
+        pages = []
+        for w, idx in enumerate(waves):
+            where, misses = pool_map.admit(req.numpy()[idx], w)
+            plan_tok[w, :len(idx)] = torch.tensor([where[int(a)] for a in req.numpy()[idx]], dtype=torch.int32)
+            pages.append(misses)
+        plan_tok = plan_tok.pin_memory()
+        t_page = t_all = 0.0
+        a, b = ev(), ev()
+        a.record(stream)
+        n_paged = 0
+        with torch.cuda.stream(stream):
+            for w in range(len(waves)):
+                slots_w = [s_ for s_, _ in pages[w]]
+                n = len(slots_w)
+                n_paged += n
+                if n:
+                    for m in range(len(mods)):
+                        stage_in[m][:n].copy_(host_in[m][:n], non_blocking=True)
+                        stage_out[m][:n].copy_(host_out[m][:n], non_blocking=True)
+                        bank_u.write_clusters(m, slots_w, stage_in[m][:n], stage_out[m][:n], stream=stream)
+                tok_u.copy_(plan_tok[w], non_blocking=True)
+                for _ in range(L):
+                    gr_u.replay()
+        b.record(stream)
+        b.synchronize()
+        t_all = a.elapsed_time(b)
+        return t_all, n_paged
+
+    run_waves()                                  # warm-up pass (page-in path, graph)
+    runs_u = []
+    for _ in range(max(1, min(args.steps, 2))):
+        runs_u.append(run_waves())
+    ms_u = statistics.median(t for t, _ in runs_u)
+    n_paged = runs_u[0][1]
+    # compute-only time of the uncompressed arm: the same waves without page-ins
+    a, b = ev(), ev()
+    a.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(len(waves) * L):
+            gr_u.replay()
+    b.record(stream)
+    b.synchronize()
+    ms_u_compute = a.elapsed_time(b)
+    plan_u.close()
+    bank_u.close()
+
+    req_s_c = R / (ms_c / 1e3)
+    req_s_u = R / (ms_u / 1e3)
+    line = {"metric": "requests/s serving 1024 LoRAs at matched adapter memory (App F), LoRA apply only",
+            "value": req_s_c, "unit": "requests/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_c / L, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "tokens_per_s": R * L / (ms_c / 1e3),
+            "compressed": {"bank_bytes": bytes_c, "requests_per_s": req_s_c, "tokens_per_s": R * L / (ms_c / 1e3),
+                           "ms_all_requests": ms_c},
+            "uncompressed_matched": {"slots": P, "bank_bytes": bytes_u, "requests_per_s": req_s_u,
+                                     "tokens_per_s": R * L / (ms_u / 1e3), "ms_all_requests": ms_u,
+                                     "waves": len(waves), "adapters_paged": n_paged,
+                                     "paged_bytes": n_paged * lora_bytes,
+                                     "ms_compute_only": ms_u_compute,
+                                     "h2d_gbs": n_paged * lora_bytes / max(ms_u - ms_u_compute, 1e-3) / 1e6},
+            "ratio_compressed_over_uncompressed": req_s_c / req_s_u,
+            "paper": "1.6x over vLLM multi-LoRA at >1000 LoRAs, full model, H100 at 40% memory (P:L70, P:L359)",
+            "clocks": clocks.result(),
+            "config": {"workload": cfg["workload"], "n_adapters": N, "n_clusters": C, "rank": r,
+                       "requests": R, "generated_tokens_per_request": L, "uncompressed_slots": P,
+                       "modules": len(mods),
+                       "scope": "LoRA apply only (no base model), so the ratio is the adapter-side gap, "
+                                "not Fig. 1's end-to-end 1.6x",
+                       "device_mode": "exclusive (cts_set_exclusive_device)"}}
+    emit(line)
+    return 0
+
+
 _JSON_FD = None
 
 
@@ -832,6 +1078,8 @@ def main():
         return run_tp(args, cfg)
     if cfg.get("proj"):
         return run_proj(args, cfg)
+    if cfg.get("matched"):
+        return run_matched(args, cfg)
     return run_gpu(args, cfg)
 
 

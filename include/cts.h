@@ -20,7 +20,8 @@
  *   - No call throws or aborts; failures return a cts_status_t and enqueue nothing.
  *   - Element types: bf16 = IEEE-like bfloat16 (1-8-7) stored as 16-bit words; int32 little endian.
  *   - All arithmetic on device: bf16 operands, fp32 accumulation, bf16 round-to-nearest-even out.
- *   - Banks are immutable after load; several plans/streams may apply the same bank concurrently.
+ *   - Banks are immutable after load (except through cts_bank_write_clusters); several plans/streams
+ *     may apply the same bank concurrently.
  */
 #ifndef CTS_H_
 #define CTS_H_
@@ -95,6 +96,19 @@ cts_status_t cts_bank_bytes(cts_bank_t bank, size_t* device_bytes);
  * sum over clusters of (d_in + d_out) * r  +  N * (r^2 + (C > 1 ? 1 : 0)).  Unpadded.
  * CTS_SIGMA_DIAG banks count r instead of r^2 per adapter (JD-Diag, Eq. 3). */
 cts_status_t cts_bank_params(cts_bank_t bank, int32_t module, int64_t* params);
+
+/* Overwrite the shared bases of n (<= 64) distinct clusters of module m with new ones -- the
+ * page-in of a resident slot pool (the multi-LoRA baseline the paper compares against swaps adapters
+ * between host and GPU memory; App F matched-memory slots): with an
+ * uncompressed bank (cluster = adapter slot, Sigma = I) this replaces the LoRAs held in those slots.
+ * in_basis: DEVICE bf16 [n][d_in][r] and out_basis: DEVICE bf16 [n][d_out][r] (the cts_bank_desc_t
+ * layouts, cluster q's slice q); the caller stages host data itself (e.g. one cudaMemcpyAsync from
+ * pinned memory).  Stream-ordered and asynchronous: applies enqueued later on `stream` see the new
+ * bases; applies on OTHER streams must not read those clusters concurrently.  Sigma and the
+ * adapter->cluster maps are unchanged.  Errors: CTS_ERR_INVALID_ARGUMENT (null, repeated cluster),
+ * CTS_ERR_SHAPE (module, n outside [0, 64]), CTS_ERR_INDEX_OUT_OF_RANGE (cluster outside [0, C)). */
+cts_status_t cts_bank_write_clusters(cts_bank_t bank, int32_t module, int32_t n, const int32_t* clusters,
+                                     const void* in_basis, const void* out_basis, cudaStream_t stream);
 
 /* Release all device memory of the bank.  The caller must ensure no apply still uses it. */
 cts_status_t cts_bank_free(cts_bank_t bank);

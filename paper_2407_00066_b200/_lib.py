@@ -29,6 +29,7 @@ EXPORTS = (
     "cts_launch_count", "cts_plan_partial_elems", "cts_shrink_partial_group", "cts_expand_reduced_group",
     "cts_project", "cts_jd_workspace_bytes", "cts_jd_eigen_iteration", "cts_route", "cts_rows_move",
     "cts_comm_unique_id", "cts_comm_create", "cts_comm_free", "cts_apply_tp", "cts_set_exclusive_device",
+    "cts_bank_write_clusters",
 )
 
 
@@ -108,6 +109,7 @@ def lib():
         "cts_status_string": ([I32], ctypes.c_char_p),
         "cts_launch_count": ([], ctypes.c_uint64),
         "cts_set_exclusive_device": ([I32], I32),
+        "cts_bank_write_clusters": ([P, I32, I32, VP, VP, VP, P], I32),
         "cts_plan_partial_elems": ([P, ctypes.POINTER(I64)], I32),
         "cts_shrink_partial_group": ([P, I32, VP, VP, VP, F, VP, P], I32),
         "cts_expand_reduced_group": ([P, I32, VP, VP, VP, VP, P], I32),

@@ -311,6 +311,23 @@ def cts_apply_tp(plan, modules, xs, ys, comm, scale=1.0, stream=None):
                                              _stream_handle(stream)))
 
 
+def cts_bank_write_clusters(bank, module, clusters, in_basis, out_basis, stream=None):
+    """Overwrite module `module`'s bases of the listed clusters: in_basis [n][d_in][r], out_basis
+    [n][d_out][r] bf16 CUDA tensors (slot page-in of a resident pool)."""
+    n = len(clusters)
+    if n:
+        _bf16(in_basis, "in_basis")
+        _bf16(out_basis, "out_basis")
+        if not (in_basis.is_cuda and out_basis.is_cuda):
+            raise ValueError("cts_bank_write_clusters takes device sources")
+        if in_basis.shape[0] != n or out_basis.shape[0] != n:
+            raise ValueError("one basis slice per listed cluster")
+    cl = (ctypes.c_int32 * max(n, 1))(*[int(c) for c in clusters])
+    check("cts_bank_write_clusters",
+          lib().cts_bank_write_clusters(bank, module, n, cl, in_basis.data_ptr() if n else None,
+                                        out_basis.data_ptr() if n else None, _stream_handle(stream)))
+
+
 def cts_set_exclusive_device(exclusive):
     """Declare (True) or revoke (False, default) exclusive use of the GPU by libcts launches: fused
     applies then launch non-cooperatively (cts.h: only safe when no other kernel runs concurrently)."""
@@ -341,6 +358,9 @@ class Bank:
 
     def params(self, module):
         return cts_bank_params(self.handle, module)
+
+    def write_clusters(self, module, clusters, in_basis, out_basis, stream=None):
+        cts_bank_write_clusters(self.handle, module, clusters, in_basis, out_basis, stream)
 
     def close(self):
         if self.handle is not None:

@@ -113,6 +113,32 @@ __global__ void relayout_pad_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst
     dst[i] = k < r ? src[(i / rp) * r + k] : __float2bfloat16_rn(0.f);
   }
 }
+// cts_bank_write_clusters: n clusters' bases, sources [n][d][r], into the bank slices of clusters
+// cl.c[q] ([C][rp][d_in] for in_basis, [C][d_out][rp] for out_basis)
+constexpr int kMaxWriteClusters = 64;
+struct ClusterList {
+  int32_t c[kMaxWriteClusters];
+};
+__global__ void write_in_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, ClusterList cl, int n, int d_in, int r,
+                                int rp) {
+  const size_t per = size_t(rp) * d_in;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n * per; i += size_t(gridDim.x) * blockDim.x) {
+    const int q = static_cast<int>(i / per);
+    const int k = static_cast<int>((i % per) / d_in), j = static_cast<int>(i % d_in);
+    dst[size_t(cl.c[q]) * per + size_t(k) * d_in + j] =
+        k < r ? src[(size_t(q) * d_in + j) * r + k] : __float2bfloat16_rn(0.f);
+  }
+}
+__global__ void write_out_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, ClusterList cl, int n, int d_out, int r,
+                                 int rp) {
+  const size_t per = size_t(d_out) * rp;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n * per; i += size_t(gridDim.x) * blockDim.x) {
+    const int q = static_cast<int>(i / per);
+    const int row = static_cast<int>((i % per) / rp), k = static_cast<int>(i % rp);
+    dst[size_t(cl.c[q]) * per + size_t(row) * rp + k] =
+        k < r ? src[(size_t(q) * d_out + row) * r + k] : __float2bfloat16_rn(0.f);
+  }
+}
 // Sigma [N][r][r] -> [N][rp][rp]
 __global__ void relayout_sigma_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, int N, int r, int rp) {
   const size_t n = static_cast<size_t>(N) * rp * rp;
@@ -834,6 +860,28 @@ cts_status_t cts_bank_params(cts_bank_t b, int32_t module, int64_t* params) {
   const Module& m = b->mods[module];
   const int64_t sig = b->sigma_diag ? int64_t(b->r) : int64_t(b->r) * b->r;   // JD-Diag: r numbers (Eq. 3)
   *params = int64_t(b->C) * (m.d_in + m.d_out) * b->r + int64_t(b->N) * (sig + (b->C > 1 ? 1 : 0));
+  return CTS_OK;
+}
+
+cts_status_t cts_bank_write_clusters(cts_bank_t b, int32_t module, int32_t n, const int32_t* clusters,
+                                     const void* in_basis, const void* out_basis, cudaStream_t stream) {
+  if (!b || !clusters || (n > 0 && (!in_basis || !out_basis))) return CTS_ERR_INVALID_ARGUMENT;
+  if (module < 0 || module >= b->n_modules || n < 0 || n > kMaxWriteClusters) return CTS_ERR_SHAPE;
+  ClusterList cl;
+  for (int q = 0; q < n; ++q) {
+    if (clusters[q] < 0 || clusters[q] >= b->C) return CTS_ERR_INDEX_OUT_OF_RANGE;
+    for (int p = 0; p < q; ++p)
+      if (clusters[p] == clusters[q]) return CTS_ERR_INVALID_ARGUMENT;
+    cl.c[q] = clusters[q];
+  }
+  if (n == 0) return CTS_OK;
+  const Module& m = b->mods[module];
+  write_in_kernel<<<1184, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(in_basis), m.in_t, cl, n, m.d_in, b->r,
+                                            b->rp);
+  write_out_kernel<<<1184, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(out_basis), m.out, cl, n, m.d_out,
+                                             b->r, b->rp);
+  CTS_CUDA(cudaGetLastError());
+  g_launches.fetch_add(2, std::memory_order_relaxed);
   return CTS_OK;
 }
 

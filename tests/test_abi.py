@@ -103,3 +103,10 @@ def test_exclusive_device_flag(lib):
     assert L.cts_set_exclusive_device(-1) == 1
     assert L.cts_set_exclusive_device(1) == 0
     assert L.cts_set_exclusive_device(0) == 0
+
+
+def test_bank_write_clusters_validation(lib):
+    """cts_bank_write_clusters rejects a null bank / cluster list before any CUDA call."""
+    L = lib.lib()
+    cl = (ctypes.c_int32 * 1)(0)
+    assert L.cts_bank_write_clusters(None, 0, 1, cl, None, None, None) == 1

@@ -914,6 +914,46 @@ def test_two_streams_concurrent_applies(cts):
     bank.close()
 
 
+def test_bank_write_clusters_slot_pagein(cts):
+    """cts_bank_write_clusters (slot page-in of a resident pool, the matched-memory baseline): load a
+    bank, overwrite the bases of clusters {5, 1, 6} of module 1 with new ones on a side stream, then
+    apply: every row vs the oracle on the UPDATED bank; module 0 and the untouched clusters keep
+    their old bases (rows of those clusters compare against the old oracle bank)."""
+    N, C, r, T = 64, 8, 16, 600
+    shapes = [(512, 256), (512, 512)]
+    old = [quantized_bank(di, do, N, C, r, seed=1500 + m, cluster_of=cluster_map(N, C, 1510 + m))
+           for m, (di, do) in enumerate(shapes)]
+    bank = make_bank(cts, [b for b, _ in old])
+    new_bits, _ = quantized_bank(512, 512, 3, 3, r, seed=1520, cluster_of=np.arange(3, dtype=np.int32))
+    targets = [5, 1, 6]
+    s_ = torch.cuda.Stream()
+    with torch.cuda.stream(s_):
+        bank.write_clusters(1, targets, dev_bf16(new_bits["in_basis"]), dev_bf16(new_bits["out_basis"]), stream=s_)
+    s_.synchronize()
+    upd_bits = {k: old[1][0][k].copy() for k in ("in_basis", "out_basis", "sigma")}
+    for q, c in enumerate(targets):
+        upd_bits["in_basis"][c] = new_bits["in_basis"][q]
+        upd_bits["out_basis"][c] = new_bits["out_basis"][q]
+    upd = {k: bf16_to_f64(upd_bits[k]) for k in upd_bits}
+    upd["cluster_of"] = old[1][1]["cluster_of"]
+    plan = cts.Plan(bank, T)
+    ta = decode_tokens(T, N, 1521, frac_none=0.05)
+    plan.segment(torch.from_numpy(ta).cuda())
+    xb = bf16_round(activations(T, 512, 1522))
+    x = dev_bf16(xb)
+    ys = [torch.zeros(T, do, dtype=torch.bfloat16, device="cuda") for (_, do) in shapes]
+    plan.apply_group([0, 1], [x, x], ys, 2.0)
+    torch.cuda.synchronize()
+    check_delta(ta, host_bits(ys[0]), old[0][1], xb, 2.0)
+    check_delta(ta, host_bits(ys[1]), upd, xb, 2.0)
+    with pytest.raises(cts.CtsError):
+        bank.write_clusters(1, [2, 2], dev_bf16(new_bits["in_basis"][:2]), dev_bf16(new_bits["out_basis"][:2]))
+    with pytest.raises(cts.CtsError):
+        bank.write_clusters(1, [C], dev_bf16(new_bits["in_basis"][:1]), dev_bf16(new_bits["out_basis"][:1]))
+    plan.close()
+    bank.close()
+
+
 def test_exclusive_device_same_bits(cts):
     """cts_set_exclusive_device(1) (non-cooperative fused launches) computes exactly what the default
     cooperative launch computes: a Mistral-like grouped layer, both modes, bit-identical y."""
