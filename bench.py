@@ -28,10 +28,12 @@ from workloads.gen import MISTRAL_LAYERS, MISTRAL_MODULES  # noqa: E402
 
 CONFIGS = {
     # BASELINE.json configs[2]: the metric's "1000 adapters" decode configuration (default)
-    "decode": dict(workload="cfg3_decode", N=1000, C=25, r=16, T=1024, prefill=False, layers=MISTRAL_LAYERS,
+    "decode": dict(workload="cfg3_decode", N=1000, C=25, r=16, T=1024, prefill=False, jd_bank=True,
+                   layers=MISTRAL_LAYERS,
                    modules=MISTRAL_MODULES, steps=300, warmup=10),
     # configs[3]: prefill, same bank, 16k tokens per batch
-    "prefill": dict(workload="cfg4_prefill", N=1000, C=25, r=16, T=16384, prefill=True, layers=MISTRAL_LAYERS,
+    "prefill": dict(workload="cfg4_prefill", N=1000, C=25, r=16, T=16384, prefill=True, jd_bank=True,
+                    layers=MISTRAL_LAYERS,
                     modules=MISTRAL_MODULES, steps=30, warmup=3),
     # configs[1]: single q_proj, 64 LoRAs, JD without clustering r=64, decode 256
     "q_proj": dict(workload="cfg2_q_proj", N=64, C=1, r=64, T=256, prefill=False, layers=1,
@@ -138,6 +140,45 @@ class SlotPool:
                 misses.append((s_, a))
             self.last[self.where[a]] = wave
         return {a: self.where[a] for a in need}, misses
+
+
+def jd_layer_bank(cts, cfg, dev, iters=10):
+    """One decoder layer's compressed bank built ON THE GPU: per module, planted-family
+    rank-16 LoRAs grouped by the cluster map (workloads.gen_torch.planted_lora_clusters_torch), jointly
+    compressed per cluster by cts_jd_eigen_iteration (App A.2, `iters` iterations from random
+    orthonormal bases, all 7 x C clusters in one call), assembled into the C-ABI layout in bf16.
+    Returns (per-module sources, GPU ms of the compression call)."""
+    import torch
+
+    from workloads.gen_torch import orthonormal_torch, planted_lora_clusters_torch
+    N, C, r = cfg["N"], cfg["C"], cfg["r"]
+    g = torch.Generator(device=dev).manual_seed(77)
+    cls, problems = [], []
+    for m, (_, di, do) in enumerate(cfg["modules"]):
+        cl = planted_lora_clusters_torch(di, do, N, C, 16, seed=m, device=dev, cluster_seed=50 + m)
+        cls.append(cl)
+        for c in range(C):
+            problems.append({"a_stack": cl["a_stack"][c], "bt_stack": cl["bt_stack"][c],
+                             "U": orthonormal_torch(do, r, g, dev), "V": orthonormal_torch(di, r, g, dev),
+                             "sigma": torch.empty(cl["members"][c].numel(), r, r, device=dev)})
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    ws = cts.cts_jd_eigen_iteration(problems, r, iters)
+    b.record()
+    b.synchronize()
+    srcs, k = [], 0
+    for m, cl in enumerate(cls):
+        sig = torch.empty(N, r, r, device=dev)
+        for c in range(C):
+            sig[cl["members"][c]] = problems[k + c]["sigma"]
+        srcs.append({"in_basis": torch.stack([problems[k + c]["V"] for c in range(C)]).to(torch.bfloat16).contiguous(),
+                     "out_basis": torch.stack([problems[k + c]["U"] for c in range(C)]).to(torch.bfloat16).contiguous(),
+                     "sigma": sig.to(torch.bfloat16).contiguous(), "cluster_of": cl["cluster_of"]})
+        k += C
+    del ws, problems, cls
+    torch.cuda.empty_cache()
+    return srcs, a.elapsed_time(b)
 
 
 def algorithmic_bytes(tokens, cluster_maps, mods, r, sigma_diag=False):
@@ -268,6 +309,33 @@ class OracleLayer:
             if x_slot(name) not in self.xs:
                 self.xs[x_slot(name)] = f64(torch.randn(T, di, generator=g).to(torch.bfloat16))
 
+    @classmethod
+    def from_tensors(cls, cfg, toks, banks, xs):
+        """The GPU run's own layer-0 inputs (host copies of the bf16 bank tensors, token ids and x),
+        so the CPU leg times -- and spot-checks -- exactly what the GPU computed."""
+        import torch
+        from workloads.bf16 import bf16_to_f64
+
+        def f64(t):
+            return bf16_to_f64(t.contiguous().view(torch.int16).numpy().view(np.uint16))
+
+        self = cls.__new__(cls)
+        self.cfg = cfg
+        self.mods = [(0, n, di, do) for (n, di, do) in cfg["modules"]]
+        self.toks = np.asarray(toks)
+        banks = [dict(b, sigma=torch.diag_embed(b["sigma"])) if b["sigma"].dim() == 2 else b for b in banks]
+        self.banks = [{k: (f64(v) if k != "cluster_of" else v.numpy()) for k, v in b.items()} for b in banks]
+        self.xs = {k: f64(v) for k, v in xs.items()}
+        return self
+
+    def delta(self, m):
+        """The oracle's delta_y of module m for every token (apply_ref, App D order)."""
+        from oracle import apply_ref
+        (_, name, _, _), b = self.mods[m], self.banks[m]
+        dy, _ = apply_ref(self.xs[x_slot(name)], self.toks, b["cluster_of"], b["in_basis"], b["out_basis"],
+                          b["sigma"], SCALE)
+        return dy
+
     def run_module(self, m):
         """segment_ref + apply_ref of module m; returns wall seconds."""
         from oracle import apply_ref, segment_ref
@@ -310,10 +378,11 @@ def oracle_one_thread(ol):
     return ol.cfg["T"] / (t * ol.cfg["layers"])
 
 
-def oracle_sample(cfg, budget_s=20.0):
+def oracle_sample(cfg, budget_s=20.0, ol=None):
     """Time the oracle on full layers (all 7 modules) repeatedly within ~budget_s; tokens/s
-    extrapolated to the whole step (x layers).  Also one 1-thread layer and the host CPU model."""
-    ol = OracleLayer(cfg)
+    extrapolated to the whole step (x layers).  Also one 1-thread layer and the host CPU model.
+    ol: the layer to time (default: drawn from the config's seeds on the host)."""
+    ol = ol if ol is not None else OracleLayer(cfg)
     reps, t_start = [], time.perf_counter()
     while not reps or time.perf_counter() - t_start + reps[-1] < budget_s:
         reps.append(sum(ol.run_module(m) for m in range(len(ol.mods))))
@@ -392,7 +461,7 @@ def run_tp(args, cfg):
     import torch.distributed as dist
 
     import paper_2407_00066_b200 as cts
-    from paper_2407_00066_b200.tp import TensorParallelApply, shard_bank, shard_cols
+    from paper_2407_00066_b200.tp import LibTensorParallelApply, create_comm, shard_bank, shard_cols
     from workloads.gen_torch import direct_bank_torch, tokens_torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -428,7 +497,8 @@ def run_tp(args, cfg):
         xs.append(shard_cols(xbuf[key], rank, world))
         ys.append(shard_cols(torch.randn(T, do, generator=g, device=dev).to(torch.bfloat16), rank, world))
     plan = cts.Plan(bank, T)
-    tp = TensorParallelApply(plan)
+    comm = create_comm(rank, world, device=dev)              # libcts's NCCL communicator (cts_comm_create)
+    tp = LibTensorParallelApply(plan, comm)
     groups = []
     for layer in range(cfg["layers"]):
         by_slot = {}
@@ -478,13 +548,14 @@ def run_tp(args, cfg):
         "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded direct banks + Gaussian activations)",
         "config": dict(config_dict(cfg, world), parallelism=f"tp{world} (d_model split, NCCL all-reduce of the "
-                       f"rank-{r} partial, {T * rp * 4} B per module)"),
+                       f"rank-{r} partial issued inside libcts by cts_apply_tp, {T * rp * 4} B per module)"),
         "gpu_launches": args.steps * launches, "launches_per_step": launches, "graph": graph is not None,
         "clocks": clocks.result(),
     }
     if rank == 0:
         emit(line)
     dist.barrier()
+    comm.close()
     dist.destroy_process_group()
     plan.close()
     bank.close()
@@ -620,8 +691,12 @@ def run_gpu(args, cfg):
     mods = module_list(cfg)
     M = len(mods)
     # --- resident bank (replicated on every rank: same seeds)
+    jd_ms = None
     if cfg.get("uncompressed"):
         srcs = [lora_bank_torch(di, do, N, r, seed=m, device=dev) for m, (_, _, di, do) in enumerate(mods)]
+    elif cfg.get("jd_bank"):                     # one layer compressed on the GPU, the same bank in every layer
+        layer_srcs, jd_ms = jd_layer_bank(cts, cfg, dev)
+        srcs = [layer_srcs[m % len(cfg["modules"])] for m in range(M)]
     else:
         srcs = [direct_bank_torch(di, do, N, C, r, seed=m % len(cfg["modules"]) + 1000 * (m // len(cfg["modules"])),
                                   device=dev, cluster_seed=50 + m) for m, (_, _, di, do) in enumerate(mods)]
@@ -631,6 +706,7 @@ def run_gpu(args, cfg):
     bank = cts.Bank([s["in_basis"] for s in srcs], [s["out_basis"] for s in srcs], [s["sigma"] for s in srcs],
                     [s["cluster_of"] for s in srcs])
     cmaps = [s["cluster_of"].cpu().numpy() for s in srcs]
+    layer0_host = [{k: v.cpu() for k, v in srcs[m].items()} for m in range(len(cfg["modules"]))]
     del srcs
     torch.cuda.empty_cache()
     # --- this rank's batch (request sharding: its own token stream) and activations
@@ -845,14 +921,43 @@ def run_gpu(args, cfg):
         "launches_per_step": launches_per_step,
         "clocks": clocks.result(),
     }
+    if jd_ms is not None:
+        line["config"]["bank_source"] = (f"JD-built on the GPU: one layer of planted-family rank-16 LoRAs compressed "
+                                         f"by cts_jd_eigen_iteration (App A.2, 10 iterations, {len(cfg['modules'])} "
+                                         f"x {C} clusters in one call, {jd_ms:.1f} ms), the same bank in every layer")
     if world > 1:
         dist.barrier()
     if rank == 0:
         if not args.no_cpu_baseline and not cfg.get("uncompressed"):
-            tok_s, info = oracle_sample(cfg, budget_s=args.cpu_budget)
+            # CPU leg on the run's OWN inputs (layer 0: bank, token ids, x): the oracle is timed on them
+            # and its delta_y checks this GPU's delta_y of every bound token of layer 0's 7 modules,
+            # applied once more onto zeroed outputs (per-row tolerance 5e-3, north_star)
+            l0 = [m for m, (lyr, _, _, _) in enumerate(mods) if lyr == 0]
+            yz = {m: torch.zeros_like(ys[m]) for m in l0}
+            with torch.cuda.stream(stream):
+                for gm in groups:
+                    if all(m in yz for m in gm):
+                        plan.apply_group(gm, [xs[m] for m in gm], [yz[m] for m in gm], SCALE)
+            stream.synchronize()
+            xs0 = {x_slot(name): xs[m].cpu() for m, (lyr, name, _, _) in enumerate(mods) if lyr == 0}
+            ol = OracleLayer.from_tensors(cfg, tokens.cpu().numpy(), layer0_host, xs0)
+            from workloads.bf16 import bf16_to_f64
+            bound = ol.toks >= 0
+            worst = 0.0
+            for m in l0:
+                ref = ol.delta(m)[bound]
+                got = bf16_to_f64(yz[m].cpu().view(torch.int16).numpy().view(np.uint16))[bound]
+                den = np.linalg.norm(ref, axis=1)
+                ok = den > 0
+                worst = max(worst, float((np.linalg.norm(got - ref, axis=1)[ok] / den[ok]).max(initial=0.0)))
+            line["parity_check"] = {"max_row_rel_err": worst, "tol": 5e-3, "pass": worst <= 5e-3,
+                                    "rows": int(bound.sum()) * len(l0),
+                                    "scope": "layer 0, all modules, every bound token, y_base = 0; the oracle "
+                                             "(fp64) on the same bf16 bank, token ids and x as the timed run"}
+            tok_s, info = oracle_sample(cfg, budget_s=args.cpu_budget, ol=ol)
             line["cpu_baseline"] = {"value": tok_s, "unit": "tokens/s", "cores": info["cores"], "kind": "oracle",
                                     "cpu_model": info["cpu_model"], "value_1thread": info["value_1thread"],
-                                    "sample": info["sample"]}
+                                    "sample": info["sample"] + "; inputs: this run's layer-0 bank, ids and x"}
         emit(line)
     if world > 1:
         dist.barrier()

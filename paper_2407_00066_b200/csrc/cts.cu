@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <vector>
@@ -606,8 +607,9 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
                                                        96 * 1024);
   CTS_CUDA(attr);
   for (int b0 = 0; b0 < count; b0 += kJdMaxBatch) {
-    JdBatch jb;
-    std::memset(&jb, 0, sizeof(jb));
+    std::unique_ptr<JdBatch> jbp(new (std::nothrow) JdBatch());   // 30 KB: not on the host stack
+    if (!jbp) return CTS_ERR_OUT_OF_MEMORY;
+    JdBatch& jb = *jbp;
     jb.count = std::min(kJdMaxBatch, count - b0);
     int kmax = 1, dmax = 1, nmax = 1, rimax = 1;
     for (int i = 0; i < jb.count; ++i) {
@@ -632,8 +634,9 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
       nmax = std::max(nmax, q.n);
       rimax = std::max(rimax, q.r_i);
     }
-    const dim3 g_rows((kmax + 63) / 64, (dmax + kJdSeg - 1) / kJdSeg, jb.count);
-    const dim3 g_cols((dmax + 127) / 128, (kmax + kJdKSeg - 1) / kJdKSeg, jb.count);
+    const dim3 g_rows((kmax + kJdRowsPerBlock - 1) / kJdRowsPerBlock, (dmax + kJdSeg - 1) / kJdSeg, jb.count);
+    const dim3 g_cols((dmax + 256 * JdColsPer<R>::v - 1) / (256 * JdColsPer<R>::v), (kmax + kJdKSeg - 1) / kJdKSeg,
+                      jb.count);
     const dim3 g_red(std::max(1, kmax * R / 1024), jb.count), g_cred(std::max(1, dmax * R / 1024), jb.count);
     const dim3 g_small(nmax, jb.count), g_gram((dmax + kJdGramRows - 1) / kJdGramRows, jb.count, 2);
     const dim3 g_one(1, jb.count, 2), g_ew(std::max(1, dmax * R / 256 / 4), jb.count, 2);
@@ -1265,9 +1268,6 @@ cts_status_t cts_rows_move(const void* src, int64_t ld_src, void* dst, int64_t l
 
 #ifdef CTS_TRACE
 // debug-only (not part of cts.h): copy the per-CTA timeline of the last traced launch
-int cts_debug_jobtrace(unsigned long long* host, int n) {
-  return cudaMemcpyFromSymbol(host, g_cts_jobtrace, std::min<size_t>(n, sizeof(g_cts_jobtrace) / 8) * 8) == cudaSuccess ? 0 : 1;
-}
 int cts_debug_trace(unsigned long long* host, int n) {
   return cudaMemcpyFromSymbol(host, g_cts_trace, std::min<size_t>(n, sizeof(g_cts_trace) / 8) * 8) == cudaSuccess ? 0 : 1;
 }

@@ -20,7 +20,7 @@
 
 namespace cts {
 
-constexpr int kJdMaxBatch = 32;
+constexpr int kJdMaxBatch = 240;   // problems per launch (kernel parameter space: 240 x 128 B)
 
 struct JdProblem {
   const float* a;        // A_stack [n*r_i][d_in]
@@ -45,74 +45,64 @@ struct JdBatch {
   int count;
 };
 
-// out[K][R] = X[K][d] * Y[d][R], split over d: block (row block of 64, d segment of kJdSeg) writes a
-// partial [seg][K][R] to the workspace (jd_rows_reduce sums the segments in order -- deterministic).
-// Chunks of 64 d: X [64 x 64] and Y [64 x R] staged by float4 loads; thread = (row, 4 columns).
+// out[K][R] = X[K][d] * Y[d][R], split over d: block (256 rows, d segment of kJdSeg) writes a partial
+// [seg][K][R] to the workspace (jd_rows_reduce sums the segments in order -- deterministic).
+// Thread = one row of X, all R outputs: its row streams in as 16-byte loads (the 128-byte lines of
+// a warp's 32 rows are re-used from L1 over 8 consecutive loads), Y is staged in shared memory in
+// chunks of kJdYChunk rows and read as warp-broadcast 16-byte loads -- 4R FMAs per R/4 + 1 loads,
+// so the kernel streams X at close to HBM speed instead of being bound by shared-memory traffic.
 constexpr int kJdSeg = 1024;
+constexpr int kJdRowsPerBlock = 256;
 
 template <int R>
-__global__ void __launch_bounds__(256) jd_rows_times(const __grid_constant__ JdBatch b, int which) {
+__global__ void __launch_bounds__(256, R <= 16 ? 4 : (R <= 32 ? 2 : 1)) jd_rows_times(const __grid_constant__ JdBatch b, int which) {
+  constexpr int kChunk = 4096 / R;                   // 16 KB of Y per stage
   const JdProblem& p = b.pr[blockIdx.z];
   const float* X = which == 0 ? p.a : p.bt;          // 0: P = A V, 1: Q = Bt U
   const float* Y = which == 0 ? p.V : p.U;
   const int d = which == 0 ? p.d_in : p.d_out;
   const int K = p.n * p.ri;
-  const int row0 = blockIdx.x * 64, d_lo = blockIdx.y * kJdSeg;
+  const int row0 = blockIdx.x * kJdRowsPerBlock, d_lo = blockIdx.y * kJdSeg;
   if (row0 >= K || d_lo >= d) return;
   const int d_hi = min(d, d_lo + kJdSeg);
   float* part = p.part + (static_cast<size_t>(blockIdx.y) * K) * R;
-  __shared__ float4 xs4[64][16 + 1];                   // [row][64 d as 16 float4] (+1 float4 pad)
-  __shared__ float ys[64][R];
-  constexpr int RQ = R / 4;                            // threads per row (4 columns each)
-  constexpr int RPB = 256 / RQ;                        // rows computed per pass
-  const int tr = threadIdx.x / RQ, tc = (threadIdx.x % RQ) * 4;
-  float acc[(64 + RPB - 1) / RPB][4];
+  __shared__ float4 ys[kChunk * R / 4];              // [chunk row][R / 4]
+  const int row = row0 + threadIdx.x;
+  const bool live = row < K;
+  const float* xr = X + static_cast<size_t>(live ? row : 0) * d;
+  float acc[R];
 #pragma unroll
-  for (int q = 0; q < (64 + RPB - 1) / RPB; ++q)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[q][c] = 0.f;
-  for (int d0 = d_lo; d0 < d_hi; d0 += 64) {
-    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
-      const int r = i >> 4, c4 = i & 15;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (row0 + r < K && d0 + 4 * c4 < d_hi)
-        v = *reinterpret_cast<const float4*>(X + static_cast<size_t>(row0 + r) * d + d0 + 4 * c4);
-      xs4[r][c4] = v;
-    }
-    for (int i = threadIdx.x; i < 64 * R / 4; i += 256) {
-      const int r = i / (R / 4), c4 = i % (R / 4);
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (d0 + r < d_hi) v = *reinterpret_cast<const float4*>(Y + static_cast<size_t>(d0 + r) * R + 4 * c4);
-      *reinterpret_cast<float4*>(&ys[r][4 * c4]) = v;
-    }
+  for (int c = 0; c < R; ++c) acc[c] = 0.f;
+  for (int d0 = d_lo; d0 < d_hi; d0 += kChunk) {
+    const int n = min(kChunk, d_hi - d0);
     __syncthreads();
+    for (int i = threadIdx.x; i < kChunk * R / 4; i += 256)
+      ys[i] = i < n * R / 4 ? reinterpret_cast<const float4*>(Y + static_cast<size_t>(d0) * R)[i]
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    if (live) {
+#pragma unroll 2
+      for (int k = 0; k < n; k += 4) {
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + d0 + k));
+        const float xk[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-    for (int q = 0; q < (64 + RPB - 1) / RPB; ++q) {
-      const int r = tr + q * RPB;
-      if (r < 64) {
-#pragma unroll 4
-        for (int k4 = 0; k4 < 16; ++k4) {
-          const float4 xv = xs4[r][k4];
-          const float xk[4] = {xv.x, xv.y, xv.z, xv.w};
+        for (int u = 0; u < 4; ++u) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float4 yv = *reinterpret_cast<const float4*>(&ys[4 * k4 + u][tc]);
-            acc[q][0] = fmaf(xk[u], yv.x, acc[q][0]);
-            acc[q][1] = fmaf(xk[u], yv.y, acc[q][1]);
-            acc[q][2] = fmaf(xk[u], yv.z, acc[q][2]);
-            acc[q][3] = fmaf(xk[u], yv.w, acc[q][3]);
+          for (int c4 = 0; c4 < R / 4; ++c4) {
+            const float4 yv = ys[(k + u) * (R / 4) + c4];
+            acc[4 * c4] = fmaf(xk[u], yv.x, acc[4 * c4]);
+            acc[4 * c4 + 1] = fmaf(xk[u], yv.y, acc[4 * c4 + 1]);
+            acc[4 * c4 + 2] = fmaf(xk[u], yv.z, acc[4 * c4 + 2]);
+            acc[4 * c4 + 3] = fmaf(xk[u], yv.w, acc[4 * c4 + 3]);
           }
         }
       }
     }
-    __syncthreads();
   }
+  if (live) {
+    float4* dst = reinterpret_cast<float4*>(part + static_cast<size_t>(row) * R);
 #pragma unroll
-  for (int q = 0; q < (64 + RPB - 1) / RPB; ++q) {
-    const int r = tr + q * RPB;
-    if (r < 64 && row0 + r < K)
-      *reinterpret_cast<float4*>(part + static_cast<size_t>(row0 + r) * R + tc) =
-          make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+    for (int c4 = 0; c4 < R / 4; ++c4) dst[c4] = make_float4(acc[4 * c4], acc[4 * c4 + 1], acc[4 * c4 + 2], acc[4 * c4 + 3]);
   }
 }
 
@@ -166,53 +156,80 @@ __global__ void __launch_bounds__(256) jd_small(const __grid_constant__ JdBatch 
   }
 }
 
-// out[d][R] = X[K][d]^T * M[K][R], split over K: block (128 columns of d, K segment of kJdKSeg rows)
-// writes a partial [kseg][d][R] (jd_cols_reduce sums the segments in order); X chunks [32 x 128] by
-// float4 loads; thread = (column, half of the R outputs).
-constexpr int kJdKSeg = 128;
+// out[d][R] = X[K][d]^T * M[K][R], split over K: block (256 * kJdColsPer(R) columns of d, K segment
+// of kJdKSeg rows) writes a partial [kseg][d][R] (jd_cols_reduce sums the segments in order).
+// Thread = kJdColsPer consecutive columns of d, all R outputs: X rows stream in as coalesced
+// 16/8-byte loads, M is staged in shared memory and read as warp-broadcast 16-byte loads.
+constexpr int kJdKSeg = 320;
 
 template <int R>
-__global__ void __launch_bounds__(256) jd_cols_times(const __grid_constant__ JdBatch b, int which) {
+struct JdColsPer {
+  static constexpr int v = R <= 16 ? 4 : (R <= 32 ? 2 : 1);
+};
+
+template <int R>
+__global__ void __launch_bounds__(256, R <= 32 ? 2 : 1) jd_cols_times(const __grid_constant__ JdBatch b, int which) {
+  constexpr int CP = JdColsPer<R>::v;
   const JdProblem& p = b.pr[blockIdx.z];
   const float* X = which == 0 ? p.bt : p.a;           // 0: U0 = Bt^T W, 1: V0 = A^T Z
   const float* Mt = which == 0 ? p.W : p.Z;
   const int d = which == 0 ? p.d_out : p.d_in;
   const int K = p.n * p.ri;
-  const int col0 = blockIdx.x * 128, k_lo = blockIdx.y * kJdKSeg;
-  if (col0 >= d || k_lo >= K) return;
+  const int col0 = (blockIdx.x * 256 + threadIdx.x) * CP, k_lo = blockIdx.y * kJdKSeg;
+  if (blockIdx.x * 256 * CP >= d || k_lo >= K) return;
   const int k_hi = min(K, k_lo + kJdKSeg);
   float* part = p.part + static_cast<size_t>(blockIdx.y) * d * R;
-  __shared__ float xs[32][128 + 4];
-  __shared__ float ms[32][R];
-  constexpr int CG = R / 2;
-  const int tcol = threadIdx.x & 127, tg = (threadIdx.x >> 7) * CG;
-  float acc[CG];
+  constexpr int kMs = 64;                             // M rows staged per pass
+  __shared__ float4 ms[kMs * R / 4];
+  const bool live = col0 < d;                         // d is a multiple of 64 (and of CP)
+  float acc[CP][R];
 #pragma unroll
-  for (int c = 0; c < CG; ++c) acc[c] = 0.f;
-  for (int k0 = k_lo; k0 < k_hi; k0 += 32) {
-    for (int i = threadIdx.x; i < 32 * 32; i += 256) {
-      const int r = i >> 5, c4 = i & 31;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (k0 + r < k_hi && col0 + 4 * c4 < d)
-        v = *reinterpret_cast<const float4*>(X + static_cast<size_t>(k0 + r) * d + col0 + 4 * c4);
-      xs[r][4 * c4] = v.x; xs[r][4 * c4 + 1] = v.y; xs[r][4 * c4 + 2] = v.z; xs[r][4 * c4 + 3] = v.w;
-    }
-    for (int i = threadIdx.x; i < 32 * R; i += 256) {
-      const int r = i / R, c = i % R;
-      ms[r][c] = k0 + r < k_hi ? Mt[static_cast<size_t>(k0 + r) * R + c] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const float xv = xs[k][tcol];
+  for (int j = 0; j < CP; ++j)
 #pragma unroll
-      for (int c = 0; c < CG; ++c) acc[c] = fmaf(xv, ms[k][tg + c], acc[c]);
-    }
+    for (int c = 0; c < R; ++c) acc[j][c] = 0.f;
+  for (int k0 = k_lo; k0 < k_hi; k0 += kMs) {
+    const int n = min(kMs, k_hi - k0);
     __syncthreads();
+    for (int i = threadIdx.x; i < kMs * R / 4; i += 256)
+      ms[i] = i < n * R / 4 ? reinterpret_cast<const float4*>(Mt + static_cast<size_t>(k0) * R)[i]
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    if (live) {
+#pragma unroll 2
+      for (int k = 0; k < n; ++k) {
+        float xv[CP];
+        const float* xp = X + static_cast<size_t>(k0 + k) * d + col0;
+        if constexpr (CP == 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(xp));
+          xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+        } else if constexpr (CP == 2) {
+          const float2 v = __ldg(reinterpret_cast<const float2*>(xp));
+          xv[0] = v.x; xv[1] = v.y;
+        } else {
+          xv[0] = __ldg(xp);
+        }
+#pragma unroll
+        for (int c4 = 0; c4 < R / 4; ++c4) {
+          const float4 mv = ms[k * (R / 4) + c4];
+#pragma unroll
+          for (int j = 0; j < CP; ++j) {
+            acc[j][4 * c4] = fmaf(xv[j], mv.x, acc[j][4 * c4]);
+            acc[j][4 * c4 + 1] = fmaf(xv[j], mv.y, acc[j][4 * c4 + 1]);
+            acc[j][4 * c4 + 2] = fmaf(xv[j], mv.z, acc[j][4 * c4 + 2]);
+            acc[j][4 * c4 + 3] = fmaf(xv[j], mv.w, acc[j][4 * c4 + 3]);
+          }
+        }
+      }
+    }
   }
-  if (col0 + tcol < d) {
+  if (live) {
 #pragma unroll
-    for (int c = 0; c < CG; ++c) part[static_cast<size_t>(col0 + tcol) * R + tg + c] = acc[c];
+    for (int j = 0; j < CP; ++j) {
+      float4* dst = reinterpret_cast<float4*>(part + static_cast<size_t>(col0 + j) * R);
+#pragma unroll
+      for (int c4 = 0; c4 < R / 4; ++c4)
+        dst[c4] = make_float4(acc[j][4 * c4], acc[j][4 * c4 + 1], acc[j][4 * c4 + 2], acc[j][4 * c4 + 3]);
+    }
   }
 }
 

@@ -58,3 +58,40 @@ def lora_bank_torch(d_in: int, d_out: int, N: int, r: int, seed: int, device):
     sigma = torch.eye(r, device=device, dtype=torch.bfloat16).expand(N, r, r).contiguous()
     cluster_of = torch.arange(N, dtype=torch.int32, device=device)
     return {"in_basis": A_t, "out_basis": B, "sigma": sigma, "cluster_of": cluster_of}
+
+
+def planted_lora_clusters_torch(d_in: int, d_out: int, N: int, C: int, r_i: int, seed: int, device,
+                                cluster_seed: int | None = None, families: int = 4, noise: float = 0.3):
+    """Trained-like rank-r_i LoRAs B_i A_i for GPU compression, grouped by a given cluster assignment
+    (cluster_of = pi(i) mod C, the direct_bank_torch recipe).  Inside a cluster the adapters come from
+    `families` planted factor pairs plus Gaussian noise (App H: trained LoRAs share structure, random
+    ones do not); A ~ N(0, 1/d_in), B ~ N(0, 1/r_i).  fp32.  Returns cluster_of [N] int32 and per
+    cluster c: members (adapter ids, increasing), a_stack [n_c*r_i][d_in] = [A_i; ...] and bt_stack
+    [n_c*r_i][d_out] = [B_i^T; ...] in member order -- the cts_jd_eigen_iteration layout."""
+    gc = torch.Generator()
+    gc.manual_seed(seed + 7919 if cluster_seed is None else cluster_seed)
+    cluster_of = torch.randperm(N, generator=gc) % C
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    members, a_st, bt_st = [], [], []
+    for c in range(C):
+        mem = torch.nonzero(cluster_of == c).flatten()
+        n = mem.numel()
+        fam_a = torch.randn(families, r_i, d_in, generator=g, device=device) / d_in ** 0.5
+        fam_b = torch.randn(families, d_out, r_i, generator=g, device=device) / r_i ** 0.5
+        f = torch.arange(n, device=device) % families
+        A = fam_a[f] + noise * torch.randn(n, r_i, d_in, generator=g, device=device) / d_in ** 0.5
+        B = fam_b[f] + noise * torch.randn(n, d_out, r_i, generator=g, device=device) / r_i ** 0.5
+        members.append(mem)
+        a_st.append(A.reshape(n * r_i, d_in).contiguous())
+        bt_st.append(B.transpose(1, 2).reshape(n * r_i, d_out).contiguous())
+    return {"cluster_of": cluster_of.to(torch.int32).to(device), "members": members, "a_stack": a_st,
+            "bt_stack": bt_st}
+
+
+def orthonormal_torch(rows: int, r: int, g, device):
+    """A random orthonormal [rows][r] fp32 basis (QR of a Gaussian, sign-fixed): JD's initial bases."""
+    q, rr = torch.linalg.qr(torch.randn(rows, r, generator=g, device=device, dtype=torch.float32))
+    s = torch.sign(torch.diagonal(rr))
+    s[s == 0] = 1
+    return (q * s[None, :]).contiguous()
