@@ -37,11 +37,7 @@ struct FusedSmem {
   static constexpr int kOffBarF = kOffBarE + ExpandCfg<RP>::kNumBars * 8;   // "shrink operands consumed"
   static constexpr int kOffBarT = kOffBarF + 8;                                // "shrink TMEM released"
   static constexpr int kOffMisc = kOffBarT + 8;
-  // local-t tile (shrink_local_t, r_pad 16): t hi | lo of this CTA's slot, the own expand items' A operand
-  static constexpr int kOffTloc = (kOffMisc + 64 + 1023) / 1024 * 1024;
-  static constexpr int kTlocBytes = RP == 16 ? 2 * ExpandCfg<RP>::kA : 0;
-  static constexpr int kBytes = kOffTloc + kTlocBytes + 1024;
-  static_assert(kBytes <= 232448, "fused kernel shared memory");
+  static constexpr int kBytes = kOffMisc + 64 + 1024;
   static constexpr uint32_t kTmemCols = 512;
   static_assert(ShrinkCfg<RP>::kTmemCols <= kTmemCols && ExpandCfg<RP>::kTmemCols <= kTmemCols, "TMEM");
 };
@@ -58,7 +54,6 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   ExpandRing RE = expand_ring<RP>(smem, reinterpret_cast<uint64_t*>(smem + S::kOffBarE));
   uint64_t* arena_free = reinterpret_cast<uint64_t*>(smem + S::kOffBarF);
   uint64_t* tmem_free = reinterpret_cast<uint64_t*>(smem + S::kOffBarT);
-  uint8_t* tloc = S::kTlocBytes ? smem + S::kOffTloc : nullptr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     CTS_STAMP(0);
@@ -110,40 +105,28 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   const int deal_r0 = (CTS_WEIGHTED_DEAL && W.M.total > static_cast<int>(gridDim.x))
                           ? W.M.total % static_cast<int>(gridDim.x) : 0;
   const int deal_k = p.s.mod[0].kblocks * kBK / (W.ks * CTS_DEAL_DIV * kBN);
-  // local-t mode (decode, r_pad 16): own expand items read t from this CTA's tile (shrink_local_t)
-  const bool loc = tloc != nullptr && shrink_local_t<RP>(p.s, W);
-  // the local deal is derived by each role after its shrink work (off the critical path of the first
-  // loads: it scans the work of every CTA)
-  auto deal = [&]() {
-    return local_deal(loc, W.M, W.ks, expand_map(p.e, nt_lane, lane), p.e.n_mod, nt_lane,
-                      lane < p.e.n_mod ? p.e.mod[lane].nblk : 0, lane);
-  };
-  const int ready_target = loc ? 1 : (shrink_dist_finish<RP>(p.s, W) ? W.ks : 1);
   if (warp < kProducerWarps) {
     shrink_producer<RP>(p.s, RS, W, warp, lane, first);
     if (threadIdx.x == 0) CTS_STAMP(3);               // producers done issuing
-    const LocalDeal LD = deal();
     mbar_wait(arena_free, 0);
     if (threadIdx.x == 0) CTS_STAMP(7);
-    expand_producer<RP>(p.e, RE, nt_lane, warp, lane, ready_target, deal_r0, deal_k, &LD);
+    expand_producer<RP>(p.e, RE, nt_lane, warp, lane, shrink_dist_finish<RP>(p.s, W) ? W.ks : 1, deal_r0,
+                        deal_k);
   } else if (warp == kMmaWarp) {
     shrink_mma<RP>(p.s, RS, W, lane);
     if (lane == 0) { umma_commit(arena_free); CTS_STAMP(4); }
     __syncwarp();
-    const LocalDeal LD = deal();
     mbar_wait(tmem_free, 0);                  // shrink accumulators and staged Sigma all read
     tc_fence_after();
-    expand_mma<RP>(p.e, RE, nt_lane, lane, deal_r0, deal_k, &LD, tloc ? smem_u32(tloc) : 0u);
+    expand_mma<RP>(p.e, RE, nt_lane, lane, deal_r0, deal_k);
   } else {
-    const LocalDeal LD = deal();               // while the shrink MMAs run
-    if (!shrink_epilogue<RP, DIAG>(p.s, RS, W, warp, lane, loc ? tloc : nullptr, tmem_free)) {
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tmem_free);
-    }
+    shrink_epilogue<RP, DIAG>(p.s, RS, W, warp, lane);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tmem_free);
     if (threadIdx.x == 32 * kEpiWarp0) CTS_STAMP(5);        // epilogue set 0 done
     if (threadIdx.x == 32 * (kEpiWarp0 + 4)) CTS_STAMP(6);  // epilogue set 1 done
-    expand_epilogue<RP, STORE>(p.e, RE, nt_lane, warp, lane, deal_r0, deal_k, &LD);
+    expand_epilogue<RP, STORE>(p.e, RE, nt_lane, warp, lane, deal_r0, deal_k);
   }
 
   // ---------------------------------------------------------------- exit: last CTA clears flags
@@ -155,10 +138,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_fused_kernel(const __g
   __syncthreads();
   if (*s_last_exit) {
     for (int g = 0; g < p.s.n_mod; ++g)
-      for (int i = threadIdx.x; i < p.s.tiles_bound; i += blockDim.x) {
-        p.s.mod[g].ready[i] = 0;
-        if (loc) p.s.mod[g].counters[i] = 0;        // local-t arrivals (single arrival per CTA)
-      }
+      for (int i = threadIdx.x; i < p.s.tiles_bound; i += blockDim.x) p.s.mod[g].ready[i] = 0;
     if (threadIdx.x == 0) {
       *p.exit_count = 0;
     }

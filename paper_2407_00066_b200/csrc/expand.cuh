@@ -177,94 +177,6 @@ __device__ __forceinline__ int expand_deal_item(const ExpandDeal& d, int j, int 
   return j < nA ? b + j * G : d.A + (b - d.r0) + (j - nA) * (G - d.r0);
 }
 
-// Local-t expand deal (fused kernel, shrink_local_t mode).  CTA b holding K chunk kc of slot s of
-// module g first takes OWN items of that slot, j = kc + ks*i (i < own_n = min(ceil((nblk_g - kc)/ks),
-// cap)), whose t is its own shared-memory tile; the items of a slot no own CTA takes (j >= ks*cap:
-// heavy modules) form a POOL, dealt in canonical (module, slot, j) order to the CTAs by the prefix of
-// their spare capacity cap - own_n, so every CTA ends with <= cap = ceil(items / grid) items.  Pool
-// items read t from global memory after the slot's ready flag (published by kc = 0).
-// Lane g of each warp holds module g's values; every role warp derives the same deal.
-struct LocalDeal {
-  int on;                               // launch-uniform
-  int own_item0, own_n, ks;             // own items: own_item0 + ks * i, i < own_n
-  int pool0, n;                         // this CTA's pool range starts at pool0; n = own_n + pool items
-  int base_j;                           // first pool j of every slot (= ks * cap)
-  int pool_pre, left, e_pre, e_nblk;    // lane g: pool prefix, pool items per slot, expand item prefix, nblk
-};
-
-__device__ __forceinline__ LocalDeal local_deal(bool on, const ItemMap& S, int ks, const ItemMap& E, int n_mod,
-                                                int nt_lane, int nblk_lane, int lane) {
-  LocalDeal D;
-  D.on = on;
-  D.ks = ks;
-  D.own_item0 = 0;
-  D.own_n = 0;
-  D.pool0 = 0;
-  D.n = 0;
-  if (!on) return D;
-  const int G = gridDim.x, b = blockIdx.x;
-  const int cap = (E.total + G - 1) / G;
-#ifndef CTS_LOCAL_NO_OWN
-#define CTS_LOCAL_NO_OWN 0     // debug: every item through the pool (global t)
-#endif
-  const int ocap = CTS_LOCAL_NO_OWN ? 0 : cap;
-  D.base_j = ks * ocap;
-  D.e_pre = E.pre;
-  D.e_nblk = nblk_lane;
-  D.left = lane < n_mod ? max(0, nblk_lane - ks * ocap) : 0;
-  const int cnt = lane < n_mod ? nt_lane * D.left : 0;
-  int inc = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += v;
-  }
-  D.pool_pre = inc - cnt;
-  const int pool_total = __shfl_sync(0xffffffffu, inc, 31);
-  // own items of CTA bp (a function of its shrink item only); the pool is dealt by the prefix of spare
-  // capacity in the order: CTAs without a shrink item first (they are free from the start), then the
-  // others by index -- ord(bp) < ord(b) selects the CTAs before b in that order
-  const int S_total = S.total;
-  auto ord = [&](int x) { return x >= S_total ? x - S_total : x + (G - S_total); };
-  const int ob = ord(b);
-  int spare_before = 0;
-  for (int base = 0; base < G; base += 32) {
-    const int bp = base + lane;
-    int gsel = 0, kcsel = 0, tsel = 0;
-    for (int g = 0; g < n_mod; ++g) {            // uniform loop: all lanes shuffle
-      const int pre = __shfl_sync(0xffffffffu, S.pre, g);
-      if (bp >= pre) { gsel = g; kcsel = (bp - pre) % ks; tsel = (bp - pre) / ks; }
-    }
-    const int nb = __shfl_sync(0xffffffffu, nblk_lane, gsel);
-    const int epre = __shfl_sync(0xffffffffu, E.pre, gsel);
-    const int own = bp < S.total ? min(max(0, (nb - kcsel + ks - 1) / ks), ocap) : 0;
-    if (bp == b) {
-      D.own_n = own;
-      D.own_item0 = epre + tsel * nb + kcsel;
-    }
-    spare_before += warp_sum(bp < G && ord(bp) < ob ? cap - own : 0);
-  }
-  D.own_n = __shfl_sync(0xffffffffu, D.own_n, b & 31);
-  D.own_item0 = __shfl_sync(0xffffffffu, D.own_item0, b & 31);
-  D.pool0 = min(spare_before, pool_total);
-  const int pool_end = min(spare_before + cap - D.own_n, pool_total);
-  D.n = D.own_n + (pool_end - D.pool0);
-  return D;
-}
-
-// the CTA's i-th expand item under a LocalDeal (warp-uniform i, all lanes participate)
-__device__ __forceinline__ int local_item(const LocalDeal& D, int n_mod, int i, int lane) {
-  if (i < D.own_n) return D.own_item0 + D.ks * i;
-  const int q = D.pool0 + (i - D.own_n);
-  const unsigned bal = __ballot_sync(0xffffffffu, lane < n_mod && D.left > 0 && D.pool_pre <= q);
-  const int g = 31 - __clz(bal);
-  const int qq = q - __shfl_sync(0xffffffffu, D.pool_pre, g);
-  const int left = __shfl_sync(0xffffffffu, D.left, g);
-  const int slot = qq / left;
-  return __shfl_sync(0xffffffffu, D.e_pre, g) + slot * __shfl_sync(0xffffffffu, D.e_nblk, g) + D.base_j +
-         qq % left;
-}
-
 template <int RP> __device__ __forceinline__ uint8_t* stage_y(const ExpandRing& R, int s) {
   return R.arena + s * ExpandCfg<RP>::kStage;
 }
@@ -284,19 +196,16 @@ template <int RP> __device__ __forceinline__ int4* stage_info(const ExpandRing& 
 // ------------------------------------------------------------------ TMA producers (warps 0-3)
 template <int RP>
 __device__ __forceinline__ void expand_produce(const ExpandParams& p, const ExpandRing& R, const ItemMap& M, int item,
-                                               int my, int lane, int ready_target, bool own = false);
+                                               int my, int lane, int ready_target);
 
 template <int RP>
 __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane,
                                 int ready_target = 1,       // fused: arrivals on a slot's "t ready" flag
-                                int deal_r0 = 0, int deal_k = 0,   // fused: weighted deal
-                                const LocalDeal* LD = nullptr) {   // fused: local-t deal
+                                int deal_r0 = 0, int deal_k = 0) {   // fused: weighted deal
+  using L = ExpandCfg<RP>;
   const ItemMap M = expand_map(p, nt_lane, lane);
   const ExpandDeal D = expand_deal(M.total, deal_r0, deal_k);
-  if (LD != nullptr && LD->on) {
-    for (int i = warp; i < LD->n; i += kProducerWarps)
-      expand_produce<RP>(p, R, M, local_item(*LD, p.n_mod, i, lane), i, lane, ready_target, i < LD->own_n);
-  } else if (D.nB == 0) {                                // plain round-robin (decode: always)
+  if (D.nB == 0) {                                // plain round-robin (decode: always)
     int li = 0;                                   // index over this CTA's items
     for (int item = blockIdx.x; item < M.total; item += gridDim.x) {
       const int my = li++;
@@ -311,10 +220,9 @@ __device__ void expand_producer(const ExpandParams& p, const ExpandRing& R, int 
 }
 
 // One work item's loads into ring stage my % kStages (one producer warp, all lanes).
-// own = true (local-t deal): the item's t is this CTA's shared-memory tile -- no flag, no t load.
 template <int RP>
 __device__ __forceinline__ void expand_produce(const ExpandParams& p, const ExpandRing& R, const ItemMap& M, int item,
-                                               int my, int lane, int ready_target, bool own) {
+                                               int my, int lane, int ready_target) {
   using L = ExpandCfg<RP>;
   {
     int local;
@@ -330,11 +238,8 @@ __device__ __forceinline__ void expand_produce(const ExpandParams& p, const Expa
     const bool gvalid = shared ? (lane < 16 ? 4 * lane < l0 : 4 * (lane - 16) < l1) : 4 * lane < l0;
     const int ngroups = (l0 + l1) >> 2;
     const bool early = !p.poll_first && my < p.early_items;
-#ifndef CTS_DEBUG_OWN_POLL
-#define CTS_DEBUG_OWN_POLL 0   // debug: own items also wait for the slot's published flag
-#endif
-    const bool poll_late = m.ready != nullptr && early && (!own || CTS_DEBUG_OWN_POLL);
-    if (m.ready != nullptr && !early && (!own || CTS_DEBUG_OWN_POLL)) {
+    const bool poll_late = m.ready != nullptr && early;
+    if (m.ready != nullptr && !early) {
       if (lane == 0) {
         while (ld_acquire_gpu(m.ready + tile) < ready_target) nanosleep_ns(64);
         fence_proxy_async_global();
@@ -352,7 +257,7 @@ __device__ __forceinline__ void expand_produce(const ExpandParams& p, const Expa
     // out_basis blocks and y rows do not depend on the shrink: issue them first, so in the fused
     // kernel they stream in while this slot's t is still being reduced
     if (lane == 0) {
-      mbar_arrive_expect_tx(&R.full[stage], static_cast<uint32_t>((own ? 0 : 2 * L::kA) + (shared ? 2 : 1) * L::kB1 +
+      mbar_arrive_expect_tx(&R.full[stage], static_cast<uint32_t>(2 * L::kA + (shared ? 2 : 1) * L::kB1 +
                                                                    L::kSeg * ngroups * 512));
 #pragma unroll
       for (int s = 0; s < L::kSeg; ++s) {
@@ -382,10 +287,8 @@ __device__ __forceinline__ void expand_produce(const ExpandParams& p, const Expa
         fence_proxy_async_global();
         if (my == 0) CTS_STAMP(8);                // first expand item's t available
       }
-      if (!own) {
-        tma_load_2d(stage_a<RP>(R, stage), m.tm_t, &R.full[stage], 0, tile * kTileM);
-        tma_load_2d(stage_a<RP>(R, stage) + L::kA, m.tm_t, &R.full[stage], RP, tile * kTileM);
-      }
+      tma_load_2d(stage_a<RP>(R, stage), m.tm_t, &R.full[stage], 0, tile * kTileM);
+      tma_load_2d(stage_a<RP>(R, stage) + L::kA, m.tm_t, &R.full[stage], RP, tile * kTileM);
     }
     __syncwarp();
   }
@@ -394,15 +297,14 @@ __device__ __forceinline__ void expand_produce(const ExpandParams& p, const Expa
 // ------------------------------------------------------------------ MMA issuer (warp 4)
 template <int RP>
 __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_lane, int lane, int deal_r0 = 0,
-                           int deal_k = 0, const LocalDeal* LD = nullptr, uint32_t tloc = 0) {
+                           int deal_k = 0) {
   using L = ExpandCfg<RP>;
   // N = 2 kBN: the two halves' out_basis blocks are contiguous in the B stage (256 rows), so one
   // MMA per K step gives D0 = t U_c0^T (cols [0,128)) and D1 = t U_c1^T (cols [128,256)); for an
   // unshared slot the second block is stale and D1 is never read.
   constexpr uint32_t idesc = umma_idesc_bf16(kTileM, 2 * kBN);
   const ItemMap M = expand_map(p, nt_lane, lane);
-  const bool loc = LD != nullptr && LD->on;
-  const int n_items = loc ? LD->n : expand_deal_count(expand_deal(M.total, deal_r0, deal_k));
+  const int n_items = expand_deal_count(expand_deal(M.total, deal_r0, deal_k));
   int stage = 0, slot = 0;
   uint32_t phase = 0, aphase = 0;
   for (int li = 0; li < n_items; ++li) {
@@ -411,8 +313,7 @@ __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_la
     tc_fence_after();
     if (lane == 0) {
       const uint32_t acc = R.tmem + slot * L::kSlotCols;
-      const uint32_t hi = (loc && li < LD->own_n) ? tloc : smem_u32(stage_a<RP>(R, stage));
-      const uint32_t lo = hi + L::kA, b = smem_u32(stage_b<RP>(R, stage));
+      const uint32_t hi = smem_u32(stage_a<RP>(R, stage)), lo = hi + L::kA, b = smem_u32(stage_b<RP>(R, stage));
 #pragma unroll
       for (int k = 0; k < RP / 16; ++k)
         umma_bf16(acc, umma_desc_kmajor(hi + k * 32, RP * 2), umma_desc_kmajor(b + k * 32, RP * 2), idesc, k != 0);
@@ -430,14 +331,14 @@ __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_la
 // ------------------------------------------------------------------ epilogue (warps 5-12)
 template <int RP, int STORE>
 __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane,
-                                int deal_r0 = 0, int deal_k = 0, const LocalDeal* LD = nullptr) {
+                                int deal_r0 = 0, int deal_k = 0) {
   using L = ExpandCfg<RP>;
   const ItemMap M = expand_map(p, nt_lane, lane);
   const int ew = warp - kEpiWarp0;               // 0..7
   const int set = ew >> 2;
   const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
   const int row = quarter * 32 + lane;
-  const int n_items = (LD != nullptr && LD->on) ? LD->n : expand_deal_count(expand_deal(M.total, deal_r0, deal_k));
+  const int n_items = expand_deal_count(expand_deal(M.total, deal_r0, deal_k));
   for (int my = 0; my < n_items; ++my) {
     if (!kEpiSplit && my % kEpiSets != set) continue;
     static_assert(!kEpiSplit || kEpiSets == kBN / 64, "split epilogue: one 64-column segment per set");

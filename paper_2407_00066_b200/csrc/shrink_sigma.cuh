@@ -173,28 +173,6 @@ struct ShrinkWork {
 // floor K split guarantees it when items <= grid) and all CTAs co-resident -- so only the fused
 // kernel (ready flags set), which already relies on co-residency, uses it; the standalone shrink
 // kernel (CTS_FUSED=0, TP partials) keeps the wait-free last-arriver finisher.
-// Local t (fused kernel, decode regime, r_pad 16): every CTA holds at most one shrink item, so ALL
-// ks CTAs of a slot wait for the ks partials (co-resident: cooperative launch or an exclusive
-// device), each sums them in kc order -- identical bits on every CTA -- and forms the slot's whole
-// t = scale * Sigma_i s from its TMEM-staged Sigma_i straight into a shared-memory tile: the A operand
-// of its OWN expand items of that slot (no t round trip through L2, no flag poll).  kc = 0 also
-// publishes t to global memory + the ready flag for items of the slot that other CTAs take
-// (apply_fused.cuh LocalDeal).  Saves ~3 dependent L2 round trips per launch.
-#ifndef CTS_LOCAL_T
-#define CTS_LOCAL_T 0   // measured: cfg3 decode 26.2 vs 25.8 us per launch (slower), cfg5 61.6 vs 61.9
-#endif
-template <int RP>
-__device__ __forceinline__ bool shrink_local_t(const ShrinkParams& p, const ShrinkWork& W) {
-  return CTS_LOCAL_T && RP == 16 && p.mod[0].ready != nullptr && W.M.total > 0 &&
-         W.M.total <= static_cast<int>(gridDim.x);
-}
-
-// byte offset of element (row, col) of a [128][RP] bf16 tile in the 32-byte-swizzled K-major layout
-// TMA SWIZZLE_32B writes (16-byte chunk index ^= bit 2 of the row) -- RP = 16 only
-__device__ __forceinline__ uint32_t sw32_offset(int row, int chunk) {
-  return static_cast<uint32_t>(row * 32 + ((chunk ^ ((row >> 2) & 1)) << 4));
-}
-
 template <int RP>
 __device__ __forceinline__ bool shrink_dist_finish(const ShrinkParams& p, const ShrinkWork& W) {
   return CTS_DIST_FINISH && RP >= CTS_DIST_MIN_RP && !p.sigma_diag && p.mod[0].ready != nullptr && W.ks > 1 &&
@@ -515,158 +493,11 @@ __device__ __forceinline__ void store_t8(const ShrinkMod& m, int tile, int row, 
   *reinterpret_cast<uint4*>(dst + RP) = lo;
 }
 
-// Local-t finishing of a slot by one CTA of its ks (shrink_local_t): s (this CTA's partial) in
-// registers on entry.
-template <int RP, bool DIAG>
-__device__ __forceinline__ void shrink_local_finish(const ShrinkParams& p, const ShrinkMod& m, int tile, int kc, int ks,
-                                                    int row, int set, int set_tid, bool rvalid, int adapter,
-                                                    uint32_t tsig, float* s, uint8_t* tloc, uint64_t* tmem_free,
-                                                    int lane) {
-  (void)p;
-  if (ks > 1) {
-    float* const wbase = m.ws + (static_cast<size_t>(tile) * ks * kTileM + row) * RP;   // + kc*128*RP
-    if (rvalid) {
-      float4* dst = reinterpret_cast<float4*>(wbase + static_cast<size_t>(kc) * kTileM * RP);
-#pragma unroll
-      for (int c = 0; c < RP / 4; c += 2)
-        st_global_v8(dst + c, make_uint4(__float_as_uint(s[4 * c]), __float_as_uint(s[4 * c + 1]),
-                                         __float_as_uint(s[4 * c + 2]), __float_as_uint(s[4 * c + 3])),
-                     make_uint4(__float_as_uint(s[4 * c + 4]), __float_as_uint(s[4 * c + 5]),
-                                __float_as_uint(s[4 * c + 6]), __float_as_uint(s[4 * c + 7])));
-    }
-    named_bar_sync(1 + set, 128);
-    if (set_tid == 0) {
-      CTS_STAMP(12);
-      atom_add_acq_rel_gpu(&m.counters[tile], 1);
-      while (ld_acquire_gpu(&m.counters[tile]) < ks) nanosleep_ns(32);
-      // no second arrival: the last CTA to exit the launch clears the counters (apply_fused.cuh)
-    }
-    named_bar_sync(1 + set, 128);
-    if (rvalid) {
-      // sum in kc order (every CTA of the slot gets identical bits); own chunk from registers
-      float own[RP];
-#pragma unroll
-      for (int c = 0; c < RP; ++c) { own[c] = s[c]; s[c] = 0.f; }
-      constexpr int kChunk = CTS_KCHUNK_NUM / RP > 1 ? CTS_KCHUNK_NUM / RP : 1;
-      for (int q0 = 0; q0 < ks; q0 += kChunk) {
-        float4 buf[kChunk][RP / 4];
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          if (q0 + j < ks && q0 + j != kc) {
-            const float4* src = reinterpret_cast<const float4*>(wbase + static_cast<size_t>(q0 + j) * kTileM * RP);
-#pragma unroll
-            for (int c = 0; c < RP / 4; c += 2) {
-              uint4 a, b;
-              ld_global_cg_v8(src + c, a, b);
-              buf[j][c] = make_float4(__uint_as_float(a.x), __uint_as_float(a.y), __uint_as_float(a.z),
-                                      __uint_as_float(a.w));
-              buf[j][c + 1] = make_float4(__uint_as_float(b.x), __uint_as_float(b.y), __uint_as_float(b.z),
-                                          __uint_as_float(b.w));
-            }
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          if (q0 + j >= ks) break;
-          if (q0 + j == kc) {
-#pragma unroll
-            for (int c = 0; c < RP; ++c) s[c] += own[c];
-          } else {
-#pragma unroll
-            for (int c = 0; c < RP / 4; ++c) {
-              s[4 * c] += buf[j][c].x; s[4 * c + 1] += buf[j][c].y;
-              s[4 * c + 2] += buf[j][c].z; s[4 * c + 3] += buf[j][c].w;
-            }
-          }
-        }
-      }
-    }
-    if (set_tid == 0) CTS_STAMP(13);
-  }
-  // t = scale * Sigma_i s (TMEM-staged Sigma_i; JD-Diag: sigma_i .* s); zeros for padding rows
-  float t[RP];
-  if constexpr (DIAG) {
-    const uint4* sg = reinterpret_cast<const uint4*>(m.sigma + static_cast<size_t>(adapter) * RP);
-#pragma unroll
-    for (int v = 0; v < RP / 8; ++v) {
-      const uint4 q = rvalid ? __ldg(sg + v) : make_uint4(0, 0, 0, 0);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h[e]);
-        t[8 * v + 2 * e] = f.x * s[8 * v + 2 * e] * m.scale;
-        t[8 * v + 2 * e + 1] = f.y * s[8 * v + 2 * e + 1] * m.scale;
-      }
-    }
-  } else {
-#pragma unroll 1
-    for (int h = 0; h < 4; ++h) {             // warp-collective TMEM loads (whole warps)
-      float w[32];
-      tmem_ld32(tsig + 32 * h, w);
-      tmem_ld_wait();
-#pragma unroll
-      for (int oo = 0; oo < 4; ++oo) {
-        float acc = 0.f;
-#pragma unroll
-        for (int e = 0; e < RP / 2; ++e) {
-          const uint32_t u = __float_as_uint(w[oo * (RP / 2) + e]);
-          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
-          acc = fmaf(f.x, s[2 * e], acc);
-          acc = fmaf(f.y, s[2 * e + 1], acc);
-        }
-        t[4 * h + oo] = acc * m.scale;
-      }
-    }
-  }
-  // hi | lo tiles ([128][16] bf16 each, 32-byte swizzle: the layout the expand MMA reads)
-  uint4 hi[2], lo[2];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&hi[q]);
-    __nv_bfloat162* ll = reinterpret_cast<__nv_bfloat162*>(&lo[q]);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float a = rvalid ? t[8 * q + 2 * e] : 0.f, b = rvalid ? t[8 * q + 2 * e + 1] : 0.f;
-      const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-      const float2 hf = __bfloat1622float2(h2);
-      hh[e] = h2;
-      ll[e] = __floats2bfloat162_rn(a - hf.x, b - hf.y);
-    }
-  }
-  constexpr int kTile = kTileM * RP * 2;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    *reinterpret_cast<uint4*>(tloc + sw32_offset(row, q)) = hi[q];
-    *reinterpret_cast<uint4*>(tloc + kTile + sw32_offset(row, q)) = lo[q];
-  }
-  fence_proxy_async_smem();                     // generic-proxy writes -> visible to the tensor core
-  tc_fence_before();
-  __syncwarp();
-  if (lane == 0) mbar_arrive(tmem_free);        // Sigma / accumulator TMEM read, local t tile written
-  if (set_tid == 0) CTS_STAMP(14);
-  if (kc == 0) {                                 // publish t for the slot's items other CTAs take
-    if (rvalid) {
-      __nv_bfloat16* dst = m.tbuf + (static_cast<size_t>(tile) * kTileM + row) * (2 * RP);
-      st_global_v8(dst, hi[0], hi[1]);
-      st_global_v8(dst + RP, lo[0], lo[1]);
-    }
-    fence_proxy_async_global();
-    named_bar_sync(1 + set, 128);
-    if (set_tid == 0) {
-      st_release_gpu(&m.ready[tile], 1);
-      CTS_STAMP(15);
-    }
-  }
-}
-
 // ------------------------------------------------------------------ epilogue (warps 5-12)
 // DIAG: the bank is of kind CTS_SIGMA_DIAG (a separate instantiation, so the diagonal path adds no
 // register pressure to the full-Sigma path).
-// tloc / tmem_free: fused kernel only (local-t mode: the slot's t tile and the barrier the expand MMA
-// waits on before reusing TMEM).  Returns true when this warp already arrived on tmem_free.
 template <int RP, bool DIAG>
-__device__ bool shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, const ShrinkWork& W, int warp, int lane,
-                                uint8_t* tloc = nullptr, uint64_t* tmem_free = nullptr) {
+__device__ void shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, const ShrinkWork& W, int warp, int lane) {
   using L = ShrinkCfg<RP>;
   const int ks = W.ks;
   const ItemMap& M = W.M;
@@ -675,8 +506,7 @@ __device__ bool shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
   const int quarter = warp & 3;                  // TMEM lane quarter this warp may access
   const int row = quarter * 32 + lane;
   const int set_tid = (ew & 3) * 32 + lane;      // 0..127 within the set
-  const bool loc_mode = tloc != nullptr && shrink_local_t<RP>(p, W);   // launch-uniform
-  const bool dist = !loc_mode && shrink_dist_finish<RP>(p, W);          // launch-uniform
+  const bool dist = shrink_dist_finish<RP>(p, W);   // launch-uniform
   constexpr bool diag = DIAG;
   const int rpc = (kTileM + ks - 1) / ks;        // dist: rows finished per CTA of a slot
   int li = 0;                                    // index over this CTA's items
@@ -732,14 +562,6 @@ __device__ bool shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&R.acc_empty[slot]);
-
-    if constexpr (RP == 16) {
-      if (loc_mode) {
-        shrink_local_finish<RP, DIAG>(p, m, tile, kc, ks, row, set, set_tid, rvalid, adapter, tsig, s, tloc,
-                                      tmem_free, lane);
-        return true;                                 // at most one item per CTA in this mode
-      }
-    }
 
     bool finisher = true;                          // this thread's row is finished here
     if (ks > 1) {
@@ -944,7 +766,6 @@ __device__ bool shrink_epilogue(const ShrinkParams& p, const ShrinkRing& R, cons
       if (set_tid == 0) CTS_STAMP(15);                  // flag published
     }
   }
-  return false;
 }
 
 // ------------------------------------------------------------------ standalone kernel
