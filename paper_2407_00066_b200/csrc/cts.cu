@@ -20,6 +20,7 @@
 #include "expand.cuh"
 #include "proj_fused.cuh"
 #include "jd_eigen.cuh"
+#include "jd_tc.cuh"
 #include "segment.cuh"
 #include "shrink_sigma.cuh"
 
@@ -64,6 +65,20 @@ bool make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, 
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// fp32 2-D map (GPU compression, jd_tc.cuh): rows of `inner` floats, 128B swizzle
+bool make_tmap_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                   uint32_t box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -592,12 +607,96 @@ cts_status_t launch_project(cts_plan_t p, int32_t module, const void* x, int64_t
 }
 
 // ------------------------------------------------------------------ GPU compression (App A.2)
+// Tensor-core path (jd_tc.cuh) for r_pad >= 16 when every stacked K = n r_i is a multiple of 4
+// (16-byte TMA row strides); otherwise the CUDA-core kernels of jd_eigen.cuh.
+bool jd_tc_ok(const cts_jd_problem_t& q, int r) {
+  return r >= 16 && (q.n * q.r_i) % 4 == 0 && reinterpret_cast<uintptr_t>(q.a_stack) % 16 == 0 &&
+         reinterpret_cast<uintptr_t>(q.bt_stack) % 16 == 0;
+}
+
 size_t jd_problem_floats(const cts_jd_problem_t& q, int r) {
   const size_t K = size_t(q.n) * q.r_i;
   const size_t gb = (size_t(q.d_in) + 255) / 256 + (size_t(q.d_out) + 255) / 256;
   const size_t dmax = size_t(std::max(q.d_in, q.d_out));
   const size_t part = std::max((dmax + kJdSeg - 1) / kJdSeg * K, (K + kJdKSeg - 1) / kJdKSeg * dmax) * r;
-  return 4 * K * r + size_t(q.d_in + q.d_out) * r + gb * r * r + part + 64;   // + Gram, segment partials
+  size_t f = 4 * K * r + size_t(q.d_in + q.d_out) * r + gb * r * r + part + 64;   // + Gram, segment partials
+  if (jd_tc_ok(q, r))   // A^T, Bt^T, V^T, U^T, W^T, Z^T (K-major operands of the tensor-core GEMMs)
+    f += K * size_t(q.d_in + q.d_out) + size_t(r) * (q.d_in + q.d_out + 2 * K) + 64;
+  return f;
+}
+
+// One batch's tensor-core tables (maps, jobs, tile lists, transpose jobs) in one device block.
+struct JdTcTables {
+  std::vector<uint8_t> host;
+  void* dev = nullptr;
+  size_t off_jobs[4] = {}, off_tiles[4] = {}, off_tr[3] = {};
+  int n_tiles[4] = {}, n_tr[3] = {};
+};
+
+template <int R>
+cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, JdTcTables& T, cudaStream_t stream) {
+  const int n = jb.count;
+  // per problem: maps 0..7 = X: A, Bt, A^T, Bt^T; Y: V^T, U^T, W^T, Z^T
+  std::vector<CUtensorMap> maps(size_t(n) * 8);
+  std::vector<int2> tiles[4];
+  std::vector<JdTransposeJob> tr[3];
+  for (int i = 0; i < n; ++i) {
+    const JdProblem& p = jb.pr[i];
+    const int K = p.n * p.ri;
+    float* at = tc_base[i];
+    float* btt = at + size_t(K) * p.d_in;
+    float* vt = btt + size_t(K) * p.d_out;
+    float* ut = vt + size_t(R) * p.d_in;
+    float* wt = ut + size_t(R) * p.d_out;
+    float* zt = wt + size_t(R) * K;
+    CUtensorMap* m = &maps[size_t(i) * 8];
+    if (!make_tmap_f32(&m[0], p.a, p.d_in, K, 32, 128) || !make_tmap_f32(&m[1], p.bt, p.d_out, K, 32, 128) ||
+        !make_tmap_f32(&m[2], at, K, p.d_in, 32, 128) || !make_tmap_f32(&m[3], btt, K, p.d_out, 32, 128) ||
+        !make_tmap_f32(&m[4], vt, p.d_in, R, 32, R) || !make_tmap_f32(&m[5], ut, p.d_out, R, 32, R) ||
+        !make_tmap_f32(&m[6], wt, K, R, 32, R) || !make_tmap_f32(&m[7], zt, K, R, 32, R))
+      return CTS_ERR_CUDA;
+    const int rowsP = (K + 127) / 128, rowsU = (p.d_out + 127) / 128, rowsV = (p.d_in + 127) / 128;
+    for (int t = 0; t < rowsP; ++t) tiles[0].push_back(make_int2(i, t * 128));   // P = A V
+    for (int t = 0; t < rowsP; ++t) tiles[1].push_back(make_int2(i, t * 128));   // Q = Bt U
+    for (int t = 0; t < rowsU; ++t) tiles[2].push_back(make_int2(i, t * 128));   // U0 = Bt^T W
+    for (int t = 0; t < rowsV; ++t) tiles[3].push_back(make_int2(i, t * 128));   // V0 = A^T Z
+    tr[0].push_back({p.a, at, K, p.d_in});
+    tr[0].push_back({p.bt, btt, K, p.d_out});
+    tr[1].push_back({p.V, vt, p.d_in, R});
+    tr[1].push_back({p.U, ut, p.d_out, R});
+    tr[2].push_back({p.W, wt, K, R});
+    tr[2].push_back({p.Z, zt, K, R});
+  }
+  auto al = [](size_t v) { return (v + 127) / 128 * 128; };
+  size_t off = al(maps.size() * sizeof(CUtensorMap));
+  for (int g = 0; g < 4; ++g) { T.off_jobs[g] = off; off = al(off + size_t(n) * sizeof(JdTcJob)); }
+  for (int g = 0; g < 4; ++g) {
+    T.off_tiles[g] = off;
+    T.n_tiles[g] = int(tiles[g].size());
+    off = al(off + tiles[g].size() * sizeof(int2));
+  }
+  for (int g = 0; g < 3; ++g) {
+    if (tr[g].size() > size_t(kJdMaxTranspose)) return CTS_ERR_SHAPE;
+    T.off_tr[g] = off;
+    T.n_tr[g] = int(tr[g].size());
+    off = al(off + sizeof(JdTransposeBatch));
+  }
+  T.host.assign(off, 0);
+  if (cudaMallocAsync(&T.dev, off, stream) != cudaSuccess) { (void)cudaGetLastError(); return CTS_ERR_OUT_OF_MEMORY; }
+  std::memcpy(T.host.data(), maps.data(), maps.size() * sizeof(CUtensorMap));
+  const CUtensorMap* dmaps = static_cast<const CUtensorMap*>(T.dev);
+  for (int i = 0; i < n; ++i) {
+    const JdProblem& p = jb.pr[i];
+    const int K = p.n * p.ri;
+    const CUtensorMap* m = dmaps + size_t(i) * 8;
+    const JdTcJob jobs[4] = {{m + 0, m + 4, p.P, K, p.d_in}, {m + 1, m + 5, p.Q, K, p.d_out},
+                             {m + 3, m + 6, p.U0, p.d_out, K}, {m + 2, m + 7, p.V0, p.d_in, K}};
+    for (int g = 0; g < 4; ++g) std::memcpy(T.host.data() + T.off_jobs[g] + i * sizeof(JdTcJob), &jobs[g], sizeof(JdTcJob));
+  }
+  for (int g = 0; g < 4; ++g) std::memcpy(T.host.data() + T.off_tiles[g], tiles[g].data(), tiles[g].size() * sizeof(int2));
+  for (int g = 0; g < 3; ++g) std::memcpy(T.host.data() + T.off_tr[g], tr[g].data(), tr[g].size() * sizeof(JdTransposeJob));
+  if (cudaMemcpyAsync(T.dev, T.host.data(), off, cudaMemcpyHostToDevice, stream) != cudaSuccess) return CTS_ERR_CUDA;
+  return CTS_OK;
 }
 
 template <int R>
@@ -612,6 +711,8 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
     JdBatch& jb = *jbp;
     jb.count = std::min(kJdMaxBatch, count - b0);
     int kmax = 1, dmax = 1, nmax = 1, rimax = 1;
+    bool tc = true;
+    float* tc_base[kJdMaxBatch];
     for (int i = 0; i < jb.count; ++i) {
       const cts_jd_problem_t& q = problems[b0 + i];
       JdProblem& p = jb.pr[i];
@@ -628,6 +729,10 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
       p.Gu = w; w += (size_t(q.d_out) + 255) / 256 * R * R;
       p.Gv = w; w += (size_t(q.d_in) + 255) / 256 * R * R;
       p.part = w;
+      w += std::max((size_t(std::max(q.d_in, q.d_out)) + kJdSeg - 1) / kJdSeg * K,
+                    (K + kJdKSeg - 1) / kJdKSeg * size_t(std::max(q.d_in, q.d_out))) * R;
+      tc_base[i] = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(w) + 255) & ~uintptr_t(255));
+      tc = tc && jd_tc_ok(q, R);
       ws += jd_problem_floats(q, R);
       kmax = std::max<int>(kmax, int(K));
       dmax = std::max({dmax, q.d_in, q.d_out});
@@ -639,9 +744,54 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
                       jb.count);
     const dim3 g_red(std::max(1, kmax * R / 1024), jb.count), g_cred(std::max(1, dmax * R / 1024), jb.count);
     const dim3 g_small(nmax, jb.count), g_gram((dmax + kJdGramRows - 1) / kJdGramRows, jb.count, 2);
-    const dim3 g_one(1, jb.count, 2), g_ew(std::max(1, dmax * R / 256 / 4), jb.count, 2);
+    const dim3 g_one(1, jb.count, 2), g_ew(std::max(1, (dmax + 255) / 256), jb.count, 2);
     const size_t small_smem = (2 * size_t(rimax) * R + R * R) * 4;
     if (small_smem > 96 * 1024) return CTS_ERR_SHAPE;
+    if constexpr (R >= 16) {
+      if (tc) {                          // tensor-core thin GEMMs (jd_tc.cuh); same orthogonalization
+        JdTcTables T;
+        cts_status_t st = jd_tc_prepare<R>(jb, tc_base, T, stream);
+        if (st != CTS_OK) return st;
+        static const cudaError_t attr_tc = set_smem(jd_tc_gemm<R>, JdTcCfg<R>::kBytes);
+        CTS_CUDA(attr_tc);
+        uint8_t* dv = static_cast<uint8_t*>(T.dev);
+        auto gemm = [&](int g) {
+          JdTcParams prm;
+          prm.jobs = reinterpret_cast<const JdTcJob*>(dv + T.off_jobs[g]);
+          prm.tiles = reinterpret_cast<const int2*>(dv + T.off_tiles[g]);
+          prm.n_tiles = T.n_tiles[g];
+          jd_tc_gemm<R><<<std::min(sm_count(), std::max(1, T.n_tiles[g])), 320, JdTcCfg<R>::kBytes, stream>>>(prm);
+        };
+        auto transpose = [&](int g) {
+          jd_transpose<<<dim3(g == 0 ? 256 : 16, 1, std::min(T.n_tr[g], 65535)), 256, 0, stream>>>(
+              reinterpret_cast<const JdTransposeBatch*>(dv + T.off_tr[g]), T.n_tr[g]);
+        };
+        transpose(0);                     // A^T, Bt^T (once)
+        transpose(1);                     // V^T, U^T of the initial bases
+        for (int it = 0; it < iters; ++it) {
+          gemm(0);                        // P = A V
+          gemm(1);                        // Q = Bt U
+          jd_small<R><<<g_small, 256, small_smem, stream>>>(jb);
+          transpose(2);                   // W^T, Z^T
+          gemm(2);                        // U0 = Bt^T W
+          gemm(3);                        // V0 = A^T Z
+          for (int pass = 0; pass < 2; ++pass) {
+            jd_gram<R><<<g_gram, 256, 0, stream>>>(jb, pass);
+            jd_chol<R><<<g_one, 32, 0, stream>>>(jb, pass);
+            jd_apply<R><<<g_ew, 256, 0, stream>>>(jb, pass);
+          }
+          transpose(1);                   // V^T, U^T of the new bases
+          g_launches.fetch_add(13, std::memory_order_relaxed);
+        }
+        gemm(0);
+        gemm(1);
+        jd_sigma<R><<<g_small, 256, 0, stream>>>(jb);
+        g_launches.fetch_add(5, std::memory_order_relaxed);
+        CTS_CUDA(cudaGetLastError());
+        if (cudaFreeAsync(T.dev, stream) != cudaSuccess) return CTS_ERR_CUDA;
+        continue;
+      }
+    }
     for (int it = 0; it < iters; ++it) {
       jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 0);
       jd_rows_reduce<R><<<g_red, 256, 0, stream>>>(jb, 0);
@@ -657,8 +807,7 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
         jd_chol<R><<<g_one, 32, 0, stream>>>(jb, pass);
         jd_apply<R><<<g_ew, 256, 0, stream>>>(jb, pass);
       }
-      jd_copy_back<R><<<g_ew, 256, 0, stream>>>(jb);
-      g_launches.fetch_add(16, std::memory_order_relaxed);
+      g_launches.fetch_add(15, std::memory_order_relaxed);
     }
     jd_rows_times<R><<<g_rows, 256, 0, stream>>>(jb, 0);
     jd_rows_reduce<R><<<g_red, 256, 0, stream>>>(jb, 0);

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(256) jd_cols_reduce(const __grid_constant__ Jd
 //   jd_chol:  G = sum_b partials in block order (deterministic), Cholesky G = R^T R, R^-1
 //   jd_apply: Y = X R^-1                                                   (rows in parallel)
 // blockIdx.y = problem, blockIdx.z = matrix (0: U, 1: V).  Pass 0 maps X = U0 -> Y = U, pass 1
-// maps U -> U0, and jd_copy_back moves the result into U (V likewise).
+// maps U -> U in place (jd_apply: every thread reads its whole row before writing it).
 constexpr int kJdGramRows = 256;
 
 template <int R>
@@ -263,7 +263,7 @@ __device__ __forceinline__ void jd_orth_mats(const JdProblem& p, int z, int pass
   float* X0 = u ? p.U0 : p.V0;
   float* X1 = u ? p.U : p.V;
   src = pass == 0 ? X0 : X1;
-  dst = pass == 0 ? X1 : X0;
+  dst = X1;
   gram = u ? p.Gu : p.Gv;
 }
 
@@ -277,34 +277,59 @@ __global__ void __launch_bounds__(256) jd_gram(const __grid_constant__ JdBatch b
   jd_orth_mats<R>(p, blockIdx.z, pass, src, dst, d, gram);
   const int r0 = blockIdx.x * kJdGramRows;
   if (r0 >= d) return;
-  __shared__ float xs[64][R + 1];
-  constexpr int E = (R * R + 255) / 256;
-  float g[E];
+  // thread = (row a, 4 columns c4) of the R x R Gram block, GROUPS row groups split each 64-row chunk
+  constexpr int CQ = R / 4, PAIRS = R * CQ;
+  constexpr int GROUPS = PAIRS >= 256 ? 1 : 256 / PAIRS, PER = (PAIRS + 255) / 256;
+  __shared__ float4 xs[64][CQ];
+  __shared__ float4 red[GROUPS > 1 ? GROUPS : 1][GROUPS > 1 ? PAIRS : 1];
+  const int grp = threadIdx.x / (PAIRS < 256 ? PAIRS : 256);
+  float4 acc[PER];
 #pragma unroll
-  for (int q = 0; q < E; ++q) g[q] = 0.f;
+  for (int q = 0; q < PER; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int c0 = r0; c0 < min(d, r0 + kJdGramRows); c0 += 64) {
-    for (int i = threadIdx.x; i < 64 * R; i += 256) {
-      const int r = i / R, c = i % R;
-      xs[r][c] = c0 + r < d ? src[static_cast<size_t>(c0 + r) * R + c] : 0.f;
+    for (int i = threadIdx.x; i < 64 * CQ; i += 256) {
+      const int rr = i / CQ, cq = i % CQ;
+      xs[rr][cq] = c0 + rr < d ? reinterpret_cast<const float4*>(src + static_cast<size_t>(c0 + rr) * R)[cq]
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < E; ++q) {
-      const int e = threadIdx.x + 256 * q;
-      if (e < R * R) {
-        const int a = e / R, c = e % R;
-        float s = g[q];
-#pragma unroll 16
-        for (int r = 0; r < 64; ++r) s = fmaf(xs[r][a], xs[r][c], s);
-        g[q] = s;
+    for (int q = 0; q < PER; ++q) {
+      const int e = (GROUPS > 1 ? threadIdx.x % PAIRS : threadIdx.x) + 256 * q;
+      if (e < PAIRS) {
+        const int a = e / CQ, c4 = e % CQ;
+#pragma unroll 4
+        for (int rr = grp; rr < 64; rr += GROUPS) {
+          const float xa = reinterpret_cast<const float*>(&xs[rr][0])[a];
+          const float4 xc = xs[rr][c4];
+          acc[q].x = fmaf(xa, xc.x, acc[q].x);
+          acc[q].y = fmaf(xa, xc.y, acc[q].y);
+          acc[q].z = fmaf(xa, xc.z, acc[q].z);
+          acc[q].w = fmaf(xa, xc.w, acc[q].w);
+        }
       }
     }
     __syncthreads();
   }
+  float4* out = reinterpret_cast<float4*>(gram + static_cast<size_t>(blockIdx.x) * R * R);
+  if constexpr (GROUPS > 1) {
+    red[grp][threadIdx.x % PAIRS] = acc[0];
+    __syncthreads();
+    if (threadIdx.x < PAIRS) {
+      float4 t = red[0][threadIdx.x];
 #pragma unroll
-  for (int q = 0; q < E; ++q) {
-    const int e = threadIdx.x + 256 * q;
-    if (e < R * R) gram[static_cast<size_t>(blockIdx.x) * R * R + e] = g[q];
+      for (int g = 1; g < GROUPS; ++g) {                  // fixed group order: deterministic
+        const float4 u = red[g][threadIdx.x];
+        t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+      }
+      out[threadIdx.x] = t;                               // [a][c4] = row a, columns 4c4..4c4+3
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = threadIdx.x + 256 * q;
+      if (e < PAIRS) out[e] = acc[q];
+    }
   }
 }
 
@@ -402,6 +427,8 @@ __global__ void __launch_bounds__(256) jd_chol(const __grid_constant__ JdBatch b
   }
 }
 
+// Y = X R^-1 (R^-1 upper triangular), thread = one row: the row is read whole into registers, so
+// the in-place second pass is safe; R^-1 is read from shared memory as warp broadcasts.
 template <int R>
 __global__ void __launch_bounds__(256) jd_apply(const __grid_constant__ JdBatch b, int pass) {
   const JdProblem& p = b.pr[blockIdx.y];
@@ -413,24 +440,25 @@ __global__ void __launch_bounds__(256) jd_apply(const __grid_constant__ JdBatch 
   __shared__ float Ri[R][R];
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) Ri[e / R][e % R] = gram[e];
   __syncthreads();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d * R; i += gridDim.x * blockDim.x) {
-    const int r = i / R, c = i % R;
-    const float* row = src + static_cast<size_t>(r) * R;
-    float s = 0.f;
-    for (int a = 0; a <= c; ++a) s = fmaf(row[a], Ri[a][c], s);
-    dst[i] = s;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < d; r += gridDim.x * blockDim.x) {
+    float x[R], y[R];
+    const float4* row = reinterpret_cast<const float4*>(src + static_cast<size_t>(r) * R);
+#pragma unroll
+    for (int c4 = 0; c4 < R / 4; ++c4) {
+      const float4 v = row[c4];
+      x[4 * c4] = v.x; x[4 * c4 + 1] = v.y; x[4 * c4 + 2] = v.z; x[4 * c4 + 3] = v.w;
+    }
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      float s = 0.f;
+#pragma unroll
+      for (int a = 0; a <= c; ++a) s = fmaf(x[a], Ri[a][c], s);
+      y[c] = s;
+    }
+    float4* out = reinterpret_cast<float4*>(dst + static_cast<size_t>(r) * R);
+#pragma unroll
+    for (int c4 = 0; c4 < R / 4; ++c4) out[c4] = make_float4(y[4 * c4], y[4 * c4 + 1], y[4 * c4 + 2], y[4 * c4 + 3]);
   }
-}
-
-// pass 1 wrote into U0 / V0: copy back into U / V
-template <int R>
-__global__ void __launch_bounds__(256) jd_copy_back(const __grid_constant__ JdBatch b) {
-  const JdProblem& p = b.pr[blockIdx.y];
-  const bool u = blockIdx.z == 0;
-  const int n = (u ? p.d_out : p.d_in) * R;
-  const float* s = u ? p.U0 : p.V0;
-  float* t = u ? p.U : p.V;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = s[i];
 }
 
 // Sigma_i = Q_i^T P_i (R x R; row = out index); blockIdx.x = adapter

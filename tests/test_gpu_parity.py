@@ -659,8 +659,12 @@ def _jd_problem(Bs, As, U0, V0):
             "U": f32(U0), "V": f32(V0), "sigma": torch.empty(n, r, r, device="cuda")}
 
 
-@pytest.mark.parametrize("r,dims,iters", [(8, (96, 80), 6), (16, (256, 192), 8), (16, (4096, 4096), 4)])
-def test_gpu_jd_eigen_iteration(cts, r, dims, iters):
+@pytest.mark.parametrize("r,dims,iters,shapes", [
+    (8, (96, 80), 6, None), (16, (256, 192), 8, None), (16, (4096, 4096), 4, None),
+    (32, (512, 384), 5, ((6, 16), (5, 8))),          # tensor-core path at r = 32
+    (16, (256, 192), 5, ((3, 6),)),                  # stacked K = 18 (not a multiple of 4): CUDA-core path
+])
+def test_gpu_jd_eigen_iteration(cts, r, dims, iters, shapes):
     """cts_jd_eigen_iteration vs the fp64 oracle of App A.2 on the
     same fp32 factors and the same initial bases: a batch of clusters with different sizes and
     LoRA ranks; U, V unique (QR with positive R diagonal) -> compared elementwise, Sigma per adapter."""
@@ -668,7 +672,9 @@ def test_gpu_jd_eigen_iteration(cts, r, dims, iters):
     d_in, d_out = dims
     g = np.random.default_rng(r + d_in)
     probs, refs = [], []
-    for k, (n, ri) in enumerate(((5, 16), (9, 8), (3, 16)) if d_in < 1000 else ((40, 16),)):
+    if shapes is None:
+        shapes = ((5, 16), (9, 8), (3, 16)) if d_in < 1000 else ((40, 16),)
+    for k, (n, ri) in enumerate(shapes):
         Bs, As, _ = gen_loras("trained_like", d_in, d_out, n, ri, seed=100 * k + r, n_families=2)
         Bs = [B.astype(np.float32).astype(np.float64) for B in Bs]
         As = [A.astype(np.float32).astype(np.float64) for A in As]
