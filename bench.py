@@ -419,7 +419,7 @@ def run_reference(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(steps) * 1e3,
             "full_model_step_ms_extrapolated": per_layer * cfg["layers"] * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_dict(cfg, args.gpus),
+            "data": "synthetic", "config": {k: v for k, v in config_dict(cfg, args.gpus).items() if k != "device_mode"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": oracle_cores(), "kind": "oracle",
                              "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -924,7 +924,8 @@ def run_gpu(args, cfg):
     if jd_ms is not None:
         line["config"]["bank_source"] = (f"JD-built on the GPU: one layer of planted-family rank-16 LoRAs compressed "
                                          f"by cts_jd_eigen_iteration (App A.2, 10 iterations, {len(cfg['modules'])} "
-                                         f"x {C} clusters in one call, {jd_ms:.1f} ms), the same bank in every layer")
+                                         f"x {C} clusters in one call, {jd_ms:.1f} ms including the first call's "
+                                         f"setup), the same bank in every layer")
     if world > 1:
         dist.barrier()
     if rank == 0:
