@@ -230,14 +230,41 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 constexpr int kTargetItemsPerSMMax = 4;   // sizes the split-K workspace
 
-// split-K target (tuning aid): CTS_ITEMS_PER_SM shrink work items per SM per launch
-int target_items_per_sm() {
-  static int v = [] {
-    const char* e = std::getenv("CTS_ITEMS_PER_SM");
-    return e ? std::max(1, std::min(kTargetItemsPerSMMax, std::atoi(e))) : 1;
+// Run-time tuning aids, read once from the environment.  Every default is the measured best (the
+// A/B behind each is logged in DESIGN.md section 8 and profiles/); none changes results, only how
+// the work is split, issued or launched.
+//   CTS_ITEMS_PER_SM  shrink work items per SM per launch (K split target), 1..4        default 1
+//   CTS_KS_MAX        cap on K chunks per slot, 1..16                                   default 16
+//   CTS_EXPAND_STORE  expand store path: 0 TMA scatter, 1 register-direct  default by tokens/cluster
+//   CTS_POLL_FIRST    fused: poll t-ready before issuing an item's y / out_basis loads   default idem
+//   CTS_EARLY_ITEMS   fused: items whose loads may be issued before their t is ready    default 4
+//   CTS_PACK          segment: pack two <=64-token clusters per 128-row slot (0 = off)  default 1
+//   CTS_FUSED         0: shrink and expand as two launches (no inter-CTA waits)         default 1
+struct Tuning {
+  int items_per_sm = 1, ks_max = 16, expand_store = -1, poll_first = -1, early_items = 4, pack = 1;
+  bool fused = true;
+};
+
+const Tuning& tuning() {
+  static const Tuning t = [] {
+    Tuning v;
+    auto env = [](const char* name, int dflt) {
+      const char* e = std::getenv(name);
+      return e ? std::atoi(e) : dflt;
+    };
+    v.items_per_sm = std::max(1, std::min(kTargetItemsPerSMMax, env("CTS_ITEMS_PER_SM", v.items_per_sm)));
+    v.ks_max = std::max(1, std::min(16, env("CTS_KS_MAX", v.ks_max)));
+    v.expand_store = env("CTS_EXPAND_STORE", v.expand_store);
+    v.poll_first = env("CTS_POLL_FIRST", v.poll_first);
+    v.early_items = env("CTS_EARLY_ITEMS", v.early_items);
+    v.pack = env("CTS_PACK", v.pack);
+    v.fused = env("CTS_FUSED", 1) != 0;
+    return v;
   }();
-  return v;
+  return t;
 }
+
+int target_items_per_sm() { return tuning().items_per_sm; }
 
 template <typename Kern>
 cudaError_t set_smem(Kern kernel, int bytes) {
@@ -249,46 +276,27 @@ cudaError_t set_smem(Kern kernel, int bytes) {
 // are full (bandwidth-bound prefill).  Measured on B200 (expand us per launch, decode / prefill):
 // scatter 21.4 / 150.7, direct 19.4 / 179.1 (row copies out of the stage, 23.7 / 160.9, were
 // removed: the extra shared-memory round trip cost more than the fewer store wavefronts saved).
-// CTS_EXPAND_STORE = 0 / 1 forces scatter / direct (tuning aid).
 int expand_store_mode(int T, int C) {
-  static int v = [] {
-    const char* e = std::getenv("CTS_EXPAND_STORE");
-    return e ? std::atoi(e) : -1;
-  }();
+  const int v = tuning().expand_store;
   if (v == 0 || v == 1) return v;
   return T < 96 * C ? kStoreDirect : kStoreScatter;   // mean tokens per cluster < 96
 }
 
 // fused kernel, expand producer: poll the slot's t-ready flag before (1) or after (0) issuing the
-// item's out_basis / y loads.  CTS_POLL_FIRST overrides (tuning aid).
+// item's out_basis / y loads.
 int poll_first_default(int T, int C) {
-  static int v = [] {
-    const char* e = std::getenv("CTS_POLL_FIRST");
-    return e ? std::atoi(e) : -1;
-  }();
+  const int v = tuning().poll_first;
   if (v >= 0) return v != 0;
   return T < 96 * C ? 0 : 1;
 }
 
 // fused kernel, expand producer: how many of a CTA's expand items may load y / out_basis before
 // their t is ready (the rest poll first, so their loads do not queue ahead of the split-K
-// exchange's round trips).  CTS_EARLY_ITEMS overrides (tuning aid).
-int early_items_default() {
-  static int v = [] {
-    const char* e = std::getenv("CTS_EARLY_ITEMS");
-    return e ? std::atoi(e) : 4;
-  }();
-  return v;
-}
+// exchange's round trips).
+int early_items_default() { return tuning().early_items; }
 
-// cts_apply[_group] runs the fused single-launch kernel unless CTS_FUSED=0 (tuning aid).
-bool use_fused() {
-  static bool v = [] {
-    const char* e = std::getenv("CTS_FUSED");
-    return e ? std::atoi(e) != 0 : true;
-  }();
-  return v;
-}
+// cts_apply[_group] runs the fused single-launch kernel unless CTS_FUSED=0.
+bool use_fused() { return tuning().fused; }
 
 // The fused kernel launches cooperatively unless the caller declared exclusive use of the device
 // (cts_set_exclusive_device): a cooperative launch cannot start before every CTA fits, so it loses
@@ -336,13 +344,7 @@ __nv_bfloat16* module_tbuf(cts_plan_t p, int module) {
 // SM over the slots the segment kernel produced); the host only caps them: each chunk >= 4 K
 // blocks, <= 16 chunks.  The workspace holds (target * SMs + slots) * 128 rows per module, which
 // bounds slots * ks for any slot count.
-int ks_cap(int min_kblocks) {
-  static int cap = [] {
-    const char* e = std::getenv("CTS_KS_MAX");   // tuning aid
-    return e ? std::max(1, std::min(16, std::atoi(e))) : 16;
-  }();
-  return std::max(1, std::min(cap, min_kblocks / 4));
-}
+int ks_cap(int min_kblocks) { return std::max(1, std::min(tuning().ks_max, min_kblocks / 4)); }
 
 // Segment outputs may be read before griddep_wait by every kernel but the first after cts_segment:
 // each kernel triggers its dependents only after its own griddep_wait, so when launch k starts,
@@ -1149,11 +1151,7 @@ cts_status_t cts_segment(cts_plan_t p, const int32_t* token_adapter, int32_t T, 
   a.N = b->N;
   a.C = b->C;
   a.max_tiles = p->max_tiles;
-  static const int pack = [] {
-    const char* e = std::getenv("CTS_PACK");   // tuning aid: 0 disables slot packing
-    return e ? std::atoi(e) : 1;
-  }();
-  a.pack = pack;
+  a.pack = tuning().pack;
   static const cudaError_t seg_attr = cudaFuncSetAttribute(
       segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (kSegWarps + 3) * 1024 * 4);
   CTS_CUDA(seg_attr);
