@@ -19,7 +19,7 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-__global__ void __launch_bounds__(32 * 9, 1) gather_kernel(const __grid_constant__ CUtensorMap tm, const int* rows,
+__global__ void __launch_bounds__(32 * 13, 1) gather_kernel(const __grid_constant__ CUtensorMap tm, const int* rows,
                                                           int n_rows_src, int W, int box_bytes, int stages,
                                                           int jobs_per_cta, int tile_mode, const __nv_bfloat16* gsrc, unsigned long long* sink) {
   extern __shared__ uint8_t raw[];
@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(32 * 9, 1) gather_kernel(const __grid_constant
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { mbar_init(&full[s], tile_mode == 2 ? 32 : 1); mbar_init(&empty[s], 1); }
+    // tile_mode 3: one warp produces a whole stage with plain 32-byte loads (full count 1)
     fence_barrier_init();
   }
   __syncthreads();
@@ -38,11 +39,36 @@ __global__ void __launch_bounds__(32 * 9, 1) gather_kernel(const __grid_constant
       const int stage = j % stages;
       const uint32_t phase = (j / stages) & 1;
       mbar_wait(&empty[stage], phase ^ 1);
-      if (tile_mode != 2 && lane == 0) mbar_arrive_expect_tx(&full[stage], stage_bytes);
+      if (tile_mode < 2 && lane == 0) mbar_arrive_expect_tx(&full[stage], stage_bytes);
       __syncwarp();
       uint8_t* dst = smem + stage * stage_bytes;
       const int base = ((blockIdx.x * 7919 + j * 131) % (n_rows_src / 128)) * 128;
-      if (tile_mode == 2) {
+      if (tile_mode == 3) {
+        // plain loads into registers: 4 lanes per 128-byte row segment (ld.global.v8, 32 B each),
+        // 8 rows per instruction, 8 instructions in flight, then 16-byte stores at the 128B-swizzled
+        // offsets; one arrival per stage
+        const int sub = lane & 3, r8 = lane >> 2;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          uint4 v[8][2];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int rr = h * 64 + u * 8 + r8;
+            const int row = rows[base + rr];
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(gsrc) + (static_cast<size_t>(row) * 4096) * 2 + sub * 32;
+            ld_global_nc_v8(src, v[u][0], v[u][1]);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int rr = h * 64 + u * 8 + r8;
+            *reinterpret_cast<uint4*>(dst + rr * 128 + (((2 * sub) ^ (rr & 7)) * 16)) = v[u][0];
+            *reinterpret_cast<uint4*>(dst + rr * 128 + (((2 * sub + 1) ^ (rr & 7)) * 16)) = v[u][1];
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+      } else if (tile_mode == 2) {
         // cp.async (LDGSTS) 16-byte pieces of the same 128 random rows x box_bytes, each placed at
         // its 128B-swizzled offset (as an MMA A tile would need); completion via the mbarrier
         const int chunks_per_row = box_bytes / 16;
@@ -101,7 +127,8 @@ int main() {
                     {"gather4 256col noswz (2KB/op)", 256, CU_TENSOR_MAP_SWIZZLE_NONE, 0},
                     {"tile 64colx128row SW128 (16KB/op)", 64, CU_TENSOR_MAP_SWIZZLE_128B, 1},
                     {"cp.async 16B x 128 rows x 128B", 64, CU_TENSOR_MAP_SWIZZLE_128B, 2},
-                    {"cp.async 16B x 128 rows x 256B", 128, CU_TENSOR_MAP_SWIZZLE_NONE, 2}};
+                    {"cp.async 16B x 128 rows x 256B", 128, CU_TENSOR_MAP_SWIZZLE_NONE, 2},
+                    {"ldg 32B x 4 lanes per 128B row", 64, CU_TENSOR_MAP_SWIZZLE_128B, 3}};
     for (const Mode& m : modes) {
       CUtensorMap tm;
       cuuint64_t dims[2] = {cuuint64_t(COLS), cuuint64_t(src_rows)};
@@ -117,8 +144,9 @@ int main() {
       const int stages = std::max(2, (200 * 1024) / stage_bytes);
       const int smem = stages * stage_bytes + 1024 + 2 * stages * 8 + 64;
       cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      for (int W : {1, 2, 3, 4, 6}) {
-        if (2 * W > stages) continue;
+      for (int W : {1, 2, 3, 4, 6, 8, 12}) {
+        if (m.tile != 3 && W > 6) continue;
+        if (m.tile == 3 ? W + 2 > stages : 2 * W > stages) continue;
         const long long total_bytes = (src_rows == 4096 ? 4LL : 8LL) << 30;
         const int jobs = int(total_bytes / stage_bytes / sms);
         cudaEvent_t a, b;
