@@ -436,6 +436,7 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&R.empty[stage]);
+    if (warp == kEpiWarp0 && lane == 0 && my < 4) CTS_STAMP(20 + my);   // trace: item my's epilogue done
   }
   if (STORE == kStoreScatter) bulk_wait0();     // this warp's global writes complete before exit
 }

@@ -52,6 +52,48 @@ def run(tag, mods, N, C, r, T, prefill=False, groups=None):
     print(f"{tag}: ok", flush=True)
 
 
+def run_diag_and_pagein():
+    """JD-Diag bank (CTS_SIGMA_DIAG) through the fused and split paths, then a slot page-in."""
+    mods = [(1024, 512), (1024, 256)]
+    banks = [direct_bank_torch(di, do, 200, 8, 16, seed=m, device=dev, cluster_seed=50 + m)
+             for m, (di, do) in enumerate(mods)]
+    bank = cts.Bank([b["in_basis"] for b in banks], [b["out_basis"] for b in banks],
+                    [torch.diagonal(b["sigma"], dim1=1, dim2=2).contiguous() for b in banks],
+                    [b["cluster_of"] for b in banks])
+    plan = cts.Plan(bank, 300)
+    plan.segment(tokens_torch(300, 200, 3, False, dev))
+    x = torch.randn(300, 1024, device=dev).to(torch.bfloat16)
+    ys = [torch.randn(300, do, device=dev).to(torch.bfloat16) for (_, do) in mods]
+    plan.apply_group([0, 1], [x, x], ys, 2.0)
+    plan.shrink_group([0, 1], [x, x], 2.0)
+    plan.expand_group([0, 1], ys)
+    torch.cuda.synchronize()
+    bank.write_clusters(1, [2, 5], banks[1]["in_basis"][:2].contiguous(), banks[1]["out_basis"][:2].contiguous())
+    plan.apply_group([0, 1], [x, x], ys, 2.0)
+    torch.cuda.synchronize()
+    plan.close()
+    bank.close()
+    print("diag bank + page-in: ok", flush=True)
+
+
+def run_jd():
+    """GPU compression: tensor-core path (K multiple of 4) and CUDA-core fallback in one batch each."""
+    g = torch.Generator(device=dev).manual_seed(0)
+    for (n, ri) in ((6, 16), (3, 6)):
+        d_in, d_out = 256, 192
+        prob = {"a_stack": torch.randn(n * ri, d_in, generator=g, device=dev) / 16,
+                "bt_stack": torch.randn(n * ri, d_out, generator=g, device=dev) / 4,
+                "U": torch.linalg.qr(torch.randn(d_out, 16, generator=g, device=dev))[0].contiguous(),
+                "V": torch.linalg.qr(torch.randn(d_in, 16, generator=g, device=dev))[0].contiguous(),
+                "sigma": torch.empty(n, 16, 16, device=dev)}
+        ws = cts.cts_jd_eigen_iteration([prob], 16, 3)
+        torch.cuda.synchronize()
+        del ws
+    print("GPU compression (tensor-core + CUDA-core paths): ok", flush=True)
+
+
+run_diag_and_pagein()
+run_jd()
 run("tiny r=4 (r_pad 16)", [(64, 64)], N=4, C=1, r=4, T=32)
 run("decode-like r=16, 3 modules grouped", [(1024, 1024), (1024, 256), (1024, 256)], N=100, C=5, r=16, T=200,
     groups=[[0, 1, 2]])

@@ -31,8 +31,8 @@ names = {0: "start", 1: "prologue+wait", 2: "shrink first TMA", 3: "shrink produ
          9: "expand producers done", 10: "expand epi done", 11: "end",
          12: "finisher: last arrival", 13: "finisher: partials summed", 14: "finisher: t stored",
          15: "finisher: flag published", 16: "shrink: first item mapped", 17: "shrink: expect_tx armed",
-         18: "shrink: first gathers issued", 19: "shrink: first acc ready", 20: "-",
-         21: "-", 22: "-"}
+         18: "shrink: first gathers issued", 19: "shrink: first acc ready", 20: "expand item 0 epi done",
+         21: "expand item 1 epi done", 22: "expand item 2 epi done", 23: "expand item 3 epi done"}
 for grp in (([0],) if os.environ.get("QONLY") else ([0, 1, 2], [3, 4])):
     for rep in range(3):
         big.zero_()
