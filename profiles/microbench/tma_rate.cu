@@ -21,7 +21,7 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 
 __global__ void __launch_bounds__(32 * 13, 1) gather_kernel(const __grid_constant__ CUtensorMap tm, const int* rows,
                                                           int n_rows_src, int W, int box_bytes, int stages,
-                                                          int jobs_per_cta, int tile_mode, const __nv_bfloat16* gsrc, unsigned long long* sink) {
+                                                          int jobs_per_cta, int tile_mode, const __nv_bfloat16* gsrc, unsigned long long* sink, int pat) {
   extern __shared__ uint8_t raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   const int stage_bytes = 128 * box_bytes;
@@ -42,7 +42,14 @@ __global__ void __launch_bounds__(32 * 13, 1) gather_kernel(const __grid_constan
       if (tile_mode < 2 && lane == 0) mbar_arrive_expect_tx(&full[stage], stage_bytes);
       __syncwarp();
       uint8_t* dst = smem + stage * stage_bytes;
-      const int base = ((blockIdx.x * 7919 + j * 131) % (n_rows_src / 128)) * 128;
+      // pat 1 (the decode shrink's order): the same 128 rows for 21 consecutive column blocks
+      const int jj = pat ? j / 21 : j;
+      const int base = ((blockIdx.x * 7919 + jj * 131) % (n_rows_src / 128)) * 128;
+      // DRAM-sized source: also walk the column blocks, so the touched footprint is the whole
+      // source (round-2 session 3 fix: with column 0 only, a "DRAM" run touched 32-64 MB = L2)
+      const int ncb = 4096 / (box_bytes / 2);
+      const int col = n_rows_src <= 4096 ? 0
+                      : (pat ? ((j % 21) + 21 * (jj % 3)) % ncb : (blockIdx.x * 7 + j * 13) % ncb) * (box_bytes / 2);
       if (tile_mode == 3) {
         // plain loads into registers: 4 lanes per 128-byte row segment (ld.global.v8, 32 B each),
         // 8 rows per instruction, 8 instructions in flight, then 16-byte stores at the 128B-swizzled
@@ -55,7 +62,7 @@ __global__ void __launch_bounds__(32 * 13, 1) gather_kernel(const __grid_constan
           for (int u = 0; u < 8; ++u) {
             const int rr = h * 64 + u * 8 + r8;
             const int row = rows[base + rr];
-            const uint8_t* src = reinterpret_cast<const uint8_t*>(gsrc) + (static_cast<size_t>(row) * 4096) * 2 + sub * 32;
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(gsrc) + (static_cast<size_t>(row) * 4096 + col) * 2 + sub * 32;
             ld_global_nc_v8(src, v[u][0], v[u][1]);
           }
 #pragma unroll
@@ -75,16 +82,16 @@ __global__ void __launch_bounds__(32 * 13, 1) gather_kernel(const __grid_constan
         for (int i = lane; i < 128 * chunks_per_row; i += 32) {
           const int rr = i / chunks_per_row, ch = i % chunks_per_row;
           const int row = rows[base + rr];
-          const uint8_t* src = reinterpret_cast<const uint8_t*>(gsrc) + (static_cast<size_t>(row) * 4096) * 2 + ch * 16;
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(gsrc) + (static_cast<size_t>(row) * 4096 + col) * 2 + ch * 16;
           const int off = rr * box_bytes + ((ch ^ (rr & 7)) * 16);
           cp_async16(dst + off, src);
         }
         cp_async_mbar_arrive(&full[stage]);
       } else if (tile_mode) {
-        if (lane == 0) tma_load_2d(dst, &tm, &full[stage], 0, base);
+        if (lane == 0) tma_load_2d(dst, &tm, &full[stage], col, base);
       } else {
         const int4 r = *reinterpret_cast<const int4*>(rows + base + 4 * lane);
-        tma_gather4(dst + lane * 4 * box_bytes, &tm, &full[stage], 0, r.x, r.y, r.z, r.w);
+        tma_gather4(dst + lane * 4 * box_bytes, &tm, &full[stage], col, r.x, r.y, r.z, r.w);
       }
     }
   } else if (warp == W) {
@@ -108,6 +115,7 @@ int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int COLS = 4096;
+  const int pat = getenv("PAT") ? atoi(getenv("PAT")) : 0;
   for (long long src_rows : {4096LL, 262144LL}) {          // 32 MB (L2) / 2 GB (DRAM)
     __nv_bfloat16* x = nullptr;
     cudaMalloc(&x, src_rows * COLS * 2);
@@ -145,21 +153,21 @@ int main() {
       const int smem = stages * stage_bytes + 1024 + 2 * stages * 8 + 64;
       cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       for (int W : {1, 2, 3, 4, 6, 8, 12}) {
-        if (m.tile != 3 && W > 6) continue;
+        if (m.tile != 3 && W > 8) continue;
         if (m.tile == 3 ? W + 2 > stages : 2 * W > stages) continue;
         const long long total_bytes = (src_rows == 4096 ? 4LL : 8LL) << 30;
         const int jobs = int(total_bytes / stage_bytes / sms);
         cudaEvent_t a, b;
         cudaEventCreate(&a); cudaEventCreate(&b);
-        gather_kernel<<<sms, 32 * (W + 1), smem>>>(tm, rows, int(src_rows), W, box_bytes, stages, 4, m.tile, x, sink);
+        gather_kernel<<<sms, 32 * (W + 1), smem>>>(tm, rows, int(src_rows), W, box_bytes, stages, 4, m.tile, x, sink, pat);
         cudaEventRecord(a);
-        gather_kernel<<<sms, 32 * (W + 1), smem>>>(tm, rows, int(src_rows), W, box_bytes, stages, jobs, m.tile, x, sink);
+        gather_kernel<<<sms, 32 * (W + 1), smem>>>(tm, rows, int(src_rows), W, box_bytes, stages, jobs, m.tile, x, sink, pat);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms = 0;
         cudaEventElapsedTime(&ms, a, b);
         const double bytes = double(jobs) * stage_bytes * sms;
-        printf("%-36s src=%s W=%d stages=%d: %8.1f GB/s total, %6.1f GB/s per SM  (%s)\n", m.name,
+        printf("pat%d %-36s src=%s W=%d stages=%d: %8.1f GB/s total, %6.1f GB/s per SM  (%s)\n", pat, m.name,
                src_rows == 4096 ? "L2  " : "DRAM", W, stages, bytes / ms / 1e6, bytes / ms / 1e6 / sms,
                cudaGetErrorString(cudaGetLastError()));
       }
