@@ -21,6 +21,7 @@
 #include "proj_fused.cuh"
 #include "jd_eigen.cuh"
 #include "jd_tc.cuh"
+#include "jd_gram.cuh"
 #include "segment.cuh"
 #include "shrink_sigma.cuh"
 
@@ -240,9 +241,14 @@ constexpr int kTargetItemsPerSMMax = 4;   // sizes the split-K workspace
 //   CTS_EARLY_ITEMS   fused: items whose loads may be issued before their t is ready    default 4
 //   CTS_PACK          segment: pack two <=64-token clusters per 128-row slot (0 = off)  default 1
 //   CTS_FUSED         0: shrink and expand as two launches (no inter-CTA waits)         default 1
+//   CTS_JD_KSPACE     0: GPU compression iterates in the d-space only (no K-space Grams) default 1
+//   CTS_JD_KS_RECOMPUTE  K-space Cholesky-QR2: 1 = second pass recomputes G C, 0 = reuses Y R1^-1  default 0
+//                     (the last iteration is always the d-space Cholesky-QR2, so the result is orthonormal)
 struct Tuning {
   int items_per_sm = 1, ks_max = 16, expand_store = -1, poll_first = -1, early_items = 4, pack = 1;
   bool fused = true;
+  bool jd_kspace = true;
+  bool jd_ks_recompute = false;
 };
 
 const Tuning& tuning() {
@@ -259,6 +265,8 @@ const Tuning& tuning() {
     v.early_items = env("CTS_EARLY_ITEMS", v.early_items);
     v.pack = env("CTS_PACK", v.pack);
     v.fused = env("CTS_FUSED", 1) != 0;
+    v.jd_kspace = env("CTS_JD_KSPACE", 1) != 0;
+    v.jd_ks_recompute = env("CTS_JD_KS_RECOMPUTE", 0) != 0;
     return v;
   }();
   return t;
@@ -616,6 +624,12 @@ bool jd_tc_ok(const cts_jd_problem_t& q, int r) {
          reinterpret_cast<uintptr_t>(q.bt_stack) % 16 == 0;
 }
 
+// K-space path (jd_gram.cuh): tensor-core shapes, 2r <= K <= kJdGramMaxK, r = 16 or 32
+bool jd_gram_ok(const cts_jd_problem_t& q, int r) {
+  const int K = q.n * q.r_i;
+  return jd_tc_ok(q, r) && (r == 16 || r == 32) && K >= 2 * r && K <= kJdGramMaxK;
+}
+
 size_t jd_problem_floats(const cts_jd_problem_t& q, int r) {
   const size_t K = size_t(q.n) * q.r_i;
   const size_t gb = (size_t(q.d_in) + 255) / 256 + (size_t(q.d_out) + 255) / 256;
@@ -624,23 +638,25 @@ size_t jd_problem_floats(const cts_jd_problem_t& q, int r) {
   size_t f = 4 * K * r + size_t(q.d_in + q.d_out) * r + gb * r * r + part + 64;   // + Gram, segment partials
   if (jd_tc_ok(q, r))   // A^T, Bt^T, V^T, U^T, W^T, Z^T (K-major operands of the tensor-core GEMMs)
     f += K * size_t(q.d_in + q.d_out) + size_t(r) * (q.d_in + q.d_out + 2 * K) + 64;
+  if (jd_gram_ok(q, r)) f += 2 * K * K + 2 * K * size_t(r) + 64;   // G_A, G_B, Y_A, Y_B
   return f;
 }
 
 // One batch's tensor-core tables (maps, jobs, tile lists, transpose jobs) in one device block.
+// Groups 0-3: the thin GEMMs; group 4 (K-space path only): the Grams G_A = A A^T, G_B = Bt Bt^T.
 struct JdTcTables {
   std::vector<uint8_t> host;
   void* dev = nullptr;
-  size_t off_jobs[4] = {}, off_tiles[4] = {}, off_tr[3] = {};
-  int n_tiles[4] = {}, n_tr[3] = {};
+  size_t off_jobs[5] = {}, off_tiles[5] = {}, off_tr[3] = {};
+  int n_tiles[5] = {}, n_tr[3] = {};
 };
 
 template <int R>
-cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, JdTcTables& T, cudaStream_t stream) {
+cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, bool gram, JdTcTables& T, cudaStream_t stream) {
   const int n = jb.count;
   // per problem: maps 0..7 = X: A, Bt, A^T, Bt^T; Y: V^T, U^T, W^T, Z^T
   std::vector<CUtensorMap> maps(size_t(n) * 8);
-  std::vector<int2> tiles[4];
+  std::vector<int4> tiles[5];
   std::vector<JdTransposeJob> tr[3];
   for (int i = 0; i < n; ++i) {
     const JdProblem& p = jb.pr[i];
@@ -658,10 +674,15 @@ cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, JdTcTables&
         !make_tmap_f32(&m[6], wt, K, R, 32, R) || !make_tmap_f32(&m[7], zt, K, R, 32, R))
       return CTS_ERR_CUDA;
     const int rowsP = (K + 127) / 128, rowsU = (p.d_out + 127) / 128, rowsV = (p.d_in + 127) / 128;
-    for (int t = 0; t < rowsP; ++t) tiles[0].push_back(make_int2(i, t * 128));   // P = A V
-    for (int t = 0; t < rowsP; ++t) tiles[1].push_back(make_int2(i, t * 128));   // Q = Bt U
-    for (int t = 0; t < rowsU; ++t) tiles[2].push_back(make_int2(i, t * 128));   // U0 = Bt^T W
-    for (int t = 0; t < rowsV; ++t) tiles[3].push_back(make_int2(i, t * 128));   // V0 = A^T Z
+    for (int t = 0; t < rowsP; ++t) tiles[0].push_back(make_int4(i, t * 128, 0, 0));   // P = A V
+    for (int t = 0; t < rowsP; ++t) tiles[1].push_back(make_int4(i, t * 128, 0, 0));   // Q = Bt U
+    for (int t = 0; t < rowsU; ++t) tiles[2].push_back(make_int4(i, t * 128, 0, 0));   // U0 = Bt^T W
+    for (int t = 0; t < rowsV; ++t) tiles[3].push_back(make_int4(i, t * 128, 0, 0));   // V0 = A^T Z
+    if (gram)                                                                          // G_A, G_B tiles
+      for (int side = 0; side < 2; ++side)
+        for (int a = 0; a < rowsP; ++a)
+          for (int c = a; c < rowsP; ++c)   // G symmetric: upper tiles, each off-diagonal one mirrored
+            tiles[4].push_back(make_int4(2 * i + side, a * 128, c * 128, c > a ? 1 : 0));
     tr[0].push_back({p.a, at, K, p.d_in});
     tr[0].push_back({p.bt, btt, K, p.d_out});
     tr[1].push_back({p.V, vt, p.d_in, R});
@@ -671,11 +692,11 @@ cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, JdTcTables&
   }
   auto al = [](size_t v) { return (v + 127) / 128 * 128; };
   size_t off = al(maps.size() * sizeof(CUtensorMap));
-  for (int g = 0; g < 4; ++g) { T.off_jobs[g] = off; off = al(off + size_t(n) * sizeof(JdTcJob)); }
-  for (int g = 0; g < 4; ++g) {
+  for (int g = 0; g < 5; ++g) { T.off_jobs[g] = off; off = al(off + size_t(g == 4 ? 2 * n : n) * sizeof(JdTcJob)); }
+  for (int g = 0; g < 5; ++g) {
     T.off_tiles[g] = off;
     T.n_tiles[g] = int(tiles[g].size());
-    off = al(off + tiles[g].size() * sizeof(int2));
+    off = al(off + tiles[g].size() * sizeof(int4));
   }
   for (int g = 0; g < 3; ++g) {
     if (tr[g].size() > size_t(kJdMaxTranspose)) return CTS_ERR_SHAPE;
@@ -691,11 +712,15 @@ cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, JdTcTables&
     const JdProblem& p = jb.pr[i];
     const int K = p.n * p.ri;
     const CUtensorMap* m = dmaps + size_t(i) * 8;
-    const JdTcJob jobs[4] = {{m + 0, m + 4, p.P, K, p.d_in}, {m + 1, m + 5, p.Q, K, p.d_out},
-                             {m + 3, m + 6, p.U0, p.d_out, K}, {m + 2, m + 7, p.V0, p.d_in, K}};
+    const JdTcJob jobs[4] = {{m + 0, m + 4, p.P, K, p.d_in, R, R}, {m + 1, m + 5, p.Q, K, p.d_out, R, R},
+                             {m + 3, m + 6, p.U0, p.d_out, K, R, R}, {m + 2, m + 7, p.V0, p.d_in, K, R, R}};
     for (int g = 0; g < 4; ++g) std::memcpy(T.host.data() + T.off_jobs[g] + i * sizeof(JdTcJob), &jobs[g], sizeof(JdTcJob));
+    if (gram) {   // X = Y = the stack (box {32, 128} serves both operands)
+      const JdTcJob gj[2] = {{m + 0, m + 0, p.Ga, K, p.d_in, K, K}, {m + 1, m + 1, p.Gb, K, p.d_out, K, K}};
+      std::memcpy(T.host.data() + T.off_jobs[4] + 2 * i * sizeof(JdTcJob), gj, sizeof(gj));
+    }
   }
-  for (int g = 0; g < 4; ++g) std::memcpy(T.host.data() + T.off_tiles[g], tiles[g].data(), tiles[g].size() * sizeof(int2));
+  for (int g = 0; g < 5; ++g) std::memcpy(T.host.data() + T.off_tiles[g], tiles[g].data(), tiles[g].size() * sizeof(int4));
   for (int g = 0; g < 3; ++g) std::memcpy(T.host.data() + T.off_tr[g], tr[g].data(), tr[g].size() * sizeof(JdTransposeJob));
   if (cudaMemcpyAsync(T.dev, T.host.data(), off, cudaMemcpyHostToDevice, stream) != cudaSuccess) return CTS_ERR_CUDA;
   return CTS_OK;
@@ -713,7 +738,7 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
     JdBatch& jb = *jbp;
     jb.count = std::min(kJdMaxBatch, count - b0);
     int kmax = 1, dmax = 1, nmax = 1, rimax = 1;
-    bool tc = true;
+    bool tc = true, gram = true;
     float* tc_base[kJdMaxBatch];
     for (int i = 0; i < jb.count; ++i) {
       const cts_jd_problem_t& q = problems[b0 + i];
@@ -734,7 +759,16 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
       w += std::max((size_t(std::max(q.d_in, q.d_out)) + kJdSeg - 1) / kJdSeg * K,
                     (K + kJdKSeg - 1) / kJdKSeg * size_t(std::max(q.d_in, q.d_out))) * R;
       tc_base[i] = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(w) + 255) & ~uintptr_t(255));
+      p.Ga = p.Gb = p.Ya = p.Yb = nullptr;
+      if (jd_gram_ok(q, R)) {
+        float* g0 = tc_base[i] + K * size_t(q.d_in + q.d_out) + size_t(R) * (q.d_in + q.d_out + 2 * K);
+        p.Ga = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(g0) + 255) & ~uintptr_t(255));
+        p.Gb = p.Ga + K * K;
+        p.Ya = p.Gb + K * K;
+        p.Yb = p.Ya + K * R;
+      }
       tc = tc && jd_tc_ok(q, R);
+      gram = gram && jd_gram_ok(q, R);
       ws += jd_problem_floats(q, R);
       kmax = std::max<int>(kmax, int(K));
       dmax = std::max({dmax, q.d_in, q.d_out});
@@ -752,7 +786,8 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
     if constexpr (R >= 16) {
       if (tc) {                          // tensor-core thin GEMMs (jd_tc.cuh); same orthogonalization
         JdTcTables T;
-        cts_status_t st = jd_tc_prepare<R>(jb, tc_base, T, stream);
+        gram = gram && iters >= 2 && tuning().jd_kspace;
+        cts_status_t st = jd_tc_prepare<R>(jb, tc_base, gram, T, stream);
         if (st != CTS_OK) return st;
         static const cudaError_t attr_tc = set_smem(jd_tc_gemm<R>, JdTcCfg<R>::kBytes);
         CTS_CUDA(attr_tc);
@@ -760,7 +795,7 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
         auto gemm = [&](int g) {
           JdTcParams prm;
           prm.jobs = reinterpret_cast<const JdTcJob*>(dv + T.off_jobs[g]);
-          prm.tiles = reinterpret_cast<const int2*>(dv + T.off_tiles[g]);
+          prm.tiles = reinterpret_cast<const int4*>(dv + T.off_tiles[g]);
           prm.n_tiles = T.n_tiles[g];
           jd_tc_gemm<R><<<std::min(sm_count(), std::max(1, T.n_tiles[g])), 320, JdTcCfg<R>::kBytes, stream>>>(prm);
         };
@@ -770,9 +805,40 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
         };
         transpose(0);                     // A^T, Bt^T (once)
         transpose(1);                     // V^T, U^T of the initial bases
-        for (int it = 0; it < iters; ++it) {
-          gemm(0);                        // P = A V
-          gemm(1);                        // Q = Bt U
+        int it0 = 0;
+        if constexpr (R == 16 || R == 32) {
+          if (gram) {                     // iterations 0 .. iters-2 in the K-space (jd_gram.cuh)
+            static const cudaError_t attr_g = set_smem(jd_tc_gemm<128>, JdTcCfg<128>::kBytes);
+            CTS_CUDA(attr_g);
+            gemm(0);
+            gemm(1);
+            JdTcParams gp;
+            gp.jobs = reinterpret_cast<const JdTcJob*>(dv + T.off_jobs[4]);
+            gp.tiles = reinterpret_cast<const int4*>(dv + T.off_tiles[4]);
+            gp.n_tiles = T.n_tiles[4];
+            jd_tc_gemm<128><<<std::min(sm_count(), std::max(1, T.n_tiles[4])), 320, JdTcCfg<128>::kBytes, stream>>>(gp);
+            const dim3 g_gm((kmax + JdGm<R>::kRows - 1) / JdGm<R>::kRows, 2, jb.count), g_go(2, jb.count);
+            for (; it0 < iters - 1; ++it0) {
+              jd_small<R><<<g_small, 256, small_smem, stream>>>(jb);
+              for (int pass = 0; pass < 2; ++pass) {
+                if (pass == 0 || tuning().jd_ks_recompute) {   // pass 2: G C recomputed, or Y R1^-1 reused
+                  jd_gmul<R><<<g_gm, 256, 0, stream>>>(jb);
+                  g_launches.fetch_add(1, std::memory_order_relaxed);
+                }
+                jd_gorth<R><<<g_go, 256, 0, stream>>>(jb, pass);
+              }
+              g_launches.fetch_add(3, std::memory_order_relaxed);
+            }
+            g_launches.fetch_add(3, std::memory_order_relaxed);
+          }
+        }
+        for (int it = it0; it < iters; ++it) {
+          if (it > it0 || it0 == 0) {     // (the K-space iterations leave P, Q of the current iterate)
+            gemm(0);                      // P = A V
+            gemm(1);                      // Q = Bt U
+          } else {
+            g_launches.fetch_sub(2, std::memory_order_relaxed);
+          }
           jd_small<R><<<g_small, 256, small_smem, stream>>>(jb);
           transpose(2);                   // W^T, Z^T
           gemm(2);                        // U0 = Bt^T W

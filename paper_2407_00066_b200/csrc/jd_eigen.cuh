@@ -20,7 +20,7 @@
 
 namespace cts {
 
-constexpr int kJdMaxBatch = 240;   // problems per launch (kernel parameter space: 240 x 128 B)
+constexpr int kJdMaxBatch = 200;   // problems per launch (kernel parameter space: 200 x 160 B)
 
 struct JdProblem {
   const float* a;        // A_stack [n*r_i][d_in]
@@ -37,6 +37,10 @@ struct JdProblem {
   float* part;           // partials: [ceil(d/1024)][n*r_i][R] of P / Q, [ceil(n*r_i/128)][d][R] of U0 / V0
   float* Gu;             // [ceil(d_out/256)][R][R] partial Gram matrices; slot 0 then holds R^-1
   float* Gv;             // [ceil(d_in/256)][R][R]
+  float* Ga;             // K-space path (jd_gram.cuh): G_A = A_stack A_stack^T [K][K]
+  float* Gb;             // G_B = Bt_stack Bt_stack^T [K][K]
+  float* Ya;             // [K][R] G_A C_V
+  float* Yb;             // [K][R] G_B C_U
   int n, ri, d_in, d_out;
 };
 

@@ -1,0 +1,223 @@
+// jd_gram.cuh -- the App A.2 eigenvalue iteration (jd_eigen.cuh) carried in the stacked-factor
+// ("Gram") space, so a call streams the fp32 LoRA factors a fixed number of times instead of four
+// times per iteration.
+//
+// The paper's iteration with the factors stacked, A = [A_1; ..; A_n] (K x d_in),
+// Bt = [B_1^T; ..; B_n^T] (K x d_out), K = n r_i:
+//     P = A V, Q = Bt U;  W_i = P_i (P_i^T Q_i), Z_i = Q_i (Q_i^T P_i)        (jd_small)
+//     U' = orthogonalize(Bt^T W),  V' = orthogonalize(A^T Z)
+// orthogonalize = the Q of a QR with a positive R diagonal = X R^-1 with R^T R = X^T X (Cholesky).
+// For X = A^T Z:  X^T X = Z^T (A A^T) Z,  so with G_A = A A^T (K x K) and R from chol(Z^T G_A Z):
+//     V' = A^T C_V,  C_V = Z R^-1,  and the next  P' = A V' = G_A C_V.
+// The same holds for U' with G_B = Bt Bt^T and C_U = W R_U^-1, Q' = G_B C_U.  So after ONE pass
+// that forms G_A and G_B on the tensor cores (jd_tc_gemm<128>, 3xTF32), every further iteration is
+// K x K x r work on data that never leaves L2-sized buffers; only the last iteration returns to the
+// d-space (explicit U0 = Bt^T W, V0 = A^T Z, Cholesky-QR2 with the collapse completion, then P, Q and
+// Sigma) -- the same iterates in exact arithmetic, a different rounding.  As in the d-space path the
+// orthogonalization is applied twice (Cholesky-QR2: the second pass recomputes G C from the updated
+// C), with the r x r Gram and its Cholesky in fp64.
+//
+// Used when every problem of a batch has 2r <= K <= kJdGramMaxK (cts.cu jd_gram_ok): below 2r a
+// cluster's span can collapse (the d-space path completes it with standard basis vectors, which
+// cannot be expressed in the K-space), above kJdGramMaxK the K x K Grams outgrow their purpose.
+#pragma once
+#include <cstdint>
+#include "jd_eigen.cuh"
+
+namespace cts {
+
+constexpr int kJdGramMaxK = 1024;
+
+// Y[K][R] = G[K][K] C[K][R] for side s (blockIdx.y: 0 = A side (G_A, C = Z), 1 = B side (G_B,
+// C = W)); blockIdx.z = problem.  Thread = 4 rows x 4 columns (16 FMAs per two 16-byte shared
+// loads).  G is symmetric, so the block's [K chunk][rows] operand is read straight from the rows
+// k of G (coalesced), no transpose; the next chunk is held in registers while the current one is
+// multiplied.
+template <int R>
+struct JdGm {
+  static constexpr int kCG = R / 4;                 // column groups
+  static constexpr int kRG = 256 / kCG;             // row groups
+  static constexpr int kRows = 4 * kRG;             // rows per block: 256 (R = 16) / 128 (R = 32)
+  static constexpr int kK = 32;                     // K chunk
+  static constexpr int kG4 = kK * kRows / 4 / 256;  // float4 of G per thread per chunk
+  static constexpr int kC4 = kK * R / 4;            // float4 of C per chunk
+};
+
+template <int R>
+__global__ void __launch_bounds__(256) jd_gmul(const __grid_constant__ JdBatch b) {
+  using L = JdGm<R>;
+  const JdProblem& p = b.pr[blockIdx.z];
+  const int K = p.n * p.ri;
+  const int row0 = blockIdx.x * L::kRows;
+  if (row0 >= K) return;
+  const float* G = blockIdx.y == 0 ? p.Ga : p.Gb;
+  const float* C = blockIdx.y == 0 ? p.Z : p.W;
+  float* Y = blockIdx.y == 0 ? p.Ya : p.Yb;
+  __shared__ float4 Gs[L::kK][L::kRows / 4];       // Gs[k][r] = G[k0 + k][row0 + r]
+  __shared__ float4 Cs[L::kK][R / 4];
+  const int cg = threadIdx.x % L::kCG, rg = threadIdx.x / L::kCG;
+  float4 gr[L::kG4], cr[(L::kC4 + 255) / 256];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int j = 0; j < L::kG4; ++j) {
+      const int e = threadIdx.x + 256 * j, k = e / (L::kRows / 4), r = 4 * (e % (L::kRows / 4));
+      gr[j] = (k0 + k < K && row0 + r < K) ? *reinterpret_cast<const float4*>(G + static_cast<size_t>(k0 + k) * K + row0 + r)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < (L::kC4 + 255) / 256; ++j) {
+      const int e = threadIdx.x + 256 * j, k = e / (R / 4);
+      cr[j] = (e < L::kC4 && k0 + k < K) ? reinterpret_cast<const float4*>(C + static_cast<size_t>(k0) * R)[e]
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+  load(0);
+  for (int k0 = 0; k0 < K; k0 += L::kK) {
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < L::kG4; ++j) {
+      const int e = threadIdx.x + 256 * j;
+      Gs[e / (L::kRows / 4)][e % (L::kRows / 4)] = gr[j];
+    }
+#pragma unroll
+    for (int j = 0; j < (L::kC4 + 255) / 256; ++j) {
+      const int e = threadIdx.x + 256 * j;
+      if (e < L::kC4) Cs[e / (R / 4)][e % (R / 4)] = cr[j];
+    }
+    __syncthreads();
+    if (k0 + L::kK < K) load(k0 + L::kK);           // next chunk in flight during the FMAs
+#pragma unroll 8
+    for (int k = 0; k < L::kK; ++k) {
+      const float4 g = Gs[k][rg], c = Cs[k][cg];
+      const float gv[4] = {g.x, g.y, g.z, g.w}, cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] = fmaf(gv[i], cv[q], acc[i][q]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = row0 + 4 * rg + i;
+    if (row < K)
+      reinterpret_cast<float4*>(Y + static_cast<size_t>(row) * R)[cg] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+  }
+}
+
+// One Cholesky-QR pass in the K-space for side s (blockIdx.x), problem blockIdx.y:
+//     M = C^T Y (= X^T X of the implicit X = A^T C), M = L L^T (fp64), Rinv = (L^T)^-1,
+//     C <- C Rinv,  Y <- Y Rinv  (written to P / Q on the last pass: P = G_A C_V = A V').
+// A pivot below kJdCollapse of its diagonal (a collapsed direction; not expected for K >= 2r) keeps
+// the column finite (pivot clamped to its diagonal); the final d-space Cholesky-QR2 re-orthogonalizes.
+template <int R>
+__global__ void __launch_bounds__(256, 2) jd_gorth(const __grid_constant__ JdBatch b, int last) {
+  const JdProblem& p = b.pr[blockIdx.y];
+  const int K = p.n * p.ri;
+  const int side = blockIdx.x;
+  float* C = side == 0 ? p.Z : p.W;
+  const float* Y = side == 0 ? p.Ya : p.Yb;
+  float* Yout = last ? (side == 0 ? p.P : p.Q) : (side == 0 ? p.Ya : p.Yb);
+  constexpr int kE = R * R / 256;                  // M entries per thread (1 at R = 16, 4 at R = 32)
+  constexpr int kCh = 64;                          // rows of C / Y staged per chunk
+  __shared__ float4 Cs[kCh * R / 4], Ys[kCh * R / 4];
+  __shared__ double M[R][R + 1];
+  __shared__ double dg[R];
+  __shared__ float Ri[R][R];
+  // M = C^T Y: fp32 products, fp64 accumulation, over staged 64-row chunks
+  double acc[kE];
+#pragma unroll
+  for (int q = 0; q < kE; ++q) acc[q] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += kCh) {
+    const int nk = min(kCh, K - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nk * R / 4; e += 256) {
+      Cs[e] = reinterpret_cast<const float4*>(C + static_cast<size_t>(k0) * R)[e];
+      Ys[e] = reinterpret_cast<const float4*>(Y + static_cast<size_t>(k0) * R)[e];
+    }
+    __syncthreads();
+    const float* cs = reinterpret_cast<const float*>(Cs);
+    const float* ys = reinterpret_cast<const float*>(Ys);
+#pragma unroll
+    for (int q = 0; q < kE; ++q) {
+      const int e = threadIdx.x + 256 * q, a = e / R, c = e % R;
+      double s = 0.0;
+      for (int k = 0; k < nk; ++k) s += static_cast<double>(cs[k * R + a] * ys[k * R + c]);
+      acc[q] += s;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    const int e = threadIdx.x + 256 * q;
+    M[e / R][e % R] = acc[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int j = lane; j < R; j += 32) dg[j] = M[j][j];
+    __syncwarp();
+    // symmetrize (M = C^T G C is symmetric in exact arithmetic), then L L^T = M in place (lower)
+    for (int e = lane; e < R * R; e += 32) {
+      const int a = e / R, c = e % R;
+      if (a > c) M[a][c] = 0.5 * (M[a][c] + M[c][a]);
+    }
+    __syncwarp();
+    for (int j = 0; j < R; ++j) {
+      if (lane == 0) {
+        double s = M[j][j];
+        for (int k = 0; k < j; ++k) s -= M[j][k] * M[j][k];
+        if (!(s > static_cast<double>(kJdCollapse) * dg[j])) s = dg[j] > 0.0 ? dg[j] : 1.0;
+        M[j][j] = sqrt(s);
+      }
+      __syncwarp();
+      for (int i = j + 1 + lane; i < R; i += 32) {
+        double t = M[i][j];
+        for (int k = 0; k < j; ++k) t -= M[i][k] * M[j][k];
+        M[i][j] = t / M[j][j];
+      }
+      __syncwarp();
+    }
+    // Rinv = (L^T)^-1 (upper): lane c solves L^T x = e_c, back substitution in place in column c
+    for (int c = lane; c < R; c += 32) {
+#pragma unroll 1
+      for (int i = R - 1; i >= 0; --i) {
+        double t = i == c ? 1.0 : 0.0;
+        for (int k = i + 1; k <= c; ++k) t -= M[k][i] * static_cast<double>(Ri[k][c]);
+        Ri[i][c] = i <= c ? static_cast<float>(t / M[i][i]) : 0.f;
+      }
+    }
+  }
+  __syncthreads();
+  // C <- C Rinv, Y <- Y Rinv: thread = row, one matrix at a time (fewer live registers)
+  for (int mat = 0; mat < 2; ++mat) {
+    float* src = mat == 0 ? C : const_cast<float*>(Y);
+    float* dst = mat == 0 ? C : Yout;
+    for (int k = threadIdx.x; k < K; k += 256) {
+      float x[R];
+#pragma unroll
+      for (int c4 = 0; c4 < R / 4; ++c4) {
+        const float4 v = reinterpret_cast<const float4*>(src + static_cast<size_t>(k) * R)[c4];
+        x[4 * c4] = v.x; x[4 * c4 + 1] = v.y; x[4 * c4 + 2] = v.z; x[4 * c4 + 3] = v.w;
+      }
+#pragma unroll
+      for (int c4 = 0; c4 < R / 4; ++c4) {
+        float o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = 4 * c4 + u;
+          float s = 0.f;
+#pragma unroll
+          for (int a = 0; a <= c; ++a) s = fmaf(x[a], Ri[a][c], s);
+          o[u] = s;
+        }
+        reinterpret_cast<float4*>(dst + static_cast<size_t>(k) * R)[c4] = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  }
+}
+
+}  // namespace cts

@@ -31,14 +31,15 @@ namespace cts {
 
 struct JdTcJob {
   const CUtensorMap* tm_x;     // X [M][Kd] fp32, box {32, 128}, 128B swizzle
-  const CUtensorMap* tm_y;     // Y [R][Kd] fp32, box {32, R}, 128B swizzle
-  float* D;                    // [M][R]
+  const CUtensorMap* tm_y;     // Y [N][Kd] fp32, box {32, R}, 128B swizzle
+  float* D;                    // [M][ldD]
   int M, Kd;
+  int N, ldD;                  // rows of Y (columns of D); thin GEMMs: N = ldD = R
 };
 
 struct JdTcParams {
   const JdTcJob* jobs;
-  const int2* tiles;           // (job, first row)
+  const int4* tiles;           // (job, first row of X, first row of Y = first column of D, mirror)
   int n_tiles;
 };
 
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(320, 1) jd_tc_gemm(const __grid_constant__ JdT
   if (warp == 0) {                                          // ---------------- TMA producer
     int it = 0;
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-      const int2 tl = p.tiles[t];
+      const int4 tl = p.tiles[t];
       const JdTcJob& j = p.jobs[tl.x];
       const int nkb = (j.Kd + 31) / 32;
       for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(320, 1) jd_tc_gemm(const __grid_constant__ JdT
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], L::kX + L::kY);
           tma_load_2d(stage_x(s), j.tm_x, &full[s], kb * 32, tl.y);
-          tma_load_2d(stage_y(s), j.tm_y, &full[s], kb * 32, 0);
+          tma_load_2d(stage_y(s), j.tm_y, &full[s], kb * 32, tl.z);
         }
         __syncwarp();
       }
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(320, 1) jd_tc_gemm(const __grid_constant__ JdT
         float4* yl = reinterpret_cast<float4*>(stage_ylo(s));
         for (int i = tid; i < L::kY / 16; i += 128) {
           const float4 v = y[i], h = tf32_hi(v);
-          y[i] = h;
+          if (CTS_JD_HI_INPLACE) y[i] = h;                  // else the MMA's own tf32 read of y
           yl[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
         }
         fence_proxy_async_smem();                           // generic writes -> tensor-core reads
@@ -206,30 +207,47 @@ __global__ void __launch_bounds__(320, 1) jd_tc_gemm(const __grid_constant__ JdT
     const int row = quarter * 32 + lane;
     int tile_i = 0;
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++tile_i) {
-      const int2 tl = p.tiles[t];
+      const int4 tl = p.tiles[t];
       const JdTcJob& j = p.jobs[tl.x];
       const int slot = tile_i & 1;
       mbar_wait(&acc_full[slot], (tile_i >> 1) & 1);
       tc_fence_after();
-      float v[R], w[R];
       const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + slot * 2 * R;
+      const int m = tl.y + row;
+      const int ncols = min(R, j.N - tl.z);                 // Gram tiles: the last column block is partial
+      float* drow = j.D + static_cast<size_t>(m) * j.ldD + tl.z;
+      constexpr int kC = R < 32 ? R : 32;                   // accumulator columns per TMEM load
+#pragma unroll 1
+      for (int c0 = 0; c0 < R; c0 += kC) {
+        float v[kC], w[kC];
 #pragma unroll
-      for (int c = 0; c < R; c += 16) {
-        tmem_ld16(ta + c, v + c);
-        tmem_ld16(ta + R + c, w + c);
+        for (int c = 0; c < kC; c += 16) {
+          tmem_ld16(ta + c0 + c, v + c);
+          tmem_ld16(ta + R + c0 + c, w + c);
+        }
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < kC; ++c) v[c] += w[c];          // X_hi Y_hi + X_lo Y_hi  +  X_hi Y_lo
+        if (m < j.M) {
+          if (c0 + kC <= ncols && (j.ldD & 3) == 0) {
+            float4* dst = reinterpret_cast<float4*>(drow + c0);
+#pragma unroll
+            for (int c = 0; c < kC / 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < kC; ++c)
+              if (c0 + c < ncols) drow[c0 + c] = v[c];
+          }
+          if (tl.w) {                                       // symmetric Gram: the mirrored tile too
+#pragma unroll
+            for (int c = 0; c < kC; ++c)                    // lanes = consecutive m: coalesced
+              if (c0 + c < ncols) j.D[static_cast<size_t>(tl.z + c0 + c) * j.ldD + m] = v[c];
+          }
+        }
       }
-      tmem_ld_wait();
-#pragma unroll
-      for (int c = 0; c < R; ++c) v[c] += w[c];             // X_hi Y_hi + X_lo Y_hi  +  X_hi Y_lo
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[slot]);
-      const int m = tl.y + row;
-      if (m < j.M) {
-        float4* dst = reinterpret_cast<float4*>(j.D + static_cast<size_t>(m) * R);
-#pragma unroll
-        for (int c = 0; c < R / 4; ++c) dst[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-      }
     }
   }
   __syncthreads();

@@ -40,7 +40,7 @@ torch.cuda.synchronize()
 ws = cts.cts_jd_eigen_iteration(problems, r, iters)     # warm-up (allocations, kernel attributes, pools)
 torch.cuda.synchronize()
 runs = []
-for rep in range(3):                                     # each from fresh random bases; median reported
+for rep in range(5):                                     # each from fresh random bases; median reported
     for q in problems:
         q["U"].copy_(ortho(q["U"].shape[0]))
         q["V"].copy_(ortho(q["V"].shape[0]))
@@ -52,9 +52,9 @@ for rep in range(3):                                     # each from fresh rando
     b.record()
     b.synchronize()
     runs.append(a.elapsed_time(b))
-ms = sorted(runs)[1]
+ms = sorted(runs)[len(runs) // 2]
 cap = sum(float((q["sigma"] ** 2).sum()) for q in problems)
 tot = sum(float(e) for e in energy)
 print(f"{len(problems)} problems (7 modules x {C} clusters x {per} LoRAs, r_i={ri}, r={r}), {iters} iterations: "
-      f"{ms:.1f} ms on the GPU, median of 3 ({', '.join(f'{x:.1f}' for x in runs)}; {ms / len(problems):.3f} ms "
+      f"{ms:.1f} ms on the GPU, median of {len(runs)} ({', '.join(f'{x:.1f}' for x in runs)}; {ms / len(problems):.3f} ms "
       f"per cluster); captured energy {cap / tot:.4f}; wall {time.perf_counter() - t0:.2f} s")
