@@ -124,30 +124,48 @@ __global__ void __launch_bounds__(256, 2) jd_gorth(const __grid_constant__ JdBat
   float* Yout = last ? (side == 0 ? p.P : p.Q) : (side == 0 ? p.Ya : p.Yb);
   constexpr int kE = R * R / 256;                  // M entries per thread (1 at R = 16, 4 at R = 32)
   constexpr int kCh = 64;                          // rows of C / Y staged per chunk
+  constexpr int kV = kCh * R / 4 / 256;            // float4 of C (and of Y) per thread per chunk
   __shared__ float4 Cs[kCh * R / 4], Ys[kCh * R / 4];
   __shared__ double M[R][R + 1];
   __shared__ double dg[R];
   __shared__ float Ri[R][R];
-  // M = C^T Y: fp32 products, fp64 accumulation, over staged 64-row chunks
+  // M = C^T Y: fp32 products, fp64 accumulation, over staged 64-row chunks; the next chunk is
+  // loaded into registers while the current one is reduced
+  float4 cr[kV], yr[kV];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+      const int e = threadIdx.x + 256 * j;
+      const bool in = k0 + e / (R / 4) < K;
+      cr[j] = in ? reinterpret_cast<const float4*>(C + static_cast<size_t>(k0) * R)[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+      yr[j] = in ? reinterpret_cast<const float4*>(Y + static_cast<size_t>(k0) * R)[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
   double acc[kE];
 #pragma unroll
   for (int q = 0; q < kE; ++q) acc[q] = 0.0;
+  load(0);
   for (int k0 = 0; k0 < K; k0 += kCh) {
-    const int nk = min(kCh, K - k0);
     __syncthreads();
-    for (int e = threadIdx.x; e < nk * R / 4; e += 256) {
-      Cs[e] = reinterpret_cast<const float4*>(C + static_cast<size_t>(k0) * R)[e];
-      Ys[e] = reinterpret_cast<const float4*>(Y + static_cast<size_t>(k0) * R)[e];
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+      Cs[threadIdx.x + 256 * j] = cr[j];
+      Ys[threadIdx.x + 256 * j] = yr[j];
     }
     __syncthreads();
+    if (k0 + kCh < K) load(k0 + kCh);
     const float* cs = reinterpret_cast<const float*>(Cs);
     const float* ys = reinterpret_cast<const float*>(Ys);
 #pragma unroll
     for (int q = 0; q < kE; ++q) {
       const int e = threadIdx.x + 256 * q, a = e / R, c = e % R;
-      double s = 0.0;
-      for (int k = 0; k < nk; ++k) s += static_cast<double>(cs[k * R + a] * ys[k * R + c]);
-      acc[q] += s;
+      double s0 = 0.0, s1 = 0.0;                   // two chains (rows are zero-filled past K)
+#pragma unroll 8
+      for (int k = 0; k < kCh; k += 2) {
+        s0 += static_cast<double>(cs[k * R + a] * ys[k * R + c]);
+        s1 += static_cast<double>(cs[(k + 1) * R + a] * ys[(k + 1) * R + c]);
+      }
+      acc[q] += s0 + s1;
     }
   }
 #pragma unroll
