@@ -309,7 +309,9 @@ __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_la
   uint32_t phase = 0, aphase = 0;
   for (int li = 0; li < n_items; ++li) {
     mbar_wait(&R.acc_empty[slot], aphase ^ 1);
+    if (lane == 0 && li >= 1 && li <= 3) CTS_STAMP(27 + 4 * (li - 1));   // MMA: accumulator free
     mbar_wait(&R.full[stage], phase);
+    if (lane == 0 && li >= 1 && li <= 3) CTS_STAMP(36 + (li - 1));       // MMA: operands (t) landed
     tc_fence_after();
     if (lane == 0) {
       const uint32_t acc = R.tmem + slot * L::kSlotCols;
@@ -346,6 +348,7 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
     const int stage = my % L::kStages, slot = my % kExpandAccSlots;
     const uint32_t phase = (my / L::kStages) & 1, aphase = (my / kExpandAccSlots) & 1;
     mbar_wait(&R.acc_full[slot], aphase);
+    if (warp == kEpiWarp0 && lane == 0 && my >= 1 && my <= 3) CTS_STAMP(24 + 4 * (my - 1));   // acc ready
     mbar_wait(&R.full[stage], phase);            // y rows + metadata landed (acquire for this thread)
     tc_fence_after();
     const int4 info = stage_info<RP>(R, stage)[0];    // (g, cluster0, nb, len0)
@@ -365,6 +368,7 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
         tmem_ld32(taddr, v);
         tmem_ld32(taddr + 32, v + 32);
         tmem_ld_wait();
+        if (warp == kEpiWarp0 && lane == 0 && my >= 1 && my <= 3) CTS_STAMP(25 + 4 * (my - 1));   // TMEM read
         // rows len..len4 duplicate the last token (identical bytes for the 4-row scatter); the
         // direct variant stores real rows only
         constexpr bool DIRECT = STORE == kStoreDirect;
@@ -406,6 +410,7 @@ __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int 
         }
       }
     }
+    if (warp == kEpiWarp0 && lane == 0 && my >= 1 && my <= 3) CTS_STAMP(26 + 4 * (my - 1));     // stores issued
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&R.acc_empty[slot]);

@@ -340,7 +340,7 @@ __device__ __forceinline__ void nanosleep_ns(uint32_t ns) { asm volatile("nanosl
 
 // ------------------------------------------------------------------ debug timeline (off unless traced)
 // A kernel built with CTS_TRACE records %globaltimer stamps per CTA into g_cts_trace[cta][slot].
-constexpr int kTraceSlots = 24;
+constexpr int kTraceSlots = 40;
 constexpr int kTraceCtas = 160;
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;

@@ -31,9 +31,9 @@ for grp in ([0], [0, 1, 2]):
         big.zero_()                         # flush L2 so y comes from HBM
         plan.expand_group(grp, [ys[m] for m in grp])
         torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (160 * 24))()
-    L.cts_debug_trace(buf, 160 * 24)
-    a = np.array(buf, dtype=np.int64).reshape(160, 24)[:148].astype(np.float64)
+    buf = (ctypes.c_ulonglong * (160 * 40))()
+    L.cts_debug_trace(buf, 160 * 40)
+    a = np.array(buf, dtype=np.int64).reshape(160, 40)[:148].astype(np.float64)
     t0 = a[:, 0].min()
     rel = (a - t0) / 1e3
     print(f"expand group {grp}: us after first CTA start: min / median / max over CTAs")

@@ -33,14 +33,19 @@ names = {0: "start", 1: "prologue+wait", 2: "shrink first TMA", 3: "shrink produ
          15: "finisher: flag published", 16: "shrink: first item mapped", 17: "shrink: expect_tx armed",
          18: "shrink: first gathers issued", 19: "shrink: first acc ready", 20: "expand item 0 epi done",
          21: "expand item 1 epi done", 22: "expand item 2 epi done", 23: "expand item 3 epi done"}
+for k in range(3):   # expand items 1..3: epilogue acc ready, TMEM read, stores issued; MMA accumulator free
+    names.update({24 + 4 * k: f"item {k + 1}: epi acc ready", 25 + 4 * k: f"item {k + 1}: epi TMEM read",
+                  26 + 4 * k: f"item {k + 1}: epi stores issued", 27 + 4 * k: f"item {k + 1}: MMA acc free",
+                  36 + k: f"item {k + 1}: MMA operands landed"})
+NS = 40
 for grp in (([0],) if os.environ.get("QONLY") else ([0, 1, 2], [3, 4])):
     for rep in range(3):
         big.zero_()
         plan.apply_group(grp, [x] * len(grp), [ys[m] for m in grp], 2.0)
         torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (160 * 24))()
-    L.cts_debug_trace(buf, 160 * 24)
-    a = np.array(buf, dtype=np.int64).reshape(160, 24)[:148].astype(np.float64)
+    buf = (ctypes.c_ulonglong * (160 * NS))()
+    L.cts_debug_trace(buf, 160 * NS)
+    a = np.array(buf, dtype=np.int64).reshape(160, NS)[:148].astype(np.float64)
     a = a[a[:, 0] > 0]                                 # CTAs of this launch (grid may be < 148)
     t0 = a[:, 0].min()
     rel = (a - t0) / 1e3

@@ -38,9 +38,9 @@ for name, gm in groups.items():
         big.zero_()
         plan.apply_group(gm, [xs[name]] * len(gm), [ys[m] for m in gm], 2.0)
         torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (160 * 24))()
-    L.cts_debug_trace(buf, 160 * 24)
-    a = np.array(buf, dtype=np.int64).reshape(160, 24)[:148].astype(np.float64)
+    buf = (ctypes.c_ulonglong * (160 * 40))()
+    L.cts_debug_trace(buf, 160 * 40)
+    a = np.array(buf, dtype=np.int64).reshape(160, 40)[:148].astype(np.float64)
     a = a[a[:, 0] > 0]
     t0 = a[:, 0].min()
     rel = (a - t0) / 1e3
