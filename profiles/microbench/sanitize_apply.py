@@ -79,21 +79,26 @@ def run_diag_and_pagein():
 def run_jd():
     """GPU compression: tensor-core path (K multiple of 4) and CUDA-core fallback in one batch each."""
     g = torch.Generator(device=dev).manual_seed(0)
-    for (n, ri) in ((6, 16), (3, 6)):
+    # (6, 16) and (21, 16): K-space iterations (K = 96, 336: partial and mirrored Gram tiles);
+    # (3, 6): CUDA-core fallback; r = 32 with K = 96: K-space at r_pad 32
+    for (n, ri, r) in ((6, 16, 16), (21, 16, 16), (3, 6, 16), (6, 16, 32)):
         d_in, d_out = 256, 192
         prob = {"a_stack": torch.randn(n * ri, d_in, generator=g, device=dev) / 16,
                 "bt_stack": torch.randn(n * ri, d_out, generator=g, device=dev) / 4,
-                "U": torch.linalg.qr(torch.randn(d_out, 16, generator=g, device=dev))[0].contiguous(),
-                "V": torch.linalg.qr(torch.randn(d_in, 16, generator=g, device=dev))[0].contiguous(),
-                "sigma": torch.empty(n, 16, 16, device=dev)}
-        ws = cts.cts_jd_eigen_iteration([prob], 16, 3)
+                "U": torch.linalg.qr(torch.randn(d_out, r, generator=g, device=dev))[0].contiguous(),
+                "V": torch.linalg.qr(torch.randn(d_in, r, generator=g, device=dev))[0].contiguous(),
+                "sigma": torch.empty(n, r, r, device=dev)}
+        ws = cts.cts_jd_eigen_iteration([prob], r, 3)
         torch.cuda.synchronize()
         del ws
-    print("GPU compression (tensor-core + CUDA-core paths): ok", flush=True)
+    print("GPU compression (K-space, tensor-core d-space and CUDA-core paths): ok", flush=True)
 
 
-run_diag_and_pagein()
+if not os.environ.get("JD_ONLY"):
+    run_diag_and_pagein()
 run_jd()
+if os.environ.get("JD_ONLY"):
+    sys.exit(0)
 run("tiny r=4 (r_pad 16)", [(64, 64)], N=4, C=1, r=4, T=32)
 run("decode-like r=16, 3 modules grouped", [(1024, 1024), (1024, 256), (1024, 256)], N=100, C=5, r=16, T=200,
     groups=[[0, 1, 2]])
