@@ -643,20 +643,21 @@ size_t jd_problem_floats(const cts_jd_problem_t& q, int r) {
 }
 
 // One batch's tensor-core tables (maps, jobs, tile lists, transpose jobs) in one device block.
-// Groups 0-3: the thin GEMMs; group 4 (K-space path only): the Grams G_A = A A^T, G_B = Bt Bt^T.
+// Groups 0-3: the thin GEMMs; K-space path only: group 4 the Grams G_A = A A^T, G_B = Bt Bt^T,
+// group 5 the per-iteration products Y_A = G_A Z, Y_B = G_B W (X = G, Y = Z^T / W^T).
 struct JdTcTables {
   std::vector<uint8_t> host;
   void* dev = nullptr;
-  size_t off_jobs[5] = {}, off_tiles[5] = {}, off_tr[3] = {};
-  int n_tiles[5] = {}, n_tr[3] = {};
+  size_t off_jobs[6] = {}, off_tiles[6] = {}, off_tr[3] = {};
+  int n_tiles[6] = {}, n_tr[3] = {};
 };
 
 template <int R>
 cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, bool gram, JdTcTables& T, cudaStream_t stream) {
   const int n = jb.count;
   // per problem: maps 0..7 = X: A, Bt, A^T, Bt^T; Y: V^T, U^T, W^T, Z^T
-  std::vector<CUtensorMap> maps(size_t(n) * 8);
-  std::vector<int4> tiles[5];
+  std::vector<CUtensorMap> maps(size_t(n) * 10);
+  std::vector<int4> tiles[6];
   std::vector<JdTransposeJob> tr[3];
   for (int i = 0; i < n; ++i) {
     const JdProblem& p = jb.pr[i];
@@ -667,11 +668,13 @@ cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, bool gram, 
     float* ut = vt + size_t(R) * p.d_in;
     float* wt = ut + size_t(R) * p.d_out;
     float* zt = wt + size_t(R) * K;
-    CUtensorMap* m = &maps[size_t(i) * 8];
+    CUtensorMap* m = &maps[size_t(i) * 10];
     if (!make_tmap_f32(&m[0], p.a, p.d_in, K, 32, 128) || !make_tmap_f32(&m[1], p.bt, p.d_out, K, 32, 128) ||
         !make_tmap_f32(&m[2], at, K, p.d_in, 32, 128) || !make_tmap_f32(&m[3], btt, K, p.d_out, 32, 128) ||
         !make_tmap_f32(&m[4], vt, p.d_in, R, 32, R) || !make_tmap_f32(&m[5], ut, p.d_out, R, 32, R) ||
         !make_tmap_f32(&m[6], wt, K, R, 32, R) || !make_tmap_f32(&m[7], zt, K, R, 32, R))
+      return CTS_ERR_CUDA;
+    if (gram && (!make_tmap_f32(&m[8], p.Ga, K, K, 32, 128) || !make_tmap_f32(&m[9], p.Gb, K, K, 32, 128)))
       return CTS_ERR_CUDA;
     const int rowsP = (K + 127) / 128, rowsU = (p.d_out + 127) / 128, rowsV = (p.d_in + 127) / 128;
     for (int t = 0; t < rowsP; ++t) tiles[0].push_back(make_int4(i, t * 128, 0, 0));   // P = A V
@@ -683,6 +686,9 @@ cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, bool gram, 
         for (int a = 0; a < rowsP; ++a)
           for (int c = a; c < rowsP; ++c)   // G symmetric: upper tiles, each off-diagonal one mirrored
             tiles[4].push_back(make_int4(2 * i + side, a * 128, c * 128, c > a ? 1 : 0));
+    if (gram)                                                                          // G_A Z, G_B W tiles
+      for (int side = 0; side < 2; ++side)
+        for (int t = 0; t < rowsP; ++t) tiles[5].push_back(make_int4(2 * i + side, t * 128, 0, 0));
     tr[0].push_back({p.a, at, K, p.d_in});
     tr[0].push_back({p.bt, btt, K, p.d_out});
     tr[1].push_back({p.V, vt, p.d_in, R});
@@ -692,8 +698,8 @@ cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, bool gram, 
   }
   auto al = [](size_t v) { return (v + 127) / 128 * 128; };
   size_t off = al(maps.size() * sizeof(CUtensorMap));
-  for (int g = 0; g < 5; ++g) { T.off_jobs[g] = off; off = al(off + size_t(g == 4 ? 2 * n : n) * sizeof(JdTcJob)); }
-  for (int g = 0; g < 5; ++g) {
+  for (int g = 0; g < 6; ++g) { T.off_jobs[g] = off; off = al(off + size_t(g >= 4 ? 2 * n : n) * sizeof(JdTcJob)); }
+  for (int g = 0; g < 6; ++g) {
     T.off_tiles[g] = off;
     T.n_tiles[g] = int(tiles[g].size());
     off = al(off + tiles[g].size() * sizeof(int4));
@@ -711,16 +717,18 @@ cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, bool gram, 
   for (int i = 0; i < n; ++i) {
     const JdProblem& p = jb.pr[i];
     const int K = p.n * p.ri;
-    const CUtensorMap* m = dmaps + size_t(i) * 8;
+    const CUtensorMap* m = dmaps + size_t(i) * 10;
     const JdTcJob jobs[4] = {{m + 0, m + 4, p.P, K, p.d_in, R, R}, {m + 1, m + 5, p.Q, K, p.d_out, R, R},
                              {m + 3, m + 6, p.U0, p.d_out, K, R, R}, {m + 2, m + 7, p.V0, p.d_in, K, R, R}};
     for (int g = 0; g < 4; ++g) std::memcpy(T.host.data() + T.off_jobs[g] + i * sizeof(JdTcJob), &jobs[g], sizeof(JdTcJob));
     if (gram) {   // X = Y = the stack (box {32, 128} serves both operands)
       const JdTcJob gj[2] = {{m + 0, m + 0, p.Ga, K, p.d_in, K, K}, {m + 1, m + 1, p.Gb, K, p.d_out, K, K}};
       std::memcpy(T.host.data() + T.off_jobs[4] + 2 * i * sizeof(JdTcJob), gj, sizeof(gj));
+      const JdTcJob yj[2] = {{m + 8, m + 7, p.Ya, K, K, R, R}, {m + 9, m + 6, p.Yb, K, K, R, R}};
+      std::memcpy(T.host.data() + T.off_jobs[5] + 2 * i * sizeof(JdTcJob), yj, sizeof(yj));
     }
   }
-  for (int g = 0; g < 5; ++g) std::memcpy(T.host.data() + T.off_tiles[g], tiles[g].data(), tiles[g].size() * sizeof(int4));
+  for (int g = 0; g < 6; ++g) std::memcpy(T.host.data() + T.off_tiles[g], tiles[g].data(), tiles[g].size() * sizeof(int4));
   for (int g = 0; g < 3; ++g) std::memcpy(T.host.data() + T.off_tr[g], tr[g].data(), tr[g].size() * sizeof(JdTransposeJob));
   if (cudaMemcpyAsync(T.dev, T.host.data(), off, cudaMemcpyHostToDevice, stream) != cudaSuccess) return CTS_ERR_CUDA;
   return CTS_OK;
@@ -817,13 +825,14 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
             gp.tiles = reinterpret_cast<const int4*>(dv + T.off_tiles[4]);
             gp.n_tiles = T.n_tiles[4];
             jd_tc_gemm<128><<<std::min(sm_count(), std::max(1, T.n_tiles[4])), 320, JdTcCfg<128>::kBytes, stream>>>(gp);
-            const dim3 g_gm((kmax + JdGm<R>::kRows - 1) / JdGm<R>::kRows, 2, jb.count), g_go(2, jb.count);
+            const dim3 g_go(2, jb.count);
             for (; it0 < iters - 1; ++it0) {
               jd_small<R><<<g_small, 256, small_smem, stream>>>(jb);
               for (int pass = 0; pass < 2; ++pass) {
                 if (pass == 0 || tuning().jd_ks_recompute) {   // pass 2: G C recomputed, or Y R1^-1 reused
-                  jd_gmul<R><<<g_gm, 256, 0, stream>>>(jb);
-                  g_launches.fetch_add(1, std::memory_order_relaxed);
+                  transpose(2);              // C^T (W^T, Z^T), then Y = G C on the tensor cores
+                  gemm(5);
+                  g_launches.fetch_add(2, std::memory_order_relaxed);
                 }
                 jd_gorth<R><<<g_go, 256, 0, stream>>>(jb, pass);
               }

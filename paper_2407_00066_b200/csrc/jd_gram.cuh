@@ -11,7 +11,8 @@
 //     V' = A^T C_V,  C_V = Z R^-1,  and the next  P' = A V' = G_A C_V.
 // The same holds for U' with G_B = Bt Bt^T and C_U = W R_U^-1, Q' = G_B C_U.  So after ONE pass
 // that forms G_A and G_B on the tensor cores (jd_tc_gemm<128>, 3xTF32), every further iteration is
-// K x K x r work on data that never leaves L2-sized buffers; only the last iteration returns to the
+// K x K x r work: Y = G C as a thin tensor-core GEMM (jd_tc_gemm<R>, X = G, Y = C^T from the batched
+// transpose), then the r x r orthogonalization below; only the last iteration returns to the
 // d-space (explicit U0 = Bt^T W, V0 = A^T Z, Cholesky-QR2 with the collapse completion, then P, Q and
 // Sigma) -- the same iterates in exact arithmetic, a different rounding.  As in the d-space path the
 // orthogonalization is applied twice (Cholesky-QR2: the second pass recomputes G C from the updated
@@ -27,87 +28,6 @@
 namespace cts {
 
 constexpr int kJdGramMaxK = 1024;
-
-// Y[K][R] = G[K][K] C[K][R] for side s (blockIdx.y: 0 = A side (G_A, C = Z), 1 = B side (G_B,
-// C = W)); blockIdx.z = problem.  Thread = 4 rows x 4 columns (16 FMAs per two 16-byte shared
-// loads).  G is symmetric, so the block's [K chunk][rows] operand is read straight from the rows
-// k of G (coalesced), no transpose; the next chunk is held in registers while the current one is
-// multiplied.
-template <int R>
-struct JdGm {
-  static constexpr int kCG = R / 4;                 // column groups
-  static constexpr int kRG = 256 / kCG;             // row groups
-  static constexpr int kRows = 4 * kRG;             // rows per block: 256 (R = 16) / 128 (R = 32)
-  static constexpr int kK = 32;                     // K chunk
-  static constexpr int kG4 = kK * kRows / 4 / 256;  // float4 of G per thread per chunk
-  static constexpr int kC4 = kK * R / 4;            // float4 of C per chunk
-};
-
-template <int R>
-__global__ void __launch_bounds__(256) jd_gmul(const __grid_constant__ JdBatch b) {
-  using L = JdGm<R>;
-  const JdProblem& p = b.pr[blockIdx.z];
-  const int K = p.n * p.ri;
-  const int row0 = blockIdx.x * L::kRows;
-  if (row0 >= K) return;
-  const float* G = blockIdx.y == 0 ? p.Ga : p.Gb;
-  const float* C = blockIdx.y == 0 ? p.Z : p.W;
-  float* Y = blockIdx.y == 0 ? p.Ya : p.Yb;
-  __shared__ float4 Gs[L::kK][L::kRows / 4];       // Gs[k][r] = G[k0 + k][row0 + r]
-  __shared__ float4 Cs[L::kK][R / 4];
-  const int cg = threadIdx.x % L::kCG, rg = threadIdx.x / L::kCG;
-  float4 gr[L::kG4], cr[(L::kC4 + 255) / 256];
-  auto load = [&](int k0) {
-#pragma unroll
-    for (int j = 0; j < L::kG4; ++j) {
-      const int e = threadIdx.x + 256 * j, k = e / (L::kRows / 4), r = 4 * (e % (L::kRows / 4));
-      gr[j] = (k0 + k < K && row0 + r < K) ? *reinterpret_cast<const float4*>(G + static_cast<size_t>(k0 + k) * K + row0 + r)
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int j = 0; j < (L::kC4 + 255) / 256; ++j) {
-      const int e = threadIdx.x + 256 * j, k = e / (R / 4);
-      cr[j] = (e < L::kC4 && k0 + k < K) ? reinterpret_cast<const float4*>(C + static_cast<size_t>(k0) * R)[e]
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  float acc[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
-  load(0);
-  for (int k0 = 0; k0 < K; k0 += L::kK) {
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < L::kG4; ++j) {
-      const int e = threadIdx.x + 256 * j;
-      Gs[e / (L::kRows / 4)][e % (L::kRows / 4)] = gr[j];
-    }
-#pragma unroll
-    for (int j = 0; j < (L::kC4 + 255) / 256; ++j) {
-      const int e = threadIdx.x + 256 * j;
-      if (e < L::kC4) Cs[e / (R / 4)][e % (R / 4)] = cr[j];
-    }
-    __syncthreads();
-    if (k0 + L::kK < K) load(k0 + L::kK);           // next chunk in flight during the FMAs
-#pragma unroll 8
-    for (int k = 0; k < L::kK; ++k) {
-      const float4 g = Gs[k][rg], c = Cs[k][cg];
-      const float gv[4] = {g.x, g.y, g.z, g.w}, cv[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[i][q] = fmaf(gv[i], cv[q], acc[i][q]);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = row0 + 4 * rg + i;
-    if (row < K)
-      reinterpret_cast<float4*>(Y + static_cast<size_t>(row) * R)[cg] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-  }
-}
 
 // One Cholesky-QR pass in the K-space for side s (blockIdx.x), problem blockIdx.y:
 //     M = C^T Y (= X^T X of the implicit X = A^T C), M = L L^T (fp64), Rinv = (L^T)^-1,
