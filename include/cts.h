@@ -277,6 +277,12 @@ cts_status_t cts_project(cts_plan_t plan, int32_t module, const void* x, int64_t
  * factor and basis pointers 16-byte aligned (else CTS_ERR_SHAPE).  workspace: device, >=
  * cts_jd_workspace_bytes(...), 16-byte aligned (CTS_ERR_SHAPE otherwise).  No normalization is
  * applied (do it on the factors beforehand, Sec. 6.1, if wanted).  Stream-ordered, deterministic.
+ * Implementation (same iterates, different rounding): when every problem of a batch has
+ * 2r <= n*r_i <= 1024 and r is 16 or 32, all iterations but the last run in the stacked-factor
+ * space through the Grams A_stack A_stack^T and Bt_stack Bt_stack^T (formed once on the tensor
+ * cores); the last iteration is the explicit one above, so U and V are orthonormal to fp32
+ * rounding.  Below 2r (a span that can collapse) every iteration is explicit, and a collapsed
+ * column is completed deterministically with standard basis vectors (as the oracle does).
  */
 typedef struct {
   const float* a_stack;
@@ -330,8 +336,9 @@ cts_status_t cts_set_exclusive_device(int32_t exclusive);
  * plans; launches recorded into a CUDA graph under stream capture count once, at capture).  The
  * difference across a call sequence is that sequence's kernel count: cts_segment = 1,
  * cts_apply / cts_apply_group = 1 (fused kernel; 2 with CTS_FUSED=0), cts_shrink* = cts_expand* = 1,
- * cts_expand_reduced_group = 2, cts_project = 2, cts_jd_eigen_iteration = 16 per iteration + 5 per
- * batch of 32 problems,
+ * cts_expand_reduced_group = 2, cts_project = 2, cts_jd_eigen_iteration per batch of up to 200
+ * problems = 5 + 13 per iteration (tensor-core path), 5 + 15 per iteration (CUDA-core path), or
+ * 5 + 3 + 5 per stacked-space iteration + 11 for the last one (stacked-space path, iters >= 2),
  * cts_bank_load = 3 per module.  Never fails. */
 uint64_t cts_launch_count(void);
 
