@@ -18,9 +18,12 @@
 // orthogonalization is applied twice (Cholesky-QR2: the second pass recomputes G C from the updated
 // C), with the r x r Gram and its Cholesky in fp64.
 //
-// Used when every problem of a batch has 2r <= K <= kJdGramMaxK (cts.cu jd_gram_ok): below 2r a
-// cluster's span can collapse (the d-space path completes it with standard basis vectors, which
-// cannot be expressed in the K-space), above kJdGramMaxK the K x K Grams outgrow their purpose.
+// Used when every problem of a batch has 2r <= K <= kJdGramMaxK (cts.cu jd_gram_ok).  A span below r
+// (duplicated or low-rank adapters) makes Cholesky pivots collapse; the standard-basis completion of
+// the d-space path cannot be expressed in the K-space, so there the collapsed directions are dropped
+// and the last, explicit iteration completes the basis (test_gpu_jd_rank_deficient_cluster
+// [kspace_duplicates]: reconstruction of every B_i A_i).  Above kJdGramMaxK the K x K Grams outgrow
+// their purpose.
 #pragma once
 #include <cstdint>
 #include "jd_eigen.cuh"
@@ -32,8 +35,9 @@ constexpr int kJdGramMaxK = 1024;
 // One Cholesky-QR pass in the K-space for side s (blockIdx.x), problem blockIdx.y:
 //     M = C^T Y (= X^T X of the implicit X = A^T C), M = L L^T (fp64), Rinv = (L^T)^-1,
 //     C <- C Rinv,  Y <- Y Rinv  (written to P / Q on the last pass: P = G_A C_V = A V').
-// A pivot below kJdCollapse of its diagonal (a collapsed direction; not expected for K >= 2r) keeps
-// the column finite (pivot clamped to its diagonal); the final d-space Cholesky-QR2 re-orthogonalizes.
+// A pivot below kJdCollapse of its diagonal (a collapsed direction: the cluster's stacked span is
+// below r, e.g. duplicated adapters) drops that column (zero in C and Y); the final d-space
+// Cholesky-QR2 completes the basis with standard basis vectors as in the d-space path.
 template <int R>
 __global__ void __launch_bounds__(256, 2) jd_gorth(const __grid_constant__ JdBatch b, int last) {
   const JdProblem& p = b.pr[blockIdx.y];
@@ -48,6 +52,7 @@ __global__ void __launch_bounds__(256, 2) jd_gorth(const __grid_constant__ JdBat
   __shared__ float4 Cs[kCh * R / 4], Ys[kCh * R / 4];
   __shared__ double M[R][R + 1];
   __shared__ double dg[R];
+  __shared__ bool drop[R];
   __shared__ float Ri[R][R];
   // M = C^T Y: fp32 products, fp64 accumulation, over staged 64-row chunks; the next chunk is
   // loaded into registers while the current one is reduced
@@ -108,14 +113,17 @@ __global__ void __launch_bounds__(256, 2) jd_gorth(const __grid_constant__ JdBat
       if (lane == 0) {
         double s = M[j][j];
         for (int k = 0; k < j; ++k) s -= M[j][k] * M[j][k];
-        if (!(s > static_cast<double>(kJdCollapse) * dg[j])) s = dg[j] > 0.0 ? dg[j] : 1.0;
-        M[j][j] = sqrt(s);
+        // a collapsed direction (already in the span of the earlier columns): DROPPED -- its column
+        // of C and Y becomes zero below, so no amplified residual enters the next iterate; the span
+        // is unchanged and the last (d-space) iteration completes the basis as the oracle does
+        drop[j] = !(s > static_cast<double>(kJdCollapse) * dg[j]);
+        M[j][j] = drop[j] ? 1.0 : sqrt(s);
       }
       __syncwarp();
       for (int i = j + 1 + lane; i < R; i += 32) {
         double t = M[i][j];
         for (int k = 0; k < j; ++k) t -= M[i][k] * M[j][k];
-        M[i][j] = t / M[j][j];
+        M[i][j] = drop[j] ? 0.0 : t / M[j][j];
       }
       __syncwarp();
     }
@@ -128,6 +136,9 @@ __global__ void __launch_bounds__(256, 2) jd_gorth(const __grid_constant__ JdBat
         Ri[i][c] = i <= c ? static_cast<float>(t / M[i][i]) : 0.f;
       }
     }
+    __syncwarp();
+    for (int e = lane; e < R * R; e += 32)          // dropped directions: zero row and column
+      if (drop[e / R] || drop[e % R]) Ri[e / R][e % R] = 0.f;
   }
   __syncthreads();
   // C <- C Rinv, Y <- Y Rinv: thread = row, one matrix at a time (fewer live registers)

@@ -811,7 +811,7 @@ def test_cluster_affinity_single_rank(cts):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["singleton", "duplicates", "ill_conditioned"])
+@pytest.mark.parametrize("case", ["singleton", "duplicates", "ill_conditioned", "kspace_duplicates"])
 def test_gpu_jd_rank_deficient_cluster(cts, case):
     """App A.2 on clusters whose stacked rank n*r_i is below r (a singleton or duplicated adapters)
     or nearly so (one adapter a 1e-4 perturbation of another): Cholesky-QR alone would return
@@ -821,7 +821,13 @@ def test_gpu_jd_rank_deficient_cluster(cts, case):
     from oracle import orthogonalize
     r, d_in, d_out = 32, 384, 256
     g = np.random.default_rng(5)
-    if case == "singleton":
+    if case == "kspace_duplicates":
+        # 8 copies of one rank-4 LoRA at r = 16: n*r_i = 32 >= 2r, so the stacked-space (Gram)
+        # iterations run although the span (rank 4) is far below r
+        r = 16
+        B1, A1, _ = gen_loras("random", d_in, d_out, 1, 4, seed=6)
+        Bs, As = [B1[0]] * 8, [A1[0]] * 8
+    elif case == "singleton":
         Bs, As, _ = gen_loras("random", d_in, d_out, 1, 16, seed=3)
     else:
         Bs, As, _ = gen_loras("random", d_in, d_out, 1, 16, seed=4)
