@@ -811,7 +811,8 @@ def test_cluster_affinity_single_rank(cts):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["singleton", "duplicates", "ill_conditioned", "kspace_duplicates"])
+@pytest.mark.parametrize("case", ["singleton", "duplicates", "ill_conditioned", "kspace_duplicates",
+                                  "kspace_ill_conditioned"])
 def test_gpu_jd_rank_deficient_cluster(cts, case):
     """App A.2 on clusters whose stacked rank n*r_i is below r (a singleton or duplicated adapters)
     or nearly so (one adapter a 1e-4 perturbation of another): Cholesky-QR alone would return
@@ -827,6 +828,13 @@ def test_gpu_jd_rank_deficient_cluster(cts, case):
         r = 16
         B1, A1, _ = gen_loras("random", d_in, d_out, 1, 4, seed=6)
         Bs, As = [B1[0]] * 8, [A1[0]] * 8
+    elif case == "kspace_ill_conditioned":
+        # 4 rank-8 LoRAs at r = 16 (n*r_i = 32 = 2r: stacked-space iterations), the second and fourth
+        # 1e-4 perturbations of the first and third: the Grams square that conditioning
+        r = 16
+        B1, A1, _ = gen_loras("random", d_in, d_out, 2, 8, seed=7)
+        Bs = [B1[0], B1[0] + 1e-4 * g.standard_normal(B1[0].shape), B1[1], B1[1] + 1e-4 * g.standard_normal(B1[1].shape)]
+        As = [A1[0], A1[0].copy(), A1[1], A1[1].copy()]
     elif case == "singleton":
         Bs, As, _ = gen_loras("random", d_in, d_out, 1, 16, seed=3)
     else:
@@ -845,7 +853,7 @@ def test_gpu_jd_rank_deficient_cluster(cts, case):
     for i, (B, A) in enumerate(zip(Bs, As)):
         BA = B.astype(np.float32).astype(np.float64) @ A.astype(np.float32).astype(np.float64)
         rel = np.linalg.norm(U @ S[i] @ V.T - BA) / np.linalg.norm(BA)
-        assert rel < (1e-3 if case == "ill_conditioned" else 2e-4), (case, i, rel)
+        assert rel < (1e-3 if "ill_conditioned" in case else 2e-4), (case, i, rel)
 
 
 @pytest.mark.parametrize("shapes,N,C,T,frac_none", [
