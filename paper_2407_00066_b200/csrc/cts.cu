@@ -648,6 +648,7 @@ size_t jd_problem_floats(const cts_jd_problem_t& q, int r) {
 struct JdTcTables {
   std::vector<uint8_t> host;
   void* dev = nullptr;
+  size_t maps_bytes = 0;                 // the tensor maps sit at offset 0 of the device block
   size_t off_jobs[6] = {}, off_tiles[6] = {}, off_tr[3] = {};
   int n_tiles[6] = {}, n_tr[3] = {};
 };
@@ -668,14 +669,6 @@ cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, bool gram, 
     float* ut = vt + size_t(R) * p.d_in;
     float* wt = ut + size_t(R) * p.d_out;
     float* zt = wt + size_t(R) * K;
-    CUtensorMap* m = &maps[size_t(i) * 10];
-    if (!make_tmap_f32(&m[0], p.a, p.d_in, K, 32, 128) || !make_tmap_f32(&m[1], p.bt, p.d_out, K, 32, 128) ||
-        !make_tmap_f32(&m[2], at, K, p.d_in, 32, 128) || !make_tmap_f32(&m[3], btt, K, p.d_out, 32, 128) ||
-        !make_tmap_f32(&m[4], vt, p.d_in, R, 32, R) || !make_tmap_f32(&m[5], ut, p.d_out, R, 32, R) ||
-        !make_tmap_f32(&m[6], wt, K, R, 32, R) || !make_tmap_f32(&m[7], zt, K, R, 32, R))
-      return CTS_ERR_CUDA;
-    if (gram && (!make_tmap_f32(&m[8], p.Ga, K, K, 32, 128) || !make_tmap_f32(&m[9], p.Gb, K, K, 32, 128)))
-      return CTS_ERR_CUDA;
     const int rowsP = (K + 127) / 128, rowsU = (p.d_out + 127) / 128, rowsV = (p.d_in + 127) / 128;
     for (int t = 0; t < rowsP; ++t) tiles[0].push_back(make_int4(i, t * 128, 0, 0));   // P = A V
     for (int t = 0; t < rowsP; ++t) tiles[1].push_back(make_int4(i, t * 128, 0, 0));   // Q = Bt U
@@ -712,7 +705,6 @@ cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, bool gram, 
   }
   T.host.assign(off, 0);
   if (cudaMallocAsync(&T.dev, off, stream) != cudaSuccess) { (void)cudaGetLastError(); return CTS_ERR_OUT_OF_MEMORY; }
-  std::memcpy(T.host.data(), maps.data(), maps.size() * sizeof(CUtensorMap));
   const CUtensorMap* dmaps = static_cast<const CUtensorMap*>(T.dev);
   for (int i = 0; i < n; ++i) {
     const JdProblem& p = jb.pr[i];
@@ -730,7 +722,42 @@ cts_status_t jd_tc_prepare(const JdBatch& jb, float* const* tc_base, bool gram, 
   }
   for (int g = 0; g < 6; ++g) std::memcpy(T.host.data() + T.off_tiles[g], tiles[g].data(), tiles[g].size() * sizeof(int4));
   for (int g = 0; g < 3; ++g) std::memcpy(T.host.data() + T.off_tr[g], tr[g].data(), tr[g].size() * sizeof(JdTransposeJob));
-  if (cudaMemcpyAsync(T.dev, T.host.data(), off, cudaMemcpyHostToDevice, stream) != cudaSuccess) return CTS_ERR_CUDA;
+  // jobs, tile lists and transpose batches now; the tensor maps (host encoding, ~1 us each) follow in
+  // jd_tc_prepare_maps while the first transposes already run on the GPU
+  T.maps_bytes = maps.size() * sizeof(CUtensorMap);
+  if (cudaMemcpyAsync(static_cast<uint8_t*>(T.dev) + T.off_jobs[0], T.host.data() + T.off_jobs[0], off - T.off_jobs[0],
+                      cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return CTS_ERR_CUDA;
+  return CTS_OK;
+}
+
+// Phase 2 of the tables: encode every problem's tensor maps (0..7 = X: A, Bt, A^T, Bt^T; Y: V^T,
+// U^T, W^T, Z^T; 8, 9 = the Grams) and copy them to the front of the device block.
+template <int R>
+cts_status_t jd_tc_prepare_maps(const JdBatch& jb, float* const* tc_base, bool gram, JdTcTables& T,
+                                cudaStream_t stream) {
+  const int n = jb.count;
+  CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(T.host.data());
+  for (int i = 0; i < n; ++i) {
+    const JdProblem& p = jb.pr[i];
+    const int K = p.n * p.ri;
+    float* at = tc_base[i];
+    float* btt = at + size_t(K) * p.d_in;
+    float* vt = btt + size_t(K) * p.d_out;
+    float* ut = vt + size_t(R) * p.d_in;
+    float* wt = ut + size_t(R) * p.d_out;
+    float* zt = wt + size_t(R) * K;
+    CUtensorMap* m = maps + size_t(i) * 10;
+    if (!make_tmap_f32(&m[0], p.a, p.d_in, K, 32, 128) || !make_tmap_f32(&m[1], p.bt, p.d_out, K, 32, 128) ||
+        !make_tmap_f32(&m[2], at, K, p.d_in, 32, 128) || !make_tmap_f32(&m[3], btt, K, p.d_out, 32, 128) ||
+        !make_tmap_f32(&m[4], vt, p.d_in, R, 32, R) || !make_tmap_f32(&m[5], ut, p.d_out, R, 32, R) ||
+        !make_tmap_f32(&m[6], wt, K, R, 32, R) || !make_tmap_f32(&m[7], zt, K, R, 32, R))
+      return CTS_ERR_CUDA;
+    if (gram && (!make_tmap_f32(&m[8], p.Ga, K, K, 32, 128) || !make_tmap_f32(&m[9], p.Gb, K, K, 32, 128)))
+      return CTS_ERR_CUDA;
+  }
+  if (cudaMemcpyAsync(T.dev, T.host.data(), T.maps_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return CTS_ERR_CUDA;
   return CTS_OK;
 }
 
@@ -813,6 +840,7 @@ cts_status_t jd_run(const cts_jd_problem_t* problems, int32_t count, int32_t ite
         };
         transpose(0);                     // A^T, Bt^T (once)
         transpose(1);                     // V^T, U^T of the initial bases
+        if ((st = jd_tc_prepare_maps<R>(jb, tc_base, gram, T, stream)) != CTS_OK) return st;
         int it0 = 0;
         if constexpr (R == 16 || R == 32) {
           if (gram) {                     // iterations 0 .. iters-2 in the K-space (jd_gram.cuh)

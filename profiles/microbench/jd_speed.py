@@ -56,5 +56,5 @@ ms = sorted(runs)[len(runs) // 2]
 cap = sum(float((q["sigma"] ** 2).sum()) for q in problems)
 tot = sum(float(e) for e in energy)
 print(f"{len(problems)} problems (7 modules x {C} clusters x {per} LoRAs, r_i={ri}, r={r}), {iters} iterations: "
-      f"{ms:.1f} ms on the GPU, median of {len(runs)} ({', '.join(f'{x:.1f}' for x in runs)}; {ms / len(problems):.3f} ms "
+      f"{ms:.1f} ms on the GPU, median of {len(runs)} (min {min(runs):.1f}; {', '.join(f'{x:.1f}' for x in runs)}; {ms / len(problems):.3f} ms "
       f"per cluster); captured energy {cap / tot:.4f}; wall {time.perf_counter() - t0:.2f} s")
