@@ -696,6 +696,35 @@ def test_gpu_jd_eigen_iteration(cts, r, dims, iters, shapes):
         assert np.allclose(U.T @ U, np.eye(r), atol=1e-5) and np.allclose(V.T @ V, np.eye(r), atol=1e-5)
 
 
+def test_gpu_jd_more_problems_than_one_batch(cts):
+    """cts_jd_eigen_iteration with 210 problems: more than one launch batch (kJdMaxBatch = 200), the
+    stacked-space path in both batches (K = 48 >= 2r); a sample of problems from each batch vs the
+    fp64 App A.2 oracle on the same factors and initial bases."""
+    from oracle import jd_eigen_iteration, orthogonalize
+    r, d_in, d_out, iters, n, ri = 16, 128, 96, 3, 3, 16
+    g = np.random.default_rng(11)
+    probs, refs = [], {}
+    for k in range(210):
+        Bs, As, _ = gen_loras("trained_like", d_in, d_out, n, ri, seed=1000 + k, n_families=2)
+        Bs = [B.astype(np.float32).astype(np.float64) for B in Bs]
+        As = [A.astype(np.float32).astype(np.float64) for A in As]
+        U0 = orthogonalize(g.standard_normal((d_out, r))).astype(np.float32).astype(np.float64)
+        V0 = orthogonalize(g.standard_normal((d_in, r))).astype(np.float32).astype(np.float64)
+        probs.append(_jd_problem(Bs, As, U0, V0))
+        if k in (0, 1, 99, 199, 200, 209):
+            refs[k] = jd_eigen_iteration(Bs, As, U0, V0, iters)
+    ws = cts.cts_jd_eigen_iteration(probs, r, iters)
+    torch.cuda.synchronize()
+    del ws
+    for k, ref in refs.items():
+        q = probs[k]
+        U, V, S = (q[key].cpu().numpy().astype(np.float64) for key in ("U", "V", "sigma"))
+        assert np.abs(U - ref["U"]).max() <= 2e-4, (k, np.abs(U - ref["U"]).max())
+        assert np.abs(V - ref["V"]).max() <= 2e-4, (k, np.abs(V - ref["V"]).max())
+        rel = np.linalg.norm(S - ref["sigma"], axis=(1, 2)) / np.linalg.norm(ref["sigma"], axis=(1, 2))
+        assert rel.max() <= 1e-4, (k, rel.max())
+
+
 # ---------------------------------------------------------------- edge cases
 def test_empty_batch_then_normal_batch(cts):
     """T = 0: segment, grouped apply and projection are no-ops (y untouched); the same plan then
