@@ -664,6 +664,8 @@ def _jd_problem(Bs, As, U0, V0):
     (32, (512, 384), 5, ((6, 16), (5, 8))),          # tensor-core path at r = 32 (K = 40 < 2r: d-space)
     (32, (512, 384), 6, ((6, 16), (4, 16), (9, 8))),  # K-space iterations at r = 32 (every K >= 2r)
     (16, (1024, 4096), 12, ((40, 16), (21, 16))),   # K-space, K = 640 / 336 (partial 128-row Gram tiles)
+    (16, (256, 192), 4, ((64, 16),)),                # K-space at its largest stack, K = 1024
+    (32, (256, 192), 4, ((64, 16),)),                # the same at r = 32
     (16, (256, 192), 5, ((3, 6),)),                  # stacked K = 18 (not a multiple of 4): CUDA-core path
 ])
 def test_gpu_jd_eigen_iteration(cts, r, dims, iters, shapes):
