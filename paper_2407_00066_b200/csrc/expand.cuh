@@ -8,15 +8,15 @@
 // of work items item = (module g, 128-row tile slot, BN-column block of d_out), laid out over the
 // host-known tile bound (empty slots skipped); a slot holds one cluster's tile or two <=64-token
 // tiles (one per 64-row half; one N = 256 MMA covers both clusters' stacked out_basis blocks):
-//   warps 0-3   TMA producers (items dealt round-robin, one warp's gather4 issue rate is not
+//   warps 0-2   TMA producers (items dealt round-robin, one warp's gather4 issue rate is not
 //               enough): t_hi / t_lo tile (A operand, K-major), the out_basis blocks (B operand,
 //               K-major) and the tile's y rows gathered by token index (tile::gather4, 64-column
 //               segments, 128B swizzle) into a kStages-deep ring.  The producer also leaves the
 //               item's token rows and slot descriptor in the stage.  In the fused kernel it first
 //               waits for the slot's "t ready" flag.
-//   warp 4      one lane issues D = t_hi U^T + t_lo U^T (M=128 tokens, N=256, K=16 per MMA) into
+//   warp 3      one lane issues D = t_hi U^T + t_lo U^T (M=128 tokens, N=256, K=16 per MMA) into
 //               one of kAccSlots TMEM accumulators.
-//   warps 5-12  epilogue: two sets of 4 warps take alternate items; in a set each warp owns one
+//   warps 4-11  epilogue: two sets of 4 warps take alternate items; in a set each warp owns one
 //               32-row quarter (its TMEM lanes).  Thread = token row: tcgen05.ld 64 fp32 columns at
 //               a time, add y_base from smem, round to bf16 (RNE), then (STORE mode)
 //                 kStoreScatter:   write back into the stage; the warp TMA-scatters its 8 four-row
@@ -193,7 +193,7 @@ template <int RP> __device__ __forceinline__ int4* stage_info(const ExpandRing& 
   return reinterpret_cast<int4*>(R.arena + ExpandCfg<RP>::kOffMeta + s * ExpandCfg<RP>::kMeta + kTileM * 4);
 }
 
-// ------------------------------------------------------------------ TMA producers (warps 0-3)
+// ------------------------------------------------------------------ TMA producers (warps 0..kProducerWarps-1)
 template <int RP>
 __device__ __forceinline__ void expand_produce(const ExpandParams& p, const ExpandRing& R, const ItemMap& M, int item,
                                                int my, int lane, int ready_target);
@@ -330,7 +330,7 @@ __device__ void expand_mma(const ExpandParams& p, const ExpandRing& R, int nt_la
   }
 }
 
-// ------------------------------------------------------------------ epilogue (warps 5-12)
+// ------------------------------------------------------------------ epilogue (warps kEpiWarp0 .. kEpiWarp0+7)
 template <int RP, int STORE>
 __device__ void expand_epilogue(const ExpandParams& p, const ExpandRing& R, int nt_lane, int warp, int lane,
                                 int deal_r0 = 0, int deal_k = 0) {

@@ -21,7 +21,7 @@
 // tokens with one adapter -- are loaded as the largest aligned {64 x 128 | 32 | 8} box; only groups
 // at run boundaries fall back to gather4.  (A slot-ordered copy of x, loaded as {64 x 128} tiles,
 // measured no better: the copy costs an extra pass over x.)
-// Persistent, one CTA per SM, 13 warps: 4 TMA producer warps (x rows as above and W0 tiles
+// Persistent, one CTA per SM, 12 warps: 3 TMA producer warps (kProducerWarps) (x rows as above and W0 tiles
 // {64 x 256} by 2-D TMA, 4-stage ring of 48 KB), 1 MMA warp (one elected
 // lane, M=128 N=256 K=16), 8 epilogue warps (set s stores columns [128 s, 128 s + 128)).  Two TMEM
 // accumulators (2 x 256 columns = all of TMEM) let the epilogue of tile i overlap the K loop of

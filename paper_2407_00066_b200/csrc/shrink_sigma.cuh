@@ -13,14 +13,14 @@
 // laid out over the host-known tile BOUND (tile slots past the real count are empty and skipped), so
 // no CTA waits on a device-side count before issuing its first load; the TMA ring keeps streaming
 // across item boundaries.
-//   warps 0-3   TMA producers: x rows gathered by token index (tile::gather4, 128B swizzle) and
+//   warps 0-2   TMA producers (kProducerWarps): x rows gathered by token index (tile::gather4, 128B swizzle) and
 //               the in_basis K-slab (tile) into a kStages-deep mbarrier ring shared by all items;
 //               K blocks are dealt round-robin to the 4 warps because one warp's gather4 issue
 //               rate caps at ~2 TB/s per GPU (measured, profiles/microbench), four reach the
 //               tile-load rate.  Token rows come from the segment kernel's per-slot row list.
-//   warp 4      one elected lane issues tcgen05.mma (M=128 tokens, N=2 r_pad, K=16) into one of
+//   warp 3      one elected lane issues tcgen05.mma (M=128 tokens, N=2 r_pad, K=16) into one of
 //               kAccSlots TMEM accumulators, commit -> acc_full[slot]
-//   warps 5-12  epilogue, two sets of 4 warps on alternate items, thread = token row (TMEM lane
+//   warps 4-11  epilogue, two sets of 4 warps on alternate items, thread = token row (TMEM lane
 //               quarter w%4): tcgen05.ld the partial s;
 //               split-K: the partial goes to an fp32 workspace, the LAST CTA to finish a tile
 //               (acq_rel per-tile arrival counter) sums the KS partials in kc order (deterministic),
@@ -44,7 +44,15 @@ __device__ unsigned long long g_cts_trace[kTraceCtas][kTraceSlots];
 
 constexpr int kBK = 64;                 // bf16 elements per K block = one 128-byte swizzle row
 constexpr int kMaxGroup = 16;           // modules per grouped launch
-constexpr int kProducerWarps = 4;
+#ifndef CTS_PRODUCER_WARPS
+// TMA producer warps.  3, not 4: with 1 MMA warp and 8 epilogue warps the CTA has 12 warps, 3 per
+// SM sub-partition, whose 16K-register files then allow 168 registers per thread instead of 128
+// (13 warps put 4 on one sub-partition) -- the r_pad 32/64 instantiations stop spilling.  Measured
+// (profiles/r02/s3/producer_warps3_ab.txt): cfg3 decode 25.70 vs 25.82 us per launch, cfg5 60.4 vs
+// 61.7, q_proj (r_pad 64) 18.5 vs 20.0, prefill unchanged.
+#define CTS_PRODUCER_WARPS 3
+#endif
+constexpr int kProducerWarps = CTS_PRODUCER_WARPS;
 constexpr int kMmaWarp = kProducerWarps;
 constexpr int kEpiWarp0 = kProducerWarps + 1;
 constexpr int kEpiSets = 2;             // epilogue warp-sets working on alternate items
@@ -226,7 +234,7 @@ __device__ __forceinline__ void shrink_init_barriers(const ShrinkRing& R) {   //
   }
 }
 
-// ------------------------------------------------------------------ TMA producers (warps 0-3)
+// ------------------------------------------------------------------ TMA producers (warps 0..kProducerWarps-1)
 // Tile metadata of a CTA's first non-empty item, loaded before griddep_wait when the segment
 // outputs are already complete (meta_ready), so the first gathers issue right after the wait
 // instead of after two dependent global loads.
@@ -493,7 +501,7 @@ __device__ __forceinline__ void store_t8(const ShrinkMod& m, int tile, int row, 
   *reinterpret_cast<uint4*>(dst + RP) = lo;
 }
 
-// ------------------------------------------------------------------ epilogue (warps 5-12)
+// ------------------------------------------------------------------ epilogue (warps kEpiWarp0 .. kEpiWarp0+7)
 // DIAG: the bank is of kind CTS_SIGMA_DIAG (a separate instantiation, so the diagonal path adds no
 // register pressure to the full-Sigma path).
 template <int RP, bool DIAG>
