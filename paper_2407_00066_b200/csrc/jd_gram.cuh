@@ -15,8 +15,8 @@
 // transpose), then the r x r orthogonalization below; only the last iteration returns to the
 // d-space (explicit U0 = Bt^T W, V0 = A^T Z, Cholesky-QR2 with the collapse completion, then P, Q and
 // Sigma) -- the same iterates in exact arithmetic, a different rounding.  As in the d-space path the
-// orthogonalization is applied twice (Cholesky-QR2: the second pass recomputes G C from the updated
-// C), with the r x r Gram and its Cholesky in fp64.
+// orthogonalization is applied twice (Cholesky-QR2); the second pass reuses Y R1^-1 for G C of the
+// updated C (CTS_JD_KS_RECOMPUTE=1 forms it again), with the r x r Gram and its Cholesky in fp64.
 //
 // Used when every problem of a batch has 2r <= K <= kJdGramMaxK (cts.cu jd_gram_ok).  A span below r
 // (duplicated or low-rank adapters) makes Cholesky pivots collapse; the standard-basis completion of
